@@ -1,0 +1,142 @@
+"""ctypes binding of ``libstokesb200.so`` (C ABI: ``include/stokesb200.h``).
+
+This is the binding a maintainer of the reference would add.
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every device entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+
+import numpy as np
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libstokesb200.so"
+
+SB_OK, SB_EINVAL, SB_EDOM, SB_ENOMEM, SB_ECUDA = 0, 22, 33, 12, 99
+KIND_CELL, KIND_FACE = 0, 1
+STATUS = {0: "converged", 1: "breakdown", 2: "maxiter"}
+
+#: every symbol declared in include/stokesb200.h (checked by the CPU tests)
+EXPORTS = (
+    "sb_create", "sb_destroy", "sb_last_error", "sb_set_coefficients", "sb_apply_M",
+    "sb_apply_A", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
+    "sb_num_levels", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
+    "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
+    "sb_launch_count", "sb_set_graphs", "sb_device_bytes",
+)
+
+
+class Smoother(C.Structure):
+    _fields_ = [("omega", C.c_double), ("sweeps_down", C.c_int), ("sweeps_up", C.c_int),
+                ("bottom_sweeps", C.c_int)]
+
+
+class Precond(C.Structure):
+    _fields_ = [("kind", C.c_int), ("velocity_cycles", C.c_int), ("schur_sign", C.c_int),
+                ("pressure_cycles", C.c_int)]
+
+
+class Gmres(C.Structure):
+    _fields_ = [("restart", C.c_int), ("max_iters", C.c_int), ("rtol", C.c_double),
+                ("atol", C.c_double), ("track_true_residual", C.c_int)]
+
+
+class HistoryRow(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("scalar_vcycles", C.c_longlong),
+                ("resid_precond", C.c_double), ("resid_true", C.c_double), ("restart", C.c_int)]
+
+
+class KernelStats(C.Structure):
+    _fields_ = [("smoother_face_ms", C.c_double), ("smoother_cell_ms", C.c_double),
+                ("smoother_face_bytes", C.c_double), ("smoother_cell_bytes", C.c_double),
+                ("smoother_face_launches", C.c_longlong), ("smoother_cell_launches", C.c_longlong),
+                ("fine_face_ms", C.c_double), ("fine_face_bytes", C.c_double),
+                ("fine_face_launches", C.c_longlong)]
+
+
+_P = C.c_void_p
+_PP = C.POINTER(C.c_void_p)
+
+_SIGS = {
+    "sb_create": (_P, [C.c_int, C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_int), C.c_int]),
+    "sb_destroy": (None, [_P]),
+    "sb_last_error": (C.c_char_p, []),
+    "sb_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
+    "sb_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),
+    "sb_apply_A": (C.c_int, [_P, _PP, _PP]),
+    "sb_apply_Lrho": (C.c_int, [_P, _P, _P]),
+    "sb_mg_solve": (C.c_int, [_P, C.c_int, C.POINTER(Smoother), C.c_int, _PP, _PP]),
+    "sb_precond_apply": (C.c_int, [_P, C.POINTER(Precond), C.POINTER(Smoother), _PP, _P, _PP, _P,
+                                   C.POINTER(C.c_longlong)]),
+    "sb_gmres_solve": (C.c_int, [_P, C.POINTER(Precond), C.POINTER(Gmres), C.POINTER(Smoother),
+                                 _PP, _P, _PP, _P, C.POINTER(HistoryRow), C.c_int,
+                                 C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
+    "sb_num_levels": (C.c_int, [_P]),
+    "sb_level_cells": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int)]),
+    "sb_get_level_coefficients": (C.c_int, [_P, C.c_int, _PP, _P, _PP, _P]),
+    "sb_smooth": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, _PP, _PP]),
+    "sb_residual_restrict": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP, _PP]),
+    "sb_prolong_add": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP]),
+    "sb_set_profiling": (None, [_P, C.c_int]),
+    "sb_get_kernel_stats": (C.c_int, [_P, C.POINTER(KernelStats)]),
+    "sb_launch_count": (C.c_longlong, [_P]),
+    "sb_set_graphs": (None, [_P, C.c_int]),
+    "sb_device_bytes": (C.c_longlong, [_P]),
+}
+
+_lib = None
+
+
+def load(path: os.PathLike | str | None = None):
+    """Load the shared library (no GPU needed just to load / inspect symbols)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = pathlib.Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()'); "
+            "there is no CPU fallback")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int):
+    """Map C-ABI status codes to the reference's exception types."""
+    if rc == SB_OK:
+        return
+    msg = (load().sb_last_error() or b"").decode()
+    if rc == SB_EINVAL:
+        raise ValueError(msg)
+    if rc == SB_EDOM:
+        raise ZeroDivisionError(msg)
+    if rc == SB_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"stokesb200 CUDA failure: {msg}")
+
+
+def ptr(a) -> int:
+    """Address of a C-contiguous float64 NumPy array or torch tensor (host or CUDA)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise TypeError("need C-contiguous float64 arrays")
+        return a.ctypes.data
+    # torch tensor (device-resident inputs for the in-HBM bench path)
+    if str(getattr(a, "dtype", "")) != "torch.float64" or not a.is_contiguous():
+        raise TypeError("need contiguous float64 tensors")
+    return a.data_ptr()
+
+
+def parr(arrs):
+    vals = [C.c_void_p(ptr(a) if a is not None else 0) for a in arrs]
+    return (C.c_void_p * max(len(vals), 1))(*vals)

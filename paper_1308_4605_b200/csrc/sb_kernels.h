@@ -1,0 +1,80 @@
+// sb_kernels.h -- host-side launchers for the sm_100a kernels (sb_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include "sb_device.cuh"
+
+namespace sb {
+
+struct Ptr3 { double* p[3]; };
+struct CPtr3 { const double* p[3]; };
+
+// Sub-box of a level: lo/hi inclusive per internal axis.
+struct Box { int lo[3], hi[3]; };
+
+// colour passes (multigrid.py:318-340)
+void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
+                        const double* rhsA, int parity, double omega);
+void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
+                        int parity, double omega);
+// two-phase variants for levels with an odd periodic extent (same-colour
+// cells couple through the wrap): compute all, then update (reference order)
+void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
+                            const double* rhsA, double* tmp, int parity, double omega);
+void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
+                            double* tmp, int parity, double omega);
+bool level_needs_two_phase(const LevelDev& L, int dim);
+// fused residual -> restriction (multigrid.py:403-406 + :177-233)
+void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
+                                int form, int A, CPtr3 u, const double* rhsA, double* coarseA);
+void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
+                                const double* phi, const double* rhs, double* coarse);
+// prolongation + add (multigrid.py:185-192, :236-295, :431-436)
+void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
+                             const double* coarseA, double* fineA);
+void launch_cell_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
+                             const double* coarse, double* fine);
+// full-level operators
+void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 u, const double* p,
+                    Ptr3 out_u, double* out_p);
+// out_A = (rhs_A - G q_A) - (A x)_A   (q or x may be null -> term dropped)
+void launch_face_residual(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 x,
+                          CPtr3 rhs, const double* q, Ptr3 out);
+void launch_cell_residual(cudaStream_t s, const LevelDev& L, int dim, const double* x,
+                          const double* rhs, double* out);  // rhs may be null -> out = L x
+// preconditioner glue (precond.py:118-152, schur.py:59-78)
+void launch_div_add(cudaStream_t s, const LevelDev& L, int dim, CPtr3 u, const double* rp, double* out);
+void launch_p1_glue(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 xu, const double* phi,
+                    const double* bc, double* xp, double sign);
+void launch_schur(cudaStream_t s, const LevelDev& L, int form, const double* r, const double* phi,
+                  double* out, double sign);
+void launch_face_sub_grad(cudaStream_t s, const LevelDev& L, int dim, CPtr3 ru, const double* q, Ptr3 out);
+// setup: coarsening (multigrid.py:112-169), inverse densities, checks
+void launch_coarsen_cellmean(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
+                             const double* fine, double* coarse);
+void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
+                         const double* fine, double* coarse);
+void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int e,
+                         const double* fine, double* coarse);
+void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag);
+void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags);
+// box utilities
+void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double v);
+void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, const double* sum,
+                           double inv_count);  // x -= sum*inv_count
+void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x);  // y += x
+
+// flat-vector kernels (GMRES; whole padded box, pads are zero)
+int reduce_blocks();
+void launch_multi_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* w,
+                      long long n, double* partials);
+void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* h,
+                       double* w, long long n, double* partials, int mode);  // mode 0: dots, 1: norm
+void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out);
+void launch_sum_partial(cudaStream_t s, const double* x, long long n, double* partials);
+void launch_scale_div(cudaStream_t s, const double* w, double d, double* out, long long n);
+void launch_combo(cudaStream_t s, double* out, const double* x, const double* V, long long vstride,
+                  int nv, const double* y, long long n);  // out = x + sum y_i V_i (y on device)
+void launch_sub(cudaStream_t s, const double* a, const double* b, double* out, long long n);  // out=a-b
+void launch_sub_norm(cudaStream_t s, const double* a, const double* b, long long n, double* partials);
+
+}  // namespace sb

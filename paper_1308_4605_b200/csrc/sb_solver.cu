@@ -1,0 +1,1236 @@
+// sb_solver.cu -- host orchestration and the C ABI (include/stokesb200.h).
+//
+// One sb_ctx per grid: it owns a CUDA stream, the device multigrid hierarchy
+// (coefficients per level, work buffers), the level-0 Krylov / preconditioner
+// vectors and the GMRES basis.  The preconditioner application P^{-1}
+// (two V-cycles plus glue, ~30 launches per level) is captured once into a
+// CUDA graph and replayed every GMRES iteration; the Arnoldi step is three
+// fused multi-vector kernels (CGS2) with one host sync per iteration for the
+// Hessenberg column.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <stdexcept>
+#include "../../include/stokesb200.h"
+#include "sb_kernels.h"
+
+namespace sb {
+extern long long g_kernel_launches;
+}
+
+using namespace sb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgErr : std::runtime_error {
+  int code;
+  ArgErr(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess)                                                          \
+      throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));               \
+  } while (0)
+
+constexpr int kMaxVec = 128;
+
+struct Level {
+  LevelDev d{};
+  int P[3]{};
+  long long block = 0;
+  bool two_phase = false;
+  double *mu_c = nullptr, *gam_c = nullptr, *mu_e[3]{}, *rho_f[3]{}, *beta_f[3]{};
+  double *fx[3]{}, *frhs[3]{}, *cx = nullptr, *crhs = nullptr, *tmp = nullptr;
+};
+
+struct ProfEv {
+  cudaEvent_t a, b;
+  int cls;       // 0 face, 1 cell
+  bool fine;
+  double bytes;
+};
+
+}  // namespace
+
+struct sb_ctx {
+  int dim = 3, form = 1, off = 0;
+  int n[3]{};         // internal cells
+  int bc[3][2]{};     // internal bcs
+  double h = 1.0;
+  cudaStream_t st = nullptr;
+  std::vector<Level> lv;
+  std::vector<void*> allocs;
+  long long bytes = 0;
+  bool have_coef = false;
+  double theta = 0.0;
+  int flag_rho = 0, flag_face = 0, flag_cell = 0;
+  std::vector<int> null_comps;  // internal axes
+  int* dflags = nullptr;
+  double* dpart = nullptr;
+  double* dsmall = nullptr;   // [h1 kMaxVec][h2 kMaxVec][misc 64][y kMaxVec]
+  double* hsmall = nullptr;   // pinned mirror
+  long long vlen = 0;         // vector length (nblk * block)
+  double *vb = nullptr, *vz0 = nullptr, *vx = nullptr, *vw = nullptr, *vMv = nullptr, *vt = nullptr;
+  double* basis = nullptr;
+  int basis_cap = 0;
+  double *sc0 = nullptr, *sc1 = nullptr, *scR = nullptr, *scC = nullptr;
+  double *sf0[3]{}, *sf1[3]{}, *sfR[3]{}, *sfC[3]{};
+  bool scratch = false, scratch_mg = false;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  long long gnodes = 0;
+  sb_precond gpc{};
+  sb_smoother gsm{};
+  bool use_graphs = true;
+  bool profiling = false;
+  std::vector<ProfEv> prof;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  long long launches_base = 0;  // g_kernel_launches at creation
+  long long graph_launches = 0; // kernel nodes replayed through graphs
+  sb_kernel_stats stats{};
+};
+
+namespace {
+
+double* dalloc(sb_ctx* c, long long n) {
+  void* p = nullptr;
+  if (n < 1) n = 1;
+  cudaError_t e = cudaMalloc(&p, (size_t)n * sizeof(double));
+  if (e != cudaSuccess) throw ArgErr(SB_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  CK(cudaMemsetAsync(p, 0, (size_t)n * sizeof(double), c->st));
+  c->allocs.push_back(p);
+  c->bytes += n * (long long)sizeof(double);
+  return (double*)p;
+}
+
+bool can_coarsen(const int* n, int dim) {
+  for (int a = 3 - dim; a < 3; ++a)
+    if (n[a] < 4 || (n[a] & 1)) return false;
+  return true;
+}
+
+void make_level(sb_ctx* c, const int* n, double h) {
+  Level L;
+  for (int a = 0; a < 3; ++a) {
+    L.d.n[a] = n[a];
+    L.d.bclo[a] = c->bc[a][0];
+    L.d.bchi[a] = c->bc[a][1];
+    L.P[a] = n[a] + (c->bc[a][0] != BC_PER ? 1 : 0);
+  }
+  L.P[2] = (L.P[2] + 3) / 4 * 4;
+  L.d.s1 = L.P[2];
+  L.d.s0 = (long long)L.P[1] * L.P[2];
+  L.block = (long long)L.P[0] * L.P[1] * L.P[2];
+  L.d.h = h;
+  L.d.inv_h = 1.0 / h;
+  L.d.inv_h2 = 1.0 / (h * h);
+  L.d.theta = 0.0;
+  L.two_phase = level_needs_two_phase(L.d, c->dim);
+  c->lv.push_back(L);
+}
+
+void alloc_level(sb_ctx* c, Level& L, bool first) {
+  const long long B = L.block;
+  L.mu_c = dalloc(c, B);
+  L.gam_c = dalloc(c, B);
+  for (int a = 3 - c->dim; a < 3; ++a) {
+    L.rho_f[a] = dalloc(c, B);
+    L.beta_f[a] = dalloc(c, B);
+  }
+  if (c->dim == 3) {
+    for (int e = 0; e < 3; ++e) L.mu_e[e] = dalloc(c, B);
+  } else {
+    L.mu_e[0] = dalloc(c, B);
+  }
+  if (!first) {
+    for (int a = 3 - c->dim; a < 3; ++a) {
+      L.fx[a] = dalloc(c, B);
+      L.frhs[a] = dalloc(c, B);
+    }
+    L.cx = dalloc(c, B);
+    L.crhs = dalloc(c, B);
+  }
+  if (L.two_phase) L.tmp = dalloc(c, B);
+  L.d.mu_c = L.mu_c;
+  L.d.gam_c = L.gam_c;
+  for (int a = 0; a < 3; ++a) {
+    L.d.mu_e[a] = L.mu_e[a];
+    L.d.rho_f[a] = L.rho_f[a];
+    L.d.beta_f[a] = L.beta_f[a];
+  }
+}
+
+// extents (internal axes) of an array kind: -1 cell, A face A, 10+e edge e
+void extents(const sb_ctx* c, const Level& L, int kind, int* ext) {
+  for (int a = 0; a < 3; ++a) ext[a] = L.d.n[a];
+  auto wall = [&](int a) { return c->bc[a][0] != BC_PER; };
+  if (kind >= 0 && kind < 3) {
+    if (wall(kind)) ext[kind] += 1;
+  } else if (kind >= 10) {
+    const int e = kind - 10;
+    for (int a = 3 - c->dim; a < 3; ++a)
+      if (a != e && wall(a)) ext[a] += 1;
+  }
+}
+
+void copy_in(sb_ctx* c, const Level& L, int kind, const double* src, double* dst) {
+  int ext[3];
+  extents(c, L, kind, ext);
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)ext[2] * 8, (size_t)ext[2], (size_t)ext[1]);
+  p.dstPtr = make_cudaPitchedPtr((void*)dst, (size_t)L.P[2] * 8, (size_t)L.P[2], (size_t)L.P[1]);
+  p.extent = make_cudaExtent((size_t)ext[2] * 8, (size_t)ext[1], (size_t)ext[0]);
+  p.kind = cudaMemcpyDefault;
+  CK(cudaMemcpy3DAsync(&p, c->st));
+}
+
+void copy_out(sb_ctx* c, const Level& L, int kind, const double* src, double* dst) {
+  int ext[3];
+  extents(c, L, kind, ext);
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)L.P[2] * 8, (size_t)L.P[2], (size_t)L.P[1]);
+  p.dstPtr = make_cudaPitchedPtr((void*)dst, (size_t)ext[2] * 8, (size_t)ext[2], (size_t)ext[1]);
+  p.extent = make_cudaExtent((size_t)ext[2] * 8, (size_t)ext[1], (size_t)ext[0]);
+  p.kind = cudaMemcpyDefault;
+  CK(cudaMemcpy3DAsync(&p, c->st));
+}
+
+// zero the wall-normal boundary faces of a face array (they are not unknowns)
+void zero_wall_faces(sb_ctx* c, const Level& L, int A, double* x) {
+  if (c->bc[A][0] == BC_PER) return;
+  Box b;
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = 0;
+    b.hi[a] = L.d.n[a] - 1;
+  }
+  b.lo[A] = b.hi[A] = 0;
+  launch_box_fill(c->st, L.d, b, x, 0.0);
+  b.lo[A] = b.hi[A] = L.d.n[A];
+  launch_box_fill(c->st, L.d, b, x, 0.0);
+}
+
+void sync(sb_ctx* c) {
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->st));
+}
+
+void ensure_scratch(sb_ctx* c) {
+  if (c->scratch) return;
+  const long long B = c->lv[0].block;
+  c->sc0 = dalloc(c, B);
+  c->sc1 = dalloc(c, B);
+  for (int a = 3 - c->dim; a < 3; ++a) {
+    c->sf0[a] = dalloc(c, B);
+    c->sf1[a] = dalloc(c, B);
+  }
+  c->scratch = true;
+}
+void ensure_scratch_mg(sb_ctx* c) {
+  if (c->scratch_mg) return;
+  const long long B = c->lv[0].block;
+  c->scR = dalloc(c, B);
+  c->scC = dalloc(c, B);
+  for (int a = 3 - c->dim; a < 3; ++a) {
+    c->sfR[a] = dalloc(c, B);
+    c->sfC[a] = dalloc(c, B);
+  }
+  c->scratch_mg = true;
+}
+void ensure_vectors(sb_ctx* c) {
+  if (c->vb) return;
+  c->vlen = (long long)(c->dim + 1) * c->lv[0].block;
+  c->vb = dalloc(c, c->vlen);
+  c->vz0 = dalloc(c, c->vlen);
+  c->vx = dalloc(c, c->vlen);
+  c->vw = dalloc(c, c->vlen);
+  c->vMv = dalloc(c, c->vlen);
+  c->vt = dalloc(c, c->vlen);
+}
+
+// vector block pointers (reference component r -> internal axis r + off)
+double* vcomp(sb_ctx* c, double* v, int A) { return v + (long long)(A - c->off) * c->lv[0].block; }
+double* vpres(sb_ctx* c, double* v) { return v + (long long)c->dim * c->lv[0].block; }
+
+void check_ready(sb_ctx* c) {
+  if (!c->have_coef) throw ArgErr(SB_EINVAL, "coefficients not set (call sb_set_coefficients)");
+}
+void check_mg(sb_ctx* c, int kind) {
+  check_ready(c);
+  if (c->lv.size() < 2) throw ArgErr(SB_EINVAL, "grid cannot be coarsened; need even counts >= 4");
+  if (kind == SB_KIND_CELL) {
+    if (c->flag_rho) throw ArgErr(SB_EINVAL, "face density must be positive");
+    if (c->flag_cell) throw ArgErr(SB_EDOM, "zero diagonal in pressure operator");
+  } else if (c->flag_face) {
+    throw ArgErr(SB_EDOM, "zero diagonal in velocity operator (theta = 0 with mu = 0 row)");
+  }
+}
+
+// ---- profiling ---------------------------------------------------------------
+
+cudaEvent_t next_event(sb_ctx* c) {
+  if (c->evnext == c->evpool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evnext++];
+}
+
+double face_pass_bytes(const sb_ctx* c, const Level& L) {
+  double per;
+  if (c->dim == 3) per = c->form == F_LAP ? 40.0 : 56.0;
+  else per = c->form == F_LAP ? 32.0 : 40.0;
+  if (c->form == F_BULK) per += 8.0;
+  if (c->theta > 0) per += 4.0;
+  return per * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+}
+double cell_pass_bytes(const sb_ctx* c, const Level& L) {
+  const double per = 16.0 + 8.0 * c->dim;
+  return per * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+}
+
+// ---- multigrid ---------------------------------------------------------------
+
+void sweep_face(sb_ctx* c, int l, double* const* x, const double* const* rhs, double omega) {
+  Level& L = c->lv[l];
+  Ptr3 u{{x[0], x[1], x[2]}};
+  for (int A = 3 - c->dim; A < 3; ++A) {
+    for (int parity = 0; parity < 2; ++parity) {
+      cudaEvent_t ea = nullptr;
+      if (c->profiling) {
+        ea = next_event(c);
+        CK(cudaEventRecord(ea, c->st));
+      }
+      if (L.two_phase) launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
+      else launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega);
+      if (c->profiling) {
+        cudaEvent_t eb = next_event(c);
+        CK(cudaEventRecord(eb, c->st));
+        c->prof.push_back({ea, eb, 0, l == 0, face_pass_bytes(c, L)});
+      }
+    }
+  }
+}
+
+void sweep_cell(sb_ctx* c, int l, double* x, const double* rhs, double omega) {
+  Level& L = c->lv[l];
+  for (int parity = 0; parity < 2; ++parity) {
+    cudaEvent_t ea = nullptr;
+    if (c->profiling) {
+      ea = next_event(c);
+      CK(cudaEventRecord(ea, c->st));
+    }
+    if (L.two_phase) launch_cell_colour_tmp(c->st, L.d, c->dim, x, rhs, L.tmp, parity, omega);
+    else launch_cell_colour(c->st, L.d, c->dim, x, rhs, parity, omega);
+    if (c->profiling) {
+      cudaEvent_t eb = next_event(c);
+      CK(cudaEventRecord(eb, c->st));
+      c->prof.push_back({ea, eb, 1, l == 0, cell_pass_bytes(c, L)});
+    }
+  }
+}
+
+// multigrid.py:409-439 -- x is written (zero initial guess)
+void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, const sb_smoother& sm) {
+  Level& L = c->lv[l];
+  for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(x[A], 0, L.block * 8, c->st));
+  const int last = (int)c->lv.size() - 1;
+  if (l == last) {
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, x, rhs, sm.omega);
+    return;
+  }
+  for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, x, rhs, sm.omega);
+  Level& Lc = c->lv[l + 1];
+  CPtr3 xc{{x[0], x[1], x[2]}};
+  for (int A = 3 - c->dim; A < 3; ++A)
+    launch_face_resid_restrict(c->st, L.d, Lc.d, c->dim, c->form, A, xc, rhs[A], Lc.frhs[A]);
+  vcycle_face(c, l + 1, Lc.frhs, Lc.fx, sm);
+  for (int A = 3 - c->dim; A < 3; ++A)
+    launch_face_prolong_add(c->st, L.d, Lc.d, c->dim, A, Lc.fx[A], x[A]);
+  for (int s = 0; s < sm.sweeps_up; ++s) sweep_face(c, l, x, rhs, sm.omega);
+}
+
+void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smoother& sm) {
+  Level& L = c->lv[l];
+  CK(cudaMemsetAsync(x, 0, L.block * 8, c->st));
+  const int last = (int)c->lv.size() - 1;
+  if (l == last) {
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, x, rhs, sm.omega);
+    return;
+  }
+  for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, x, rhs, sm.omega);
+  Level& Lc = c->lv[l + 1];
+  launch_cell_resid_restrict(c->st, L.d, Lc.d, c->dim, x, rhs, Lc.crhs);
+  vcycle_cell(c, l + 1, Lc.crhs, Lc.cx, sm);
+  launch_cell_prolong_add(c->st, L.d, Lc.d, c->dim, Lc.cx, x);
+  for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, x, rhs, sm.omega);
+}
+
+// multigrid.py:442-460 on level-0 device buffers
+void mg_face(sb_ctx* c, int ncyc, const double* const* rhs, double* const* out, const sb_smoother& sm) {
+  vcycle_face(c, 0, rhs, out, sm);
+  if (ncyc <= 1) return;
+  ensure_scratch_mg(c);
+  const Level& L = c->lv[0];
+  Box fb;
+  for (int k = 1; k < ncyc; ++k) {
+    CPtr3 xo{{out[0], out[1], out[2]}}, rr{{rhs[0], rhs[1], rhs[2]}};
+    Ptr3 R{{c->sfR[0], c->sfR[1], c->sfR[2]}};
+    launch_face_residual(c->st, L.d, c->dim, c->form, xo, rr, nullptr, R);
+    vcycle_face(c, 0, c->sfR, c->sfC, sm);
+    for (int A = 3 - c->dim; A < 3; ++A) {
+      for (int a = 0; a < 3; ++a) {
+        fb.lo[a] = 0;
+        fb.hi[a] = L.d.n[a] - 1 + ((a == A && c->bc[A][0] != BC_PER) ? 1 : 0);
+      }
+      launch_axpy_box(c->st, L.d, fb, out[A], c->sfC[A]);
+    }
+  }
+}
+
+void mg_cell(sb_ctx* c, int ncyc, const double* rhs, double* out, const sb_smoother& sm) {
+  vcycle_cell(c, 0, rhs, out, sm);
+  if (ncyc <= 1) return;
+  ensure_scratch_mg(c);
+  const Level& L = c->lv[0];
+  Box cb;
+  for (int a = 0; a < 3; ++a) {
+    cb.lo[a] = 0;
+    cb.hi[a] = L.d.n[a] - 1;
+  }
+  for (int k = 1; k < ncyc; ++k) {
+    launch_cell_residual(c->st, L.d, c->dim, out, rhs, c->scR);
+    vcycle_cell(c, 0, c->scR, c->scC, sm);
+    launch_axpy_box(c->st, L.d, cb, out, c->scC);
+  }
+}
+
+// ---- reductions ----------------------------------------------------------------
+
+double* dh1(sb_ctx* c) { return c->dsmall; }
+double* dh2(sb_ctx* c) { return c->dsmall + kMaxVec; }
+double* dmisc(sb_ctx* c) { return c->dsmall + 2 * kMaxVec; }
+double* dy(sb_ctx* c) { return c->dsmall + 2 * kMaxVec + 64; }
+double* hh1(sb_ctx* c) { return c->hsmall; }
+double* hh2(sb_ctx* c) { return c->hsmall + kMaxVec; }
+double* hmisc(sb_ctx* c) { return c->hsmall + 2 * kMaxVec; }
+double* hy(sb_ctx* c) { return c->hsmall + 2 * kMaxVec + 64; }
+
+// device sum of a full block into dmisc[slot]
+void block_sum(sb_ctx* c, const double* x, long long n, int slot) {
+  launch_sum_partial(c->st, x, n, c->dpart);
+  launch_finalize(c->st, c->dpart, 1, dmisc(c) + slot);
+}
+
+// ||x||^2 of a flat vector into dmisc[slot]
+void vec_norm2(sb_ctx* c, const double* x, int slot) {
+  launch_multi_dot(c->st, x, 0, 1, x, c->vlen, c->dpart);
+  launch_finalize(c->st, c->dpart, 1, dmisc(c) + slot);
+}
+
+double fetch_misc(sb_ctx* c, int slot) {
+  CK(cudaMemcpyAsync(hmisc(c) + slot, dmisc(c) + slot, 8, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return hmisc(c)[slot];
+}
+
+// ---- preconditioner (precond.py:111-168) ------------------------------------------
+
+long long precond_cost(const sb_ctx* c, const sb_precond& pc) {
+  const long long v = (long long)c->dim * pc.velocity_cycles, p = pc.pressure_cycles;
+  const bool th = c->theta > 0;
+  switch (pc.kind) {
+    case SB_P1: return v + p;
+    case SB_P2: case SB_P3: case SB_P4: return v + (th ? p : 0);
+    case SB_P5: return 2 * v + (th ? p : 0);
+    default: return 0;
+  }
+}
+
+void project_nulls(sb_ctx* c, double* x) {
+  const Level& L = c->lv[0];
+  Box cb;
+  for (int a = 0; a < 3; ++a) {
+    cb.lo[a] = 0;
+    cb.hi[a] = L.d.n[a] - 1;
+  }
+  const double ncell = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+  double* xp = vpres(c, x);
+  block_sum(c, xp, L.block, 0);
+  launch_box_add_scalar(c->st, L.d, cb, xp, dmisc(c) + 0, 1.0 / ncell);
+  int slot = 1;
+  for (int A : c->null_comps) {
+    double* xa = vcomp(c, x, A);
+    block_sum(c, xa, L.block, slot);
+    // null components are periodic along A: every stored face is an unknown
+    launch_box_add_scalar(c->st, L.d, cb, xa, dmisc(c) + slot, 1.0 / ncell);
+    ++slot;
+  }
+}
+
+// x = P^{-1} r on level-0 vectors (all device, stream-ordered, graph-capturable)
+void precond_dev(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm, double* r, double* x) {
+  const Level& L = c->lv[0];
+  const int d = c->dim, o = c->off;
+  const double sign = pc.schur_sign < 0 ? -1.0 : 1.0;
+  const double* ru[3] = {nullptr, nullptr, nullptr};
+  double* xu[3] = {nullptr, nullptr, nullptr};
+  for (int A = o; A < 3; ++A) {
+    ru[A] = vcomp(c, r, A);
+    xu[A] = vcomp(c, x, A);
+  }
+  double* rp = vpres(c, r);
+  double* xp = vpres(c, x);
+  if (pc.kind == SB_IDENTITY) {
+    CK(cudaMemcpyAsync(x, r, c->vlen * 8, cudaMemcpyDeviceToDevice, c->st));
+    return;
+  }
+  ensure_scratch(c);
+  const bool th = c->theta > 0;
+  CPtr3 cxu{{xu[0], xu[1], xu[2]}};
+  switch (pc.kind) {
+    case SB_P1: {
+      mg_face(c, pc.velocity_cycles, ru, xu, sm);
+      launch_div_add(c->st, L.d, d, cxu, rp, c->sc0);
+      mg_cell(c, pc.pressure_cycles, c->sc0, c->sc1, sm);
+      Ptr3 pxu{{xu[0], xu[1], xu[2]}};
+      launch_p1_glue(c->st, L.d, d, c->form, pxu, c->sc1, c->sc0, xp, sign);
+      break;
+    }
+    case SB_P2: {
+      mg_face(c, pc.velocity_cycles, ru, xu, sm);
+      launch_div_add(c->st, L.d, d, cxu, rp, c->sc0);
+      if (th) mg_cell(c, pc.pressure_cycles, c->sc0, c->sc1, sm);
+      launch_schur(c->st, L.d, c->form, c->sc0, th ? c->sc1 : nullptr, xp, sign);
+      break;
+    }
+    case SB_P3: {
+      if (th) mg_cell(c, pc.pressure_cycles, rp, c->sc1, sm);
+      launch_schur(c->st, L.d, c->form, rp, th ? c->sc1 : nullptr, xp, sign);
+      CPtr3 cru{{ru[0], ru[1], ru[2]}};
+      Ptr3 f0{{c->sf0[0], c->sf0[1], c->sf0[2]}};
+      launch_face_sub_grad(c->st, L.d, d, cru, xp, f0);
+      mg_face(c, pc.velocity_cycles, c->sf0, xu, sm);
+      break;
+    }
+    case SB_P4: {
+      mg_face(c, pc.velocity_cycles, ru, xu, sm);
+      if (th) mg_cell(c, pc.pressure_cycles, rp, c->sc1, sm);
+      launch_schur(c->st, L.d, c->form, rp, th ? c->sc1 : nullptr, xp, sign);
+      break;
+    }
+    case SB_P5: {
+      mg_face(c, pc.velocity_cycles, ru, c->sf1, sm);
+      CPtr3 cs1{{c->sf1[0], c->sf1[1], c->sf1[2]}};
+      launch_div_add(c->st, L.d, d, cs1, rp, c->sc0);
+      if (th) mg_cell(c, pc.pressure_cycles, c->sc0, c->sc1, sm);
+      launch_schur(c->st, L.d, c->form, c->sc0, th ? c->sc1 : nullptr, xp, sign);
+      CPtr3 cru{{ru[0], ru[1], ru[2]}};
+      Ptr3 f0{{c->sf0[0], c->sf0[1], c->sf0[2]}};
+      launch_face_residual(c->st, L.d, d, c->form, cs1, cru, xp, f0);
+      mg_face(c, pc.velocity_cycles, c->sf0, xu, sm);
+      for (int A = o; A < 3; ++A) {
+        Box fb;
+        for (int a = 0; a < 3; ++a) {
+          fb.lo[a] = 0;
+          fb.hi[a] = L.d.n[a] - 1 + ((a == A && c->bc[A][0] != BC_PER) ? 1 : 0);
+        }
+        launch_axpy_box(c->st, L.d, fb, xu[A], c->sf1[A]);
+      }
+      break;
+    }
+    default:
+      throw ArgErr(SB_EINVAL, "unknown preconditioner kind");
+  }
+  project_nulls(c, x);
+}
+
+void drop_graph(sb_ctx* c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+}
+
+// vw = P^{-1} vMv, through the cached CUDA graph when enabled
+void precond_apply_graph(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm) {
+  if (!c->use_graphs || c->profiling) {
+    precond_dev(c, pc, sm, c->vMv, c->vw);
+    return;
+  }
+  const bool same = c->gexec && std::memcmp(&c->gpc, &pc, sizeof(pc)) == 0 &&
+                    std::memcmp(&c->gsm, &sm, sizeof(sm)) == 0;
+  if (!same) {
+    drop_graph(c);
+    ensure_scratch(c);
+    if (pc.velocity_cycles > 1 || pc.pressure_cycles > 1) ensure_scratch_mg(c);
+    const long long before = g_kernel_launches;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      precond_dev(c, pc, sm, c->vMv, c->vw);
+    } catch (...) {
+      cudaStreamEndCapture(c->st, &g);
+      if (g) cudaGraphDestroy(g);
+      g_kernel_launches = before;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->st, &g));
+    g_kernel_launches = before;
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    long long nk = 0;
+    for (auto& nd : nodes) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(nd, &t));
+      if (t == cudaGraphNodeTypeKernel) ++nk;
+    }
+    CK(cudaGraphInstantiate(&c->gexec, g, 0));
+    CK(cudaGraphDestroy(g));
+    c->gnodes = nk;
+    c->gpc = pc;
+    c->gsm = sm;
+  }
+  CK(cudaGraphLaunch(c->gexec, c->st));
+  c->graph_launches += c->gnodes;
+}
+
+// ---- GMRES (krylov.py:81-214) -----------------------------------------------------
+
+void solve_upper(const std::vector<double>& H, int ld, const double* g, int n, double* y) {
+  for (int i = n - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int k = i + 1; k < n; ++k) s += H[i * ld + k] * y[k];
+    y[i] = (g[i] - s) / H[i * ld + i];
+  }
+}
+
+void apply_M_vec(sb_ctx* c, const double* x, double* out) {
+  const Level& L = c->lv[0];
+  CPtr3 u{{nullptr, nullptr, nullptr}};
+  Ptr3 o{{nullptr, nullptr, nullptr}};
+  for (int A = c->off; A < 3; ++A) {
+    u.p[A] = vcomp(c, (double*)x, A);
+    o.p[A] = vcomp(c, out, A);
+  }
+  launch_apply_M(c->st, L.d, c->dim, c->form, u, vpres(c, (double*)x), o, vpres(c, out));
+}
+
+// upload a host/device vector in the reference layout into a level-0 vector
+void vec_in(sb_ctx* c, const double* const* u, const double* p, double* v) {
+  const Level& L = c->lv[0];
+  for (int r = 0; r < c->dim; ++r) {
+    const int A = r + c->off;
+    copy_in(c, L, A, u[r], vcomp(c, v, A));
+    zero_wall_faces(c, L, A, vcomp(c, v, A));
+  }
+  copy_in(c, L, -1, p, vpres(c, v));
+}
+void vec_out(sb_ctx* c, const double* v, double* const* u, double* p) {
+  const Level& L = c->lv[0];
+  for (int r = 0; r < c->dim; ++r) {
+    const int A = r + c->off;
+    copy_out(c, L, A, vcomp(c, (double*)v, A), u[r]);
+  }
+  copy_out(c, L, -1, vpres(c, (double*)v), p);
+}
+
+void ensure_basis(sb_ctx* c, int m) {
+  if (c->basis_cap >= m + 1) return;
+  if (c->basis) {
+    for (auto it = c->allocs.begin(); it != c->allocs.end(); ++it)
+      if (*it == c->basis) {
+        c->allocs.erase(it);
+        break;
+      }
+    CK(cudaFree(c->basis));
+    c->bytes -= (long long)c->basis_cap * c->vlen * 8;
+    c->basis = nullptr;
+  }
+  c->basis = dalloc(c, (long long)(m + 1) * c->vlen);
+  c->basis_cap = m + 1;
+}
+
+void prof_reset(sb_ctx* c) {
+  c->prof.clear();
+  c->evnext = 0;
+}
+
+void prof_collect(sb_ctx* c) {
+  sb_kernel_stats s{};
+  for (auto& e : c->prof) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e.a, e.b));
+    if (e.cls == 0) {
+      s.smoother_face_ms += ms;
+      s.smoother_face_bytes += e.bytes;
+      s.smoother_face_launches++;
+      if (e.fine) {
+        s.fine_face_ms += ms;
+        s.fine_face_bytes += e.bytes;
+        s.fine_face_launches++;
+      }
+    } else {
+      s.smoother_cell_ms += ms;
+      s.smoother_cell_bytes += e.bytes;
+      s.smoother_cell_launches++;
+    }
+  }
+  c->stats = s;
+}
+
+int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother& sm,
+          const double* const* bu, const double* bp, double* const* xu, double* xpo,
+          sb_history_row* rows, int max_rows, int* n_rows, int* status, long long* vcyc) {
+  if (pc.kind != SB_IDENTITY) {
+    check_mg(c, SB_KIND_FACE);
+    if (pc.kind == SB_P1 || c->theta > 0) check_mg(c, SB_KIND_CELL);
+  } else {
+    check_ready(c);
+  }
+  const int m = gc.restart;
+  if (m < 1 || m >= kMaxVec) throw ArgErr(SB_EINVAL, "restart must be in [1, 127] on the device path");
+  ensure_vectors(c);
+  ensure_basis(c, m);
+  if (c->profiling) prof_reset(c);
+  const long long vl = c->vlen;
+  int nr = 0;
+  auto add_row = [&](int it, double rp, double rt, bool rf) {
+    if (nr < max_rows) rows[nr] = sb_history_row{it, *vcyc, rp, rt, rf ? 1 : 0};
+    ++nr;
+  };
+  vec_in(c, bu, bp, c->vb);
+  vec_norm2(c, c->vb, 0);
+  const double bnorm = std::sqrt(fetch_misc(c, 0));
+  // z0 = P^{-1} b
+  CK(cudaMemcpyAsync(c->vMv, c->vb, vl * 8, cudaMemcpyDeviceToDevice, c->st));
+  precond_apply_graph(c, pc, sm);
+  *vcyc += precond_cost(c, pc);
+  CK(cudaMemcpyAsync(c->vz0, c->vw, vl * 8, cudaMemcpyDeviceToDevice, c->st));
+  vec_norm2(c, c->vz0, 0);
+  const double rp0 = std::sqrt(fetch_misc(c, 0));
+  add_row(0, rp0, bnorm, false);
+  CK(cudaMemsetAsync(c->vx, 0, vl * 8, c->st));
+  auto finish = [&](int st) {
+    vec_out(c, c->vx, xu, xpo);
+    sync(c);
+    *status = st;
+    *n_rows = nr;
+    if (c->profiling) prof_collect(c);
+    return SB_OK;
+  };
+  if (rp0 <= gc.atol || rp0 == 0.0) return finish(SB_STATUS_CONVERGED);
+  const double target = gc.rtol * rp0 + gc.atol;
+  const double bd_tol = std::max(gc.atol, 1e-14 * rp0);
+
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1);
+  int k = 0;
+  bool first = true;
+  const double* r = c->vz0;
+  double beta = rp0;
+  while (true) {
+    if (!first) {
+      vec_norm2(c, r, 0);
+      beta = std::sqrt(fetch_misc(c, 0));
+    }
+    if (beta == 0.0) return finish(SB_STATUS_CONVERGED);
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(cs.begin(), cs.end(), 0.0);
+    std::fill(sn.begin(), sn.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    double* V = c->basis;
+    launch_scale_div(c->st, r, beta, V, vl);
+    g[0] = beta;
+    int j = 0;
+    int ydim = 0;  // columns in the last least-squares solve
+    while (j < m && k < gc.max_iters) {
+      apply_M_vec(c, V + (long long)j * vl, c->vMv);
+      precond_apply_graph(c, pc, sm);
+      *vcyc += precond_cost(c, pc);
+      ++k;
+      // CGS2 Arnoldi (parity-safe replacement of MGS)
+      const int nv = j + 1;
+      launch_multi_dot(c->st, V, vl, nv, c->vw, vl, c->dpart);
+      launch_finalize(c->st, c->dpart, nv, dh1(c));
+      launch_update_dot(c->st, V, vl, nv, dh1(c), c->vw, vl, c->dpart, 0);
+      launch_finalize(c->st, c->dpart, nv, dh2(c));
+      launch_update_dot(c->st, V, vl, nv, dh2(c), c->vw, vl, c->dpart, 1);
+      launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
+      CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      for (int i = 0; i <= j; ++i) H[i * m + j] = hh1(c)[i] + hh2(c)[i];
+      const double hn = std::sqrt(hmisc(c)[1]);
+      H[(j + 1) * m + j] = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+        H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
+        H[i * m + j] = t;
+      }
+      const double den = std::hypot(H[j * m + j], H[(j + 1) * m + j]);
+      if (den == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = H[j * m + j] / den;
+        sn[j] = H[(j + 1) * m + j] / den;
+      }
+      H[j * m + j] = den;
+      H[(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      const double rp = std::fabs(g[j + 1]);
+      const bool conv = rp <= target;
+      const bool brk = !conv && hn <= bd_tol;
+      ydim = j + 1;
+      double rt = NAN;
+      if (gc.track_true_residual || conv || brk) {
+        solve_upper(H, m, g.data(), ydim, y.data());
+        std::memcpy(hy(c), y.data(), ydim * 8);
+        CK(cudaMemcpyAsync(dy(c), hy(c), ydim * 8, cudaMemcpyHostToDevice, c->st));
+      }
+      if (gc.track_true_residual) {
+        launch_combo(c->st, c->vt, c->vx, V, vl, ydim, dy(c), vl);
+        apply_M_vec(c, c->vt, c->vMv);
+        launch_sub_norm(c->st, c->vb, c->vMv, vl, c->dpart);
+        launch_finalize(c->st, c->dpart, 1, dmisc(c) + 2);
+        rt = std::sqrt(fetch_misc(c, 2));
+      }
+      add_row(k, rp, rt, j == 0 && !first);
+      if (conv || brk) {
+        launch_combo(c->st, c->vx, c->vx, V, vl, ydim, dy(c), vl);
+        return finish(conv ? SB_STATUS_CONVERGED : SB_STATUS_BREAKDOWN);
+      }
+      launch_scale_div(c->st, c->vw, hn, V + (long long)(j + 1) * vl, vl);
+      ++j;
+    }
+    // x = x + V[:j] y  (the last iteration's least-squares solution)
+    solve_upper(H, m, g.data(), ydim, y.data());
+    std::memcpy(hy(c), y.data(), ydim * 8);
+    CK(cudaMemcpyAsync(dy(c), hy(c), ydim * 8, cudaMemcpyHostToDevice, c->st));
+    launch_combo(c->st, c->vx, c->vx, V, vl, ydim, dy(c), vl);
+    first = false;
+    if (k >= gc.max_iters) return finish(SB_STATUS_MAXITER);
+    // r = z0 - P^{-1} M x
+    apply_M_vec(c, c->vx, c->vMv);
+    precond_apply_graph(c, pc, sm);
+    *vcyc += precond_cost(c, pc);
+    launch_sub(c->st, c->vz0, c->vw, c->vt, vl);
+    r = c->vt;
+  }
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    return f();
+  } catch (const ArgErr& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const CudaErr& e) {
+    g_err = e.what();
+    return SB_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SB_ECUDA;
+  }
+}
+
+}  // namespace
+
+// ====================================================================================
+// C ABI
+// ====================================================================================
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_err.c_str(); }
+
+sb_ctx* sb_create(int dim, const int* cells, double h, const int* bc, int viscous_form) {
+  sb_ctx* c = nullptr;
+  int rc = guard([&]() -> int {
+    if (dim != 2 && dim != 3) throw ArgErr(SB_EINVAL, "dim must be 2 or 3");
+    if (!(h > 0)) throw ArgErr(SB_EINVAL, "grid spacing must be positive");
+    if (viscous_form < 0 || viscous_form > 2) throw ArgErr(SB_EINVAL, "bad viscous form");
+    c = new sb_ctx();
+    c->dim = dim;
+    c->form = viscous_form;
+    c->off = 3 - dim;
+    c->h = h;
+    c->n[0] = 1;
+    c->bc[0][0] = c->bc[0][1] = BC_PER;
+    for (int r = 0; r < dim; ++r) {
+      const int A = r + c->off;
+      if (cells[r] < 2) throw ArgErr(SB_EINVAL, "cell counts must be >= 2");
+      c->n[A] = cells[r];
+      c->bc[A][0] = bc[2 * r];
+      c->bc[A][1] = bc[2 * r + 1];
+      if ((c->bc[A][0] == BC_PER) != (c->bc[A][1] == BC_PER))
+        throw ArgErr(SB_EINVAL, "periodic must hold on both sides of an axis");
+    }
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    int n[3] = {c->n[0], c->n[1], c->n[2]};
+    double hh = h;
+    make_level(c, n, hh);
+    if (can_coarsen(n, dim)) {
+      while (can_coarsen(n, dim)) {
+        for (int a = c->off; a < 3; ++a) n[a] /= 2;
+        hh *= 2.0;
+        make_level(c, n, hh);
+      }
+    }
+    for (size_t l = 0; l < c->lv.size(); ++l) alloc_level(c, c->lv[l], l == 0);
+    int* fl = nullptr;
+    CK(cudaMalloc(&fl, 16));
+    c->allocs.push_back(fl);
+    c->dflags = fl;
+    c->dpart = dalloc(c, (long long)kMaxVec * reduce_blocks());
+    c->dsmall = dalloc(c, 4 * kMaxVec);
+    CK(cudaMallocHost(&c->hsmall, 4 * kMaxVec * 8));
+    c->launches_base = g_kernel_launches;
+    sync(c);
+    return SB_OK;
+  });
+  if (rc != SB_OK) {
+    if (c) sb_destroy(c);
+    return nullptr;
+  }
+  return c;
+}
+
+void sb_destroy(sb_ctx* c) {
+  if (!c) return;
+  drop_graph(c);
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->hsmall) cudaFreeHost(c->hsmall);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+int sb_set_coefficients(sb_ctx* c, double theta, const double* const* rho_face, const double* mu_cell,
+                        const double* const* mu_edge, const double* gamma_cell) {
+  return guard([&]() -> int {
+    if (!(theta >= 0)) throw ArgErr(SB_EINVAL, "theta must be >= 0");
+    drop_graph(c);
+    c->theta = theta;
+    for (auto& L : c->lv) L.d.theta = theta;
+    Level& L0 = c->lv[0];
+    copy_in(c, L0, -1, mu_cell, L0.mu_c);
+    if (gamma_cell) copy_in(c, L0, -1, gamma_cell, L0.gam_c);
+    else CK(cudaMemsetAsync(L0.gam_c, 0, L0.block * 8, c->st));
+    for (int r = 0; r < c->dim; ++r) copy_in(c, L0, r + c->off, rho_face[r], L0.rho_f[r + c->off]);
+    if (c->dim == 3) {
+      // edge_planes order (0,1),(0,2),(1,2) -> normal axis 2,1,0
+      copy_in(c, L0, 12, mu_edge[0], L0.mu_e[2]);
+      copy_in(c, L0, 11, mu_edge[1], L0.mu_e[1]);
+      copy_in(c, L0, 10, mu_edge[2], L0.mu_e[0]);
+    } else {
+      copy_in(c, L0, 10, mu_edge[0], L0.mu_e[0]);
+    }
+    for (size_t l = 0; l + 1 < c->lv.size(); ++l) {
+      Level& F = c->lv[l];
+      Level& C = c->lv[l + 1];
+      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.mu_c, C.mu_c);
+      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.gam_c, C.gam_c);
+      for (int A = c->off; A < 3; ++A) launch_coarsen_face(c->st, F.d, C.d, c->dim, A, F.rho_f[A], C.rho_f[A]);
+      if (c->dim == 3) {
+        for (int e = 0; e < 3; ++e) launch_coarsen_edge(c->st, F.d, C.d, 3, e, F.mu_e[e], C.mu_e[e]);
+      } else {
+        launch_coarsen_edge(c->st, F.d, C.d, 2, 0, F.mu_e[0], C.mu_e[0]);
+      }
+    }
+    CK(cudaMemsetAsync(c->dflags, 0, 16, c->st));
+    int hf[4] = {0, 0, 0, 0};
+    for (size_t l = 0; l < c->lv.size(); ++l) {
+      Level& L = c->lv[l];
+      for (int A = c->off; A < 3; ++A) launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2);
+    }
+    for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
+    CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    c->flag_face = hf[0] & 1;
+    c->flag_cell = (hf[0] >> 1) & 1;
+    c->flag_rho = hf[2] & 1;
+    // operators.py:368-388 velocity_null_components
+    c->null_comps.clear();
+    if (theta == 0.0) {
+      for (int A = c->off; A < 3; ++A) {
+        if (c->bc[A][0] != BC_PER) continue;
+        bool ok = true;
+        for (int B = c->off; B < 3; ++B) {
+          if (B == A) continue;
+          const bool pb = c->bc[B][0] == BC_PER;
+          const bool fs = c->bc[B][0] == BC_FREESLIP && c->bc[B][1] == BC_FREESLIP;
+          if (!(pb || fs)) ok = false;
+        }
+        if (ok) c->null_comps.push_back(A);
+      }
+    }
+    c->have_coef = true;
+    return SB_OK;
+  });
+}
+
+int sb_apply_M(sb_ctx* c, const double* const* u, const double* p, double* const* out_u, double* out_p) {
+  return guard([&]() -> int {
+    check_ready(c);
+    ensure_vectors(c);
+    vec_in(c, u, p, c->vt);
+    apply_M_vec(c, c->vt, c->vMv);
+    vec_out(c, c->vMv, out_u, out_p);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_apply_A(sb_ctx* c, const double* const* u, double* const* out_u) {
+  return guard([&]() -> int {
+    check_ready(c);
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    for (int r = 0; r < c->dim; ++r) {
+      const int A = r + c->off;
+      copy_in(c, L, A, u[r], c->sf0[A]);
+      zero_wall_faces(c, L, A, c->sf0[A]);
+    }
+    CPtr3 x{{c->sf0[0], c->sf0[1], c->sf0[2]}}, none{{nullptr, nullptr, nullptr}};
+    Ptr3 o{{c->sf1[0], c->sf1[1], c->sf1[2]}};
+    launch_face_residual(c->st, L.d, c->dim, c->form, x, none, nullptr, o);
+    for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, c->sf1[r + c->off], out_u[r]);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_apply_Lrho(sb_ctx* c, const double* p, double* out_p) {
+  return guard([&]() -> int {
+    check_ready(c);
+    if (c->flag_rho) throw ArgErr(SB_EINVAL, "face density must be positive");
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    copy_in(c, L, -1, p, c->sc0);
+    launch_cell_residual(c->st, L.d, c->dim, c->sc0, nullptr, c->sc1);
+    copy_out(c, L, -1, c->sc1, out_p);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_mg_solve(sb_ctx* c, int kind, const sb_smoother* sm, int n_cycles, const double* const* rhs,
+                double* const* out) {
+  return guard([&]() -> int {
+    if (kind != SB_KIND_CELL && kind != SB_KIND_FACE) throw ArgErr(SB_EINVAL, "kind must be 'cell' or 'face'");
+    if (n_cycles < 1) throw ArgErr(SB_EINVAL, "need at least one cycle");
+    check_mg(c, kind);
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    if (kind == SB_KIND_CELL) {
+      copy_in(c, L, -1, rhs[0], c->sc0);
+      mg_cell(c, n_cycles, c->sc0, c->sc1, *sm);
+      copy_out(c, L, -1, c->sc1, out[0]);
+    } else {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, L, A, rhs[r], c->sf0[A]);
+        zero_wall_faces(c, L, A, c->sf0[A]);
+      }
+      mg_face(c, n_cycles, c->sf0, c->sf1, *sm);
+      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, c->sf1[r + c->off], out[r]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_precond_apply(sb_ctx* c, const sb_precond* pc, const sb_smoother* sm, const double* const* r_u,
+                     const double* r_p, double* const* x_u, double* x_p, long long* scalar_vcycles) {
+  return guard([&]() -> int {
+    if (pc->kind != SB_IDENTITY) {
+      check_mg(c, SB_KIND_FACE);
+      if (pc->kind == SB_P1 || c->theta > 0) check_mg(c, SB_KIND_CELL);
+    } else {
+      check_ready(c);
+    }
+    ensure_vectors(c);
+    vec_in(c, r_u, r_p, c->vMv);
+    precond_apply_graph(c, *pc, *sm);
+    vec_out(c, c->vw, x_u, x_p);
+    sync(c);
+    if (scalar_vcycles) *scalar_vcycles += precond_cost(c, *pc);
+    return SB_OK;
+  });
+}
+
+int sb_gmres_solve(sb_ctx* c, const sb_precond* pc, const sb_gmres* gc, const sb_smoother* sm,
+                   const double* const* b_u, const double* b_p, double* const* x_u, double* x_p,
+                   sb_history_row* rows, int max_rows, int* n_rows, int* status, long long* scalar_vcycles) {
+  return guard([&]() -> int {
+    long long dummy = 0;
+    return gmres(c, *pc, *gc, *sm, b_u, b_p, x_u, x_p, rows, max_rows, n_rows, status,
+                 scalar_vcycles ? scalar_vcycles : &dummy);
+  });
+}
+
+int sb_num_levels(sb_ctx* c) { return (int)c->lv.size(); }
+
+int sb_level_cells(sb_ctx* c, int level, int* cells) {
+  if (level < 0 || level >= (int)c->lv.size()) {
+    g_err = "level out of range";
+    return SB_EINVAL;
+  }
+  for (int r = 0; r < c->dim; ++r) cells[r] = c->lv[level].d.n[r + c->off];
+  return SB_OK;
+}
+
+int sb_get_level_coefficients(sb_ctx* c, int level, double* const* rho_face, double* mu_cell,
+                              double* const* mu_edge, double* gamma_cell) {
+  return guard([&]() -> int {
+    check_ready(c);
+    if (level < 0 || level >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    const Level& L = c->lv[level];
+    if (mu_cell) copy_out(c, L, -1, L.mu_c, mu_cell);
+    if (gamma_cell) copy_out(c, L, -1, L.gam_c, gamma_cell);
+    if (rho_face)
+      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, L.rho_f[r + c->off], rho_face[r]);
+    if (mu_edge) {
+      if (c->dim == 3) {
+        copy_out(c, L, 12, L.mu_e[2], mu_edge[0]);
+        copy_out(c, L, 11, L.mu_e[1], mu_edge[1]);
+        copy_out(c, L, 10, L.mu_e[0], mu_edge[2]);
+      } else {
+        copy_out(c, L, 10, L.mu_e[0], mu_edge[0]);
+      }
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+// level-l staging buffers for the component entry points
+static void level_bufs(sb_ctx* c, int l, int kind, double** x, double** rhs) {
+  Level& L = c->lv[l];
+  ensure_scratch(c);
+  for (int a = 0; a < 3; ++a) {
+    if (kind == SB_KIND_FACE) {
+      x[a] = l == 0 ? c->sf0[a] : L.fx[a];
+      rhs[a] = l == 0 ? c->sf1[a] : L.frhs[a];
+    } else {
+      x[a] = l == 0 ? c->sc0 : L.cx;
+      rhs[a] = l == 0 ? c->sc1 : L.crhs;
+    }
+  }
+}
+
+int sb_smooth(sb_ctx* c, int kind, int level, double omega, double* const* x, const double* const* rhs) {
+  return guard([&]() -> int {
+    check_mg(c, kind);
+    if (level < 0 || level >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *bx[3], *br[3];
+    level_bufs(c, level, kind, bx, br);
+    const Level& L = c->lv[level];
+    if (kind == SB_KIND_FACE) {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, L, A, x[r], bx[A]);
+        copy_in(c, L, A, rhs[r], br[A]);
+      }
+      sweep_face(c, level, bx, br, omega);
+      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, bx[r + c->off], x[r]);
+    } else {
+      copy_in(c, L, -1, x[0], bx[0]);
+      copy_in(c, L, -1, rhs[0], br[0]);
+      sweep_cell(c, level, bx[0], br[0], omega);
+      copy_out(c, L, -1, bx[0], x[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_residual_restrict(sb_ctx* c, int kind, int level, const double* const* x, const double* const* rhs,
+                         double* const* coarse) {
+  return guard([&]() -> int {
+    check_mg(c, kind);
+    if (level < 0 || level + 1 >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *bx[3], *br[3];
+    level_bufs(c, level, kind, bx, br);
+    const Level& L = c->lv[level];
+    Level& C = c->lv[level + 1];
+    if (kind == SB_KIND_FACE) {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, L, A, x[r], bx[A]);
+        copy_in(c, L, A, rhs[r], br[A]);
+      }
+      CPtr3 xc{{bx[0], bx[1], bx[2]}};
+      for (int A = c->off; A < 3; ++A)
+        launch_face_resid_restrict(c->st, L.d, C.d, c->dim, c->form, A, xc, br[A], C.frhs[A]);
+      for (int r = 0; r < c->dim; ++r) copy_out(c, C, r + c->off, C.frhs[r + c->off], coarse[r]);
+    } else {
+      copy_in(c, L, -1, x[0], bx[0]);
+      copy_in(c, L, -1, rhs[0], br[0]);
+      launch_cell_resid_restrict(c->st, L.d, C.d, c->dim, bx[0], br[0], C.crhs);
+      copy_out(c, C, -1, C.crhs, coarse[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_prolong_add(sb_ctx* c, int kind, int level, const double* const* coarse, double* const* fine) {
+  return guard([&]() -> int {
+    check_ready(c);
+    if (level < 0 || level + 1 >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *bx[3], *br[3];
+    level_bufs(c, level, kind, bx, br);
+    const Level& L = c->lv[level];
+    Level& C = c->lv[level + 1];
+    if (kind == SB_KIND_FACE) {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, C, A, coarse[r], C.fx[A]);
+        copy_in(c, L, A, fine[r], bx[A]);
+        launch_face_prolong_add(c->st, L.d, C.d, c->dim, A, C.fx[A], bx[A]);
+        copy_out(c, L, A, bx[A], fine[r]);
+      }
+    } else {
+      copy_in(c, C, -1, coarse[0], C.cx);
+      copy_in(c, L, -1, fine[0], bx[0]);
+      launch_cell_prolong_add(c->st, L.d, C.d, c->dim, C.cx, bx[0]);
+      copy_out(c, L, -1, bx[0], fine[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+void sb_set_profiling(sb_ctx* c, int enabled) { c->profiling = enabled != 0; }
+
+int sb_get_kernel_stats(sb_ctx* c, sb_kernel_stats* out) {
+  *out = c->stats;
+  return SB_OK;
+}
+
+long long sb_launch_count(sb_ctx* c) { return (g_kernel_launches - c->launches_base) + c->graph_launches; }
+
+void sb_set_graphs(sb_ctx* c, int enabled) {
+  c->use_graphs = enabled != 0;
+  if (!c->use_graphs) drop_graph(c);
+}
+
+long long sb_device_bytes(sb_ctx* c) { return c->bytes; }
+
+}  // extern "C"

@@ -1,0 +1,255 @@
+"""Coefficients (host) and the saddle operators (device) -- drop-in mirror.
+
+Mirrors the hot-path surface of the reference's ``stokesmg.operators``
+(``/root/reference/pkg/src/stokesmg/operators.py``):
+
+* host-side setup, as in the reference: ``ViscousForm`` (:29), the
+  ``CoefficientSet`` container and its validation (:45-78),
+  ``make_coefficients`` with cell->face / cell->node/edge averaging
+  (:81-125), ``RescaleSpec`` / ``rescale`` (:515-550) and
+  ``velocity_null_components`` (:368-388);
+* the operators themselves run on the B200 through the C ABI:
+  ``apply_M`` (:363), ``apply_A`` (:348), ``apply_Lrho`` (:206).
+
+Inputs/outputs are the reference's field types (this package's mirror or the
+reference's own objects, duck-typed).
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib
+from .grid import (FREE_SLIP, CellField, FaceField, GridSpec, NodeEdgeField, StokesVector,
+                   as_grid, edge_planes)
+
+
+class ViscousForm(enum.Enum):
+    LAPLACIAN = "laplacian"
+    STRESS = "stress"
+    STRESS_BULK = "stress_bulk"
+
+
+LAPLACIAN = ViscousForm.LAPLACIAN
+STRESS = ViscousForm.STRESS
+STRESS_BULK = ViscousForm.STRESS_BULK
+
+FORM_CODE = {"laplacian": 0, "stress": 1, "stress_bulk": 2}
+
+
+def form_code(form) -> int:
+    return FORM_CODE[getattr(form, "value", form)]
+
+
+@dataclass
+class CoefficientSet:
+    """theta, densities (cell + face), viscosities (cell + node/edge), bulk gamma."""
+
+    theta: float
+    rho_cell: CellField
+    rho_face: FaceField
+    mu_cell: CellField
+    mu_node_edge: NodeEdgeField
+    gamma_cell: CellField
+    viscous_form: ViscousForm = STRESS
+
+    def __post_init__(self):
+        if self.theta < 0:
+            raise ValueError("theta must be >= 0")
+        if self.theta > 0 and (self.rho_cell.data <= 0).any():
+            raise ValueError("density must be positive for unsteady flow")
+        if (self.mu_cell.data < 0).any():
+            raise ValueError("viscosity must be nonnegative")
+        if self.theta == 0 and not (self.mu_cell.data > 0).any():
+            raise ValueError("steady flow (theta = 0) needs nonzero viscosity")
+
+    @property
+    def grid(self) -> GridSpec:
+        return self.rho_cell.grid
+
+    @property
+    def inviscid(self) -> bool:
+        return not (self.mu_cell.data > 0).any()
+
+
+def _stagger_mean(x: np.ndarray, axis: int, periodic: bool) -> np.ndarray:
+    """Arithmetic mean of the two cells adjacent to each staggered position;
+    wall positions take the single adjacent cell (operators.py:133-145)."""
+    if periodic:
+        return 0.5 * (x + np.roll(x, 1, axis=axis))
+    lo = np.take(x, [0], axis=axis)
+    hi = np.take(x, [-1], axis=axis)
+    inner = 0.5 * (np.delete(x, 0, axis=axis) + np.delete(x, -1, axis=axis))
+    return np.concatenate([lo, inner, hi], axis=axis)
+
+
+def average_cell_to_faces(f: CellField) -> FaceField:
+    g = f.grid
+    return FaceField(g, tuple(_stagger_mean(f.data, a, g.periodic(a)) for a in range(g.dim)))
+
+
+def average_cell_to_node_edge(f: CellField) -> NodeEdgeField:
+    g = f.grid
+    out = {}
+    for pl in edge_planes(g.dim):
+        x = f.data
+        for a in pl:
+            x = _stagger_mean(x, a, g.periodic(a))
+        out[pl] = x
+    return NodeEdgeField(g, out)
+
+
+def make_coefficients(grid, theta, rho_cell, mu_cell, gamma_cell=None, viscous_form=STRESS):
+    if gamma_cell is None:
+        gamma_cell = CellField.zeros(grid)
+    return CoefficientSet(theta=float(theta), rho_cell=rho_cell,
+                          rho_face=average_cell_to_faces(rho_cell), mu_cell=mu_cell,
+                          mu_node_edge=average_cell_to_node_edge(mu_cell),
+                          gamma_cell=gamma_cell, viscous_form=viscous_form)
+
+
+def velocity_null_components(grid, coeff) -> tuple:
+    """Velocity components with a constant null space (steady, periodic axis,
+    transverse axes periodic or free-slip)."""
+    if coeff.theta > 0:
+        return ()
+    g = as_grid(grid)
+    out = []
+    for a in range(g.dim):
+        if not g.periodic(a):
+            continue
+        if all(g.periodic(b) or (g.bc[b][0] is FREE_SLIP and g.bc[b][1] is FREE_SLIP)
+               for b in range(g.dim) if b != a):
+            out.append(a)
+    return tuple(out)
+
+
+@dataclass(frozen=True)
+class RescaleSpec:
+    c: float
+
+    def __post_init__(self):
+        if not self.c > 0:
+            raise ValueError("scale factor must be positive")
+
+    def unscale_solution(self, x):
+        return StokesVector(x.u, (1.0 / self.c) * x.p)
+
+    def scale_solution(self, x):
+        return StokesVector(x.u, self.c * x.p)
+
+
+def rescale(coeff, rhs):
+    """Scale the velocity rows and the pressure unknowns by c = h / max(mu)."""
+    mmax = float(coeff.mu_cell.data.max())
+    c = coeff.grid.h / mmax if mmax > 0 else 1.0
+    scaled = replace(
+        coeff, theta=c * coeff.theta, mu_cell=c * coeff.mu_cell,
+        mu_node_edge=NodeEdgeField(coeff.grid, {k: c * v for k, v in coeff.mu_node_edge.arrays.items()}),
+        gamma_cell=c * coeff.gamma_cell)
+    return scaled, StokesVector(c * rhs.u, rhs.p), RescaleSpec(c)
+
+
+# ---------------------------------------------------------------------------
+# device contexts
+# ---------------------------------------------------------------------------
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class DeviceContext:
+    """One ``sb_ctx``: a grid, its device hierarchy and coefficients."""
+
+    def __init__(self, grid, viscous_form=STRESS):
+        import ctypes as C
+        self.lib = _lib.load()
+        self.grid = as_grid(grid)
+        g = self.grid
+        cells = (C.c_int * 3)(*g.cells)
+        from .grid import BC_CODE
+        bcs = (C.c_int * 6)(*[BC_CODE[x] for pair in g.bc for x in pair])
+        self.form = form_code(viscous_form)
+        h = self.lib.sb_create(g.dim, cells, float(g.h), bcs, self.form)
+        if not h:
+            raise RuntimeError("sb_create failed: " + (self.lib.sb_last_error() or b"").decode())
+        self.h = h
+        self.theta = None
+
+    def set_coefficients(self, coeff):
+        g = self.grid
+        rho = [_f64(c) for c in coeff.rho_face.components]
+        mu = _f64(coeff.mu_cell.data)
+        edges = [_f64(coeff.mu_node_edge.plane(*pl)) for pl in edge_planes(g.dim)]
+        gam = _f64(coeff.gamma_cell.data)
+        for a in range(g.dim):
+            if rho[a].shape != g.face_shape(a):
+                raise ValueError("rho_face layout does not match the grid")
+        _lib.check(self.lib.sb_set_coefficients(self.h, float(coeff.theta), _lib.parr(rho),
+                                                 _lib.ptr(mu), _lib.parr(edges), _lib.ptr(gam)))
+        self.theta = float(coeff.theta)
+        self._keep = (rho, mu, edges, gam)
+
+    def num_levels(self) -> int:
+        return self.lib.sb_num_levels(self.h)
+
+    def level_cells(self, level):
+        import ctypes as C
+        out = (C.c_int * 3)()
+        _lib.check(self.lib.sb_level_cells(self.h, level, out))
+        return tuple(out[: self.grid.dim])
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ctx_for(coeff, grid=None) -> DeviceContext:
+    ctx = DeviceContext(grid if grid is not None else coeff.grid, coeff.viscous_form)
+    ctx.set_coefficients(coeff)
+    return ctx
+
+
+def _out_face(grid):
+    return [np.zeros(grid.face_shape(a)) for a in range(grid.dim)]
+
+
+def apply_M(x, coeff, ctx: DeviceContext | None = None) -> StokesVector:
+    """Saddle operator (A u + G p, -D u) on the device (operators.py:363-365)."""
+    g = as_grid(x.u.grid)
+    ctx = ctx or _ctx_for(coeff, g)
+    ou, op = _out_face(g), np.zeros(g.cells)
+    u = [_f64(c) for c in x.u.components]
+    _lib.check(ctx.lib.sb_apply_M(ctx.h, _lib.parr(u), _lib.ptr(_f64(x.p.data)), _lib.parr(ou), _lib.ptr(op)))
+    return StokesVector(FaceField(g, tuple(ou)), CellField(g, op))
+
+
+def apply_A(u, coeff, bvals=None, ctx: DeviceContext | None = None) -> FaceField:
+    """Velocity operator theta rho u - L_mu u on the device (operators.py:348-360)."""
+    if bvals is not None:
+        raise NotImplementedError("inhomogeneous walls (homogenize) are outside the device path")
+    g = as_grid(u.grid)
+    ctx = ctx or _ctx_for(coeff, g)
+    ou = _out_face(g)
+    _lib.check(ctx.lib.sb_apply_A(ctx.h, _lib.parr([_f64(c) for c in u.components]), _lib.parr(ou)))
+    return FaceField(g, tuple(ou))
+
+
+def apply_Lrho(p, coeff, ctx: DeviceContext | None = None) -> CellField:
+    """Density-weighted Poisson operator D rho^-1 G on the device (operators.py:206-215)."""
+    g = as_grid(p.grid)
+    ctx = ctx or _ctx_for(coeff, g)
+    out = np.zeros(g.cells)
+    _lib.check(ctx.lib.sb_apply_Lrho(ctx.h, _lib.ptr(_f64(p.data)), _lib.ptr(out)))
+    return CellField(g, out)
