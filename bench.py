@@ -1,0 +1,416 @@
+"""Benchmark: preconditioned MAC-Stokes solve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precond P1]
+    python bench.py --impl reference ...        # the reference's CPU path (oracle port)
+
+A step is ONE full ``gmres_solve`` of the configured problem to a relative
+preconditioned residual of 1e-9 (device setup -- coefficient upload, hierarchy
+coarsening, 1/rho, diagonal checks -- plus the GMRES(m)/P1/V-cycle solve).
+
+* ``value``  -- seconds per solve with every input already resident in HBM
+  (torch tensors handed to the C ABI), CUDA events on the stream the library
+  launches on; max over ranks.
+* ``e2e``    -- the same solve through the public drop-in API
+  ``gmres_solve(rhs, coeff, pcfg, gcfg)`` with HOST (pinned) NumPy inputs:
+  H2D of the coefficient set and rhs, the solve, D2H of the solution.
+* ``roofline`` -- the dominant kernel (finest-level face GS colour pass):
+  algorithmic bytes per launch / its average CUDA-event
+  duration in an instrumented solve, against MEASURED_PEAKS.json hbm_gbs.
+* ``cpu_baseline`` -- the oracle (NumPy restatement of the reference, which
+  is itself single-threaded NumPy) on the same recipe at a bounded sample
+  size, extrapolated (see ``cpu_sample``).
+
+The default workload is C5's single-GPU point (256^3 periodic steady Stokes,
+log10-viscosity Fourier field over 3 decades, GMRES(50), P1): C5 is the
+configuration BASELINE.json quotes the metric on ("solve time, iteration
+count, and smoother GB/s at 1/2/4/8 B200s"); C5 at 512^3 does not fit one GPU.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Stokes solve wall-time to rel. residual 1e-9; MG smoother GB/s vs HBM peak"
+ITER_FILE = ROOT / "profiles" / "bench_iterations.json"
+NCU_FILE = ROOT / "profiles" / "ncu_face_colour.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--n", type=int, default=None, help="override cells per axis")
+    ap.add_argument("--precond", default="P1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graphs", type=int, default=1)
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle port of the reference's NumPy algorithm)
+# ---------------------------------------------------------------------------
+
+
+def _oracle_case(config, n, precond):
+    from oracle import stokes_oracle as O
+    from paper_1308_4605_b200 import problems as PR
+    case = PR.make_case(config, n)
+    cs, rs, spec = PR.prepare(case)
+    g = case.grid
+    geo = O.Geo(g.cells, g.h, tuple((lo.value, hi.value) for lo, hi in g.bc))
+    oc = O.Coef(cs.theta, cs.rho_cell.data, list(cs.rho_face.components), cs.mu_cell.data,
+                dict(cs.mu_node_edge.arrays), cs.gamma_cell.data, "stress")
+    return case, geo, oc, list(rs.u.components), rs.p.data
+
+
+def cpu_sample(config, n_target, n_sample, k, precond, iterations):
+    """Time the oracle on the same recipe at n_sample^d: hierarchy setup, then a
+    GMRES run capped at k iterations (k+1 preconditioned-operator applications);
+    extrapolate linearly in cell count (every kernel is O(N)) to a full solve of
+    `iterations` iterations at n_target^d.  The oracle's per-application time
+    at small j under-counts the MGS cost of later iterations, so the
+    extrapolation is a lower bound on the reference's time."""
+    from oracle import stokes_oracle as O
+    case, geo, oc, bu, bp = _oracle_case(config, n_sample, precond)
+    t0 = time.perf_counter()
+    P = O.Precond(geo, oc, O.PrecondOpts(kind=precond))
+    t1 = time.perf_counter()
+    O.gmres_solve(geo, oc, bu, bp, P=P, gopts=O.GmresOpts(restart=case.restart, max_iters=k,
+                                                          track_true_residual=False))
+    t2 = time.perf_counter()
+    t_app = (t2 - t1) / (k + 1)
+    scale = (n_target / n_sample) ** geo.dim
+    restarts = max(0, (iterations - 1) // case.restart)
+    t_full = scale * ((t1 - t0) + (iterations + 1 + restarts) * t_app)
+    sample = (f"oracle (NumPy port of stokesmg, 1 thread) on the {config} recipe at {n_sample}^{geo.dim}: "
+              f"hierarchy setup {t1 - t0:.2f}s + {k} GMRES iterations ({k + 1} P^-1 M applications, "
+              f"{t_app:.2f}s each), extrapolated x{scale:g} in cells to {iterations} iterations at "
+              f"{n_target}^{geo.dim}")
+    return t_full, t2 - t0, sample
+
+
+def bench_iterations(config, precond, default):
+    try:
+        d = json.loads(ITER_FILE.read_text())
+        return int(d[f"{config}_{precond}"]["iterations"]), "device solve of the same inputs"
+    except Exception:
+        return default, "default estimate"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    n_target = args.n or (256 if args.config in ("C4", "C5") else (128 if args.config == "C3" else
+                                                                   (64 if args.config == "C1" else 256)))
+    its, its_src = bench_iterations(args.config, args.precond, 40)
+    n_sample = min(n_target, 128) if args.config in ("C3", "C4", "C5") else n_target
+    for _ in range(args.warmup):
+        cpu_sample(args.config, n_target, max(8, n_sample // 4), 1, args.precond, its)
+    vals, walls = [], []
+    desc = ""
+    for _ in range(args.steps):
+        v, w, desc = cpu_sample(args.config, n_target, n_sample, 1, args.precond, its)
+        vals.append(v)
+        walls.append(w)
+    v = statistics.mean(vals)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded recipe, SURVEY §8d)",
+        "config": {"workload": f"{args.config} {n_target}^3 P1 GMRES({50 if args.config in ('C3', 'C5') else 30})",
+                   "precond": args.precond, "iterations_assumed": its, "iterations_source": its_src},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
+                         "sample_wall_s": statistics.mean(walls)},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# device path
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import edge_planes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve, solve_raw
+    from paper_1308_4605_b200.precond import PrecondConfig, Preconditioner, PrecondKind
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    case = PR.make_case(args.config, args.n)
+    cs, rs, spec = PR.prepare(case)
+    g = case.grid
+    pkind = PrecondKind(args.precond)
+    gcfg = GmresConfig(restart=case.restart, max_iters=500, rtol=1e-9, atol=0.0, track_true_residual=False)
+
+    # ---- HBM-resident inputs -------------------------------------------------
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    class DevCoeff:  # duck-typed CoefficientSet with device tensors
+        pass
+    dc = DevCoeff()
+    dc.theta = cs.theta
+    dc.viscous_form = cs.viscous_form
+    dc.rho_face = type("F", (), {"components": [T(c) for c in cs.rho_face.components]})()
+    dc.mu_cell = type("C", (), {"data": T(cs.mu_cell.data)})()
+    dc.gamma_cell = type("C", (), {"data": T(cs.gamma_cell.data)})()
+    edges = {pl: T(cs.mu_node_edge.plane(*pl)) for pl in edge_planes(g.dim)}
+    dc.mu_node_edge = type("E", (), {"plane": staticmethod(lambda a, b: edges[(min(a, b), max(a, b))])})()
+    bu = [T(c) for c in rs.u.components]
+    bp = T(rs.p.data)
+    xu = [torch.zeros_like(c) for c in bu]
+    xp = torch.zeros_like(bp)
+
+    P = Preconditioner(cs, PrecondConfig(kind=pkind))
+    P.set_graphs(bool(args.graphs))
+    stream = torch.cuda.current_stream(dev)
+    P.ctx.set_stream(stream.cuda_stream)
+
+    def step():
+        P.ctx.set_coefficients(dc)
+        return solve_raw(P, gcfg, bu, bp, xu, xp)
+
+    hist = None
+    for _ in range(max(args.warmup, 0)):
+        hist = step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = P.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        hist = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ck = clocks.stop()
+    launches = P.launch_count() - l0
+    ms = e0.elapsed_time(e1) / max(args.steps, 1)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # setup share (upload + hierarchy) of one step
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    P.ctx.set_coefficients(dc)
+    s1.record(stream)
+    torch.cuda.synchronize(dev)
+    setup_ms = s0.elapsed_time(s1)
+
+    # ---- roofline: instrumented solve (untimed) -------------------------------
+    P.set_profiling(True)
+    step()
+    P.set_profiling(False)
+    st = P.kernel_stats()
+    peak, peak_src = peaks()
+    fine_launch_bytes = st["fine_face_bytes"] / max(st["fine_face_launches"], 1)
+    fine_launch_ms = st["fine_face_ms"] / max(st["fine_face_launches"], 1)
+    achieved = fine_launch_bytes / (fine_launch_ms * 1e-3) / 1e9 if fine_launch_ms > 0 else None
+    traffic = None
+    try:
+        ncu = json.loads(NCU_FILE.read_text())
+        key = f"{args.config}_{case.grid.cells[0]}"
+        traffic = ncu.get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    sm_bytes = st["smoother_face_bytes"] + st["smoother_cell_bytes"]
+    sm_ms = st["smoother_face_ms"] + st["smoother_cell_ms"]
+
+    # ---- e2e through the public API with pinned host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        from paper_1308_4605_b200.grid import CellField, FaceField, NodeEdgeField, StokesVector
+        from paper_1308_4605_b200.operators import CoefficientSet
+
+        def pinned(a):
+            t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+            t.numpy()[...] = a
+            return t.numpy()
+
+        hc = CoefficientSet.__new__(CoefficientSet)
+        hc.theta, hc.viscous_form = cs.theta, cs.viscous_form
+        hc.rho_cell = CellField(g, cs.rho_cell.data)
+        hc.rho_face = FaceField(g, tuple(pinned(c) for c in cs.rho_face.components))
+        hc.mu_cell = CellField(g, pinned(cs.mu_cell.data))
+        hc.mu_node_edge = NodeEdgeField(g, {k: pinned(v) for k, v in cs.mu_node_edge.arrays.items()})
+        hc.gamma_cell = CellField(g, pinned(cs.gamma_cell.data))
+        hr = StokesVector(FaceField(g, tuple(pinned(c) for c in rs.u.components)), CellField(g, pinned(rs.p.data)))
+        P.ctx.set_stream(None)
+        P.ctx.release()  # return the context to the pool; the public call re-acquires it
+        P.ctx = None
+        pc = PrecondConfig(kind=pkind)
+        x, _ = gmres_solve(hr, hc, pc, gcfg)  # warm (pool, graph)
+        h2d = sum(c.nbytes for c in hc.rho_face.components) + hc.mu_cell.data.nbytes + \
+            sum(v.nbytes for v in hc.mu_node_edge.arrays.values()) + hc.gamma_cell.data.nbytes + \
+            sum(c.nbytes for c in hr.u.components) + hr.p.data.nbytes
+        d2h = sum(c.nbytes for c in x.u.components) + x.p.data.nbytes
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            x, ehist = gmres_solve(hr, hc, pc, gcfg)
+        torch.cuda.synchronize(dev)
+        e2e_s = (time.perf_counter() - t0) / max(args.steps, 1)
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "iterations": ehist.iterations, "api": "paper_1308_4605_b200.gmres_solve (host NumPy, pinned)"}
+
+    iters = hist.iterations
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_t = case.grid.cells[0]
+        n_s = min(n_t, 128) if g.dim == 3 else n_t
+        v, wall, desc = cpu_sample(args.config, n_t, n_s, 2, args.precond, iters)
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
+               "sample_wall_s": wall}
+
+    if rank == 0:
+        ITER_FILE.parent.mkdir(exist_ok=True)
+        try:
+            d = json.loads(ITER_FILE.read_text()) if ITER_FILE.exists() else {}
+        except Exception:
+            d = {}
+        if args.n is None:
+            d[f"{args.config}_{args.precond}"] = {"iterations": iters, "status": hist.status,
+                                                  "scalar_vcycles": hist.entries[-1].scalar_vcycles}
+            (ROOT / "gpurun_out").mkdir(exist_ok=True)
+            (ROOT / "gpurun_out" / "bench_iterations.json").write_text(json.dumps(d, indent=1))
+        value = ms / 1e3
+        out = {
+            "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded recipe, SURVEY §8d)",
+            "config": {"workload": f"{args.config} {'x'.join(map(str, g.cells))} "
+                                   f"{'periodic' if case.steady_periodic else 'walls'} {args.precond} "
+                                   f"GMRES({case.restart}) rtol 1e-9",
+                       "precond": args.precond, "restart": case.restart, "cells": list(g.cells),
+                       "iterations": iters, "status": hist.status,
+                       "scalar_vcycles": hist.entries[-1].scalar_vcycles,
+                       "setup_ms": setup_ms,
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (no domain decomposition yet)",
+                       "l2": "every field (134 MB at 256^3) exceeds the 126 MB L2; no flush needed",
+                       "graphs": bool(args.graphs)},
+            "roofline": {"bound": "hbm", "kernel": "k_face_colour (finest level)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "bytes_per_launch": fine_launch_bytes, "ms_per_launch": fine_launch_ms,
+                         "peak_source": peak_src},
+            "smoother": {"GBps": sm_bytes / (sm_ms * 1e-3) / 1e9 if sm_ms > 0 else None,
+                         "frac": (sm_bytes / (sm_ms * 1e-3) / 1e9 / peak) if sm_ms > 0 else None,
+                         "face_ms_per_solve": st["smoother_face_ms"], "cell_ms_per_solve": st["smoother_cell_ms"],
+                         "launches": st["smoother_face_launches"] + st["smoother_cell_launches"]},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": ck, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,10 @@ long long sb_launch_count(sb_ctx* ctx);
 void sb_set_graphs(sb_ctx* ctx, int enabled);
 /* device bytes currently allocated by the context */
 long long sb_device_bytes(sb_ctx* ctx);
+/* run the context's work on a caller-owned CUDA stream (cudaStream_t; NULL
+ * restores the context's own stream), e.g. torch's current stream so that
+ * CUDA events recorded there bracket the solve */
+int sb_set_stream(sb_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

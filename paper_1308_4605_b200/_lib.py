@@ -26,7 +26,7 @@ EXPORTS = (
     "sb_apply_A", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
     "sb_num_levels", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
-    "sb_launch_count", "sb_set_graphs", "sb_device_bytes",
+    "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
 )
 
 
@@ -86,6 +86,7 @@ _SIGS = {
     "sb_launch_count": (C.c_longlong, [_P]),
     "sb_set_graphs": (None, [_P, C.c_int]),
     "sb_device_bytes": (C.c_longlong, [_P]),
+    "sb_set_stream": (C.c_int, [_P, _P]),
 }
 
 _lib = None

@@ -67,6 +67,7 @@ struct sb_ctx {
   int bc[3][2]{};     // internal bcs
   double h = 1.0;
   cudaStream_t st = nullptr;
+  cudaStream_t own_st = nullptr;
   std::vector<Level> lv;
   std::vector<void*> allocs;
   long long bytes = 0;
@@ -880,6 +881,7 @@ sb_ctx* sb_create(int dim, const int* cells, double h, const int* bc, int viscou
         throw ArgErr(SB_EINVAL, "periodic must hold on both sides of an axis");
     }
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_st = c->st;
     int n[3] = {c->n[0], c->n[1], c->n[2]};
     double hh = h;
     make_level(c, n, hh);
@@ -916,7 +918,7 @@ void sb_destroy(sb_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->hsmall) cudaFreeHost(c->hsmall);
-  if (c->st) cudaStreamDestroy(c->st);
+  if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
 }
 
@@ -1232,5 +1234,15 @@ void sb_set_graphs(sb_ctx* c, int enabled) {
 }
 
 long long sb_device_bytes(sb_ctx* c) { return c->bytes; }
+
+int sb_set_stream(sb_ctx* c, void* stream) {
+  return guard([&]() -> int {
+    sync(c);
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->own_st;
+    if (s != c->st) drop_graph(c);
+    c->st = s;
+    return SB_OK;
+  });
+}
 
 }  // extern "C"

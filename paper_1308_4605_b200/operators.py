@@ -158,12 +158,40 @@ def rescale(coeff, rhs):
 # ---------------------------------------------------------------------------
 
 
-def _f64(a) -> np.ndarray:
+def _f64(a):
+    """C-contiguous float64 NumPy array; CUDA/torch tensors pass through (device-resident inputs)."""
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        return a
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+_POOL: dict = {}
+
+
 class DeviceContext:
-    """One ``sb_ctx``: a grid, its device hierarchy and coefficients."""
+    """One ``sb_ctx``: a grid, its device hierarchy and coefficients.
+
+    Contexts own their HBM (hierarchy, Krylov basis, scratch).  ``acquire`` /
+    ``release`` keep idle contexts in a per-(grid, form) pool so repeated
+    public ``gmres_solve`` calls reuse the allocations instead of paying
+    cudaMalloc every solve (an allocator, not a result cache: coefficients
+    are re-uploaded and the hierarchy rebuilt on every use).
+    """
+
+    @classmethod
+    def acquire(cls, grid, viscous_form=STRESS):
+        key = (as_grid(grid), form_code(viscous_form))
+        free = _POOL.get(key)
+        if free:
+            return free.pop()
+        return cls(grid, viscous_form)
+
+    def release(self):
+        if getattr(self, "h", None):
+            _POOL.setdefault((self.grid, self.form), []).append(self)
+
+    def set_stream(self, stream_ptr: int | None):
+        _lib.check(self.lib.sb_set_stream(self.h, stream_ptr or None))
 
     def __init__(self, grid, viscous_form=STRESS):
         import ctypes as C

@@ -79,7 +79,7 @@ class Preconditioner:
         kind = getattr(cfg.kind, "value", cfg.kind)
         if kind != "identity" and not self.grid.can_coarsen():
             raise ValueError(f"grid {self.grid.cells} cannot be coarsened; need even counts >= 4")
-        self.ctx = DeviceContext(self.grid, coeff.viscous_form)
+        self.ctx = DeviceContext.acquire(self.grid, coeff.viscous_form)
         self.ctx.set_coefficients(coeff)
         self._hierarchy = MgHierarchy(self.ctx, coeff) if kind != "identity" else None
         self._pc = precond_c(cfg)
@@ -96,6 +96,12 @@ class Preconditioner:
             _lib.ptr(_f64(r.p.data)), _lib.parr(xu), _lib.ptr(xp), C.byref(vc)))
         self.scalar_vcycles = int(vc.value)
         return StokesVector(FaceField(g, tuple(xu)), CellField(g, xp))
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None:
+            self.ctx = None
+            ctx.release()
 
     # device-level knobs (measurement)
     def set_graphs(self, enabled: bool):
