@@ -20,7 +20,7 @@ enum { F_LAP = 0, F_STRESS = 1, F_BULK = 2 };
 struct LevelDev {
   int n[3];          // cells per internal axis
   int bclo[3], bchi[3];
-  long long s0, s1;  // strides of axes 0 and 1 (axis 2 is contiguous)
+  int s0, s1;        // strides of axes 0 and 1 (axis 2 is contiguous); boxes < 2^31 points
   double h, inv_h, inv_h2, theta;
   const double* mu_c;
   const double* gam_c;
@@ -32,35 +32,33 @@ struct LevelDev {
 __host__ __device__ __forceinline__ bool per(const LevelDev& L, int a) { return L.bclo[a] == BC_PER; }
 
 template <int AX>
-__device__ __forceinline__ long long stride(const LevelDev& L) {
-  return AX == 0 ? L.s0 : (AX == 1 ? L.s1 : 1LL);
+__device__ __forceinline__ int stride(const LevelDev& L) {
+  return AX == 0 ? L.s0 : (AX == 1 ? L.s1 : 1);
 }
 
 // index shift to the +1 / -1 neighbour along AX of coordinate c (periodic wrap)
 template <int AX>
-__device__ __forceinline__ long long dplus(const LevelDev& L, int c) {
-  return (L.bclo[AX] == BC_PER && c == L.n[AX] - 1) ? -(long long)(L.n[AX] - 1) * stride<AX>(L)
-                                                     : stride<AX>(L);
+__device__ __forceinline__ int dplus(const LevelDev& L, int c) {
+  return (L.bclo[AX] == BC_PER && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
 }
 template <int AX>
-__device__ __forceinline__ long long dminus(const LevelDev& L, int c) {
-  return (L.bclo[AX] == BC_PER && c == 0) ? (long long)(L.n[AX] - 1) * stride<AX>(L)
-                                           : -stride<AX>(L);
+__device__ __forceinline__ int dminus(const LevelDev& L, int c) {
+  return (L.bclo[AX] == BC_PER && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
 }
 
-__device__ __forceinline__ double ld(const double* p, long long i) { return __ldg(p + i); }
+__device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + i); }
 
 __host__ __device__ constexpr int edge_of(int a, int b) { return 3 - a - b; }
 
 // (D u)(c) * h accumulated in axis order: ((d0 + d1) + d2)  (operators.py:182-188)
 template <int DIM>
-__device__ __forceinline__ double div_sum(const LevelDev& L, const double* const* u, long long c,
+__device__ __forceinline__ double div_sum(const LevelDev& L, const double* const* u, int c,
                                           const int* ci) {
   double acc = 0.0;
   bool first = true;
 #pragma unroll
   for (int b = 3 - DIM; b < 3; ++b) {
-    long long dp = (b == 0) ? dplus<0>(L, ci[0]) : (b == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+    int dp = (b == 0) ? dplus<0>(L, ci[0]) : (b == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
     // on a wall axis the high face of cell c is c+1 (<= n), never wrapped
     double d = u[b][c + dp] - u[b][c];
     acc = first ? d : acc + d;
@@ -69,41 +67,63 @@ __device__ __forceinline__ double div_sum(const LevelDev& L, const double* const
   return acc;
 }
 
-// One tangential flux of row A across the edge at B-position jj, and the
-// matching diagonal weight w (operators.py:267-300, 331-340; diag :424-434).
-// f is the face index, cA/cB its coordinates, am_d the index shift to the
-// A-neighbour cell below (wrapped).
+// The 7-point u_A neighbourhood of a face: centre and +/- neighbour along each
+// axis (periodic wraps already applied).  Gathered from global memory
+// (gather_ua) or from a shared-memory tile (the fused sweep kernels).
+struct UA7 {
+  double c, p[3], m[3];
+};
+
+template <int DIM, int A>
+__device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, int f, const int* ci) {
+  UA7 s;
+  s.c = ua[f];
+#pragma unroll
+  for (int b = 3 - DIM; b < 3; ++b) {
+    const int dp = b == 0 ? dplus<0>(L, ci[0]) : (b == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+    const int dm = b == 0 ? dminus<0>(L, ci[0]) : (b == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+    // on a wall axis B != A the +/- neighbours are only read away from the wall
+    const bool wallB = b != A && L.bclo[b] != BC_PER;
+    s.p[b] = (wallB && ci[b] == L.n[b] - 1) ? 0.0 : ua[f + dp];
+    s.m[b] = (wallB && ci[b] == 0) ? 0.0 : ua[f + dm];
+  }
+  return s;
+}
+
+// One tangential flux of row A across the edge at B-position jj (lo edge
+// jj = cB, hi edge jj = cB+1) and the matching diagonal weight
+// (operators.py:267-300, 331-340; diag :424-434).  u_hi/u_lo are u_A on the
+// two sides of the edge along B.
 template <int FORM, int A, int B>
-__device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const* u, long long f,
-                                          int cB, int jj, long long am_d, double& flux, double& w) {
-  const long long sB = stride<B>(L);
+__device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const* u, int f, int cB, int jj,
+                                          int am_d, double u_hi, double u_lo, double& flux, double& w) {
+  const int sB = stride<B>(L);
   const int nB = L.n[B];
   const bool pB = per(L, B);
   // edge index: same point with B-coordinate jj (wrapped jj==nB -> 0 on periodic axes)
-  int jw = (pB && jj == nB) ? 0 : jj;
-  long long e = f + (long long)(jw - cB) * sB;
-  double mue = ld(L.mu_e[edge_of(A, B)], e);
+  const int jw = (pB && jj == nB) ? 0 : jj;
+  const int e = f + (jw - cB) * sB;
+  const double mue = ld(L.mu_e[edge_of(A, B)], e);
   double tang;
   int side = -1;  // 0: low wall, 1: high wall
   if (!pB && jj == 0) {
     side = 0;
-    tang = 2.0 * (u[A][e] - 0.0) * L.inv_h;
+    tang = 2.0 * (u_hi - 0.0) * L.inv_h;
   } else if (!pB && jj == nB) {
     side = 1;
-    tang = 2.0 * (0.0 - u[A][e - sB]) * L.inv_h;
+    tang = 2.0 * (0.0 - u_lo) * L.inv_h;
   } else {
-    long long em = (pB && jw == 0) ? e + (long long)(nB - 1) * sB : e - sB;
-    tang = (u[A][e] - u[A][em]) * L.inv_h;
+    tang = (u_hi - u_lo) * L.inv_h;
   }
   double ft = tang;
   if (FORM != F_LAP) {
-    double cross = (u[B][e] - u[B][e + am_d]) * L.inv_h;
+    const double cross = (ld(u[B], e) - ld(u[B], e + am_d)) * L.inv_h;
     ft = tang + cross;
   }
   ft = mue * ft;
   w = mue;
   if (side >= 0) {
-    int kind = side == 0 ? L.bclo[B] : L.bchi[B];
+    const int kind = side == 0 ? L.bclo[B] : L.bchi[B];
     if (kind == BC_FREESLIP) {
       ft = 0.0;
       w = 0.0;
@@ -114,20 +134,18 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const
   flux = ft;
 }
 
-// (A u)_A at unknown face f (coords ci) and the smoother diagonal of that row.
+// (A u)_A at unknown face f (coords ci) from the u_A neighbourhood s and the
+// other components u[B] (global), plus the smoother diagonal of that row.
 // operators.py:303-360 (row form multigrid.py:343-383), diag operators.py:408-439.
 template <int DIM, int FORM, int A>
-__device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, long long f,
-                                           const int* ci, double& diag) {
-  const long long dpA = (A == 0) ? dplus<0>(L, ci[0]) : (A == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
-  const long long dmA = (A == 0) ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
-  const double uf = u[A][f];
-  const double up = u[A][f + dpA];
-  const double um = u[A][f + dmA];
+__device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
+                                                const int* ci, double& diag) {
+  const int dmA = (A == 0) ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+  const double uf = s.c, up = s.p[A], um = s.m[A];
   // cells c_hi = f, c_lo = f + dmA share the face's index (uniform strides)
   const double mu_hi = ld(L.mu_c, f), mu_lo = ld(L.mu_c, f + dmA);
-  double nc_hi = FORM == F_LAP ? mu_hi : 2.0 * mu_hi;
-  double nc_lo = FORM == F_LAP ? mu_lo : 2.0 * mu_lo;
+  const double nc_hi = FORM == F_LAP ? mu_hi : 2.0 * mu_hi;
+  const double nc_lo = FORM == F_LAP ? mu_lo : 2.0 * mu_lo;
   double fn_hi = nc_hi * (up - uf) * L.inv_h;
   double fn_lo = nc_lo * (uf - um) * L.inv_h;
   double ncd_hi = nc_hi, ncd_lo = nc_lo;
@@ -151,51 +169,78 @@ __device__ __forceinline__ double face_row(const LevelDev& L, const double* cons
     double f_lo, f_hi, w_lo, w_hi;
     const int cB = ci[B];
     if (B == 0) {
-      tang_flux<FORM, A, 0>(L, u, f, cB, cB, dmA, f_lo, w_lo);
-      tang_flux<FORM, A, 0>(L, u, f, cB, cB + 1, dmA, f_hi, w_hi);
+      tang_flux<FORM, A, 0>(L, u, f, cB, cB, dmA, uf, s.m[0], f_lo, w_lo);
+      tang_flux<FORM, A, 0>(L, u, f, cB, cB + 1, dmA, s.p[0], uf, f_hi, w_hi);
     } else if (B == 1) {
-      tang_flux<FORM, A, 1>(L, u, f, cB, cB, dmA, f_lo, w_lo);
-      tang_flux<FORM, A, 1>(L, u, f, cB, cB + 1, dmA, f_hi, w_hi);
+      tang_flux<FORM, A, 1>(L, u, f, cB, cB, dmA, uf, s.m[1], f_lo, w_lo);
+      tang_flux<FORM, A, 1>(L, u, f, cB, cB + 1, dmA, s.p[1], uf, f_hi, w_hi);
     } else {
-      tang_flux<FORM, A, 2>(L, u, f, cB, cB, dmA, f_lo, w_lo);
-      tang_flux<FORM, A, 2>(L, u, f, cB, cB + 1, dmA, f_hi, w_hi);
+      tang_flux<FORM, A, 2>(L, u, f, cB, cB, dmA, uf, s.m[2], f_lo, w_lo);
+      tang_flux<FORM, A, 2>(L, u, f, cB, cB + 1, dmA, s.p[2], uf, f_hi, w_hi);
     }
     res = res + (f_hi - f_lo) * L.inv_h;
     dg = dg + (w_lo + w_hi) * L.inv_h2;
   }
   diag = dg;
-  double tr = L.theta == 0.0 ? 0.0 : (L.theta * ld(L.rho_f[A], f)) * uf;
+  const double tr = L.theta == 0.0 ? 0.0 : (L.theta * ld(L.rho_f[A], f)) * uf;
   return tr - res;
 }
 
-// (L_rho phi)(c) and its diagonal (operators.py:206-215, 396-405).
+template <int DIM, int FORM, int A>
+__device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, int f, const int* ci,
+                                           double& diag) {
+  return face_row_core<DIM, FORM, A>(L, gather_ua<DIM, A>(L, u[A], f, ci), u, f, ci, diag);
+}
+
+// (L_rho phi)(c) and its diagonal from the 7-point phi neighbourhood s
+// (operators.py:206-215, 396-405).
 template <int DIM>
-__device__ __forceinline__ double cell_row(const LevelDev& L, const double* phi, long long c,
-                                           const int* ci, double& diag) {
-  const double pc = phi[c];
+__device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s, int c, const int* ci,
+                                                double& diag) {
+  const double pc = s.c;
   double acc = 0.0, dacc = 0.0;
   bool first = true;
 #pragma unroll
   for (int a = 3 - DIM; a < 3; ++a) {
-    const long long s = a == 0 ? L.s0 : (a == 1 ? L.s1 : 1LL);
+    const int st = a == 0 ? L.s0 : (a == 1 ? L.s1 : 1);
     const int n = L.n[a];
     const bool p = per(L, a);
     const double* beta = L.beta_f[a];
     // low face of c is c (index c); high face c+1 (wrapped)
     double g_lo = 0.0, g_hi = 0.0;
-    const long long lo_nb = (p && ci[a] == 0) ? (long long)(n - 1) * s : -s;  // cell below
-    const long long hi_f = (p && ci[a] == n - 1) ? -(long long)(n - 1) * s : s; // face above / cell above
+    const int hi_f = (p && ci[a] == n - 1) ? -(n - 1) * st : st;
     const double b_lo = ld(beta, c);
     const double b_hi = ld(beta, c + hi_f);
-    if (p || ci[a] > 0) g_lo = ((pc - phi[c + lo_nb]) * L.inv_h) * b_lo;
-    if (p || ci[a] < n - 1) g_hi = ((phi[c + hi_f] - pc) * L.inv_h) * b_hi;
-    double d = g_hi - g_lo;
+    if (p || ci[a] > 0) g_lo = ((pc - s.m[a]) * L.inv_h) * b_lo;
+    if (p || ci[a] < n - 1) g_hi = ((s.p[a] - pc) * L.inv_h) * b_hi;
+    const double d = g_hi - g_lo;
     acc = first ? d : acc + d;
     dacc = dacc - (b_lo + b_hi);
     first = false;
   }
   diag = dacc * L.inv_h2;
   return acc * L.inv_h;
+}
+
+template <int DIM>
+__device__ __forceinline__ UA7 gather_cell(const LevelDev& L, const double* phi, int c, const int* ci) {
+  UA7 s;
+  s.c = phi[c];
+#pragma unroll
+  for (int a = 3 - DIM; a < 3; ++a) {
+    const int dp = a == 0 ? dplus<0>(L, ci[0]) : (a == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+    const int dm = a == 0 ? dminus<0>(L, ci[0]) : (a == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+    const bool wall = L.bclo[a] != BC_PER;
+    s.p[a] = (wall && ci[a] == L.n[a] - 1) ? 0.0 : phi[c + dp];
+    s.m[a] = (wall && ci[a] == 0) ? 0.0 : phi[c + dm];
+  }
+  return s;
+}
+
+template <int DIM>
+__device__ __forceinline__ double cell_row(const LevelDev& L, const double* phi, int c, const int* ci,
+                                           double& diag) {
+  return cell_row_core<DIM>(L, gather_cell<DIM>(L, phi, c, ci), c, ci, diag);
 }
 
 }  // namespace sb

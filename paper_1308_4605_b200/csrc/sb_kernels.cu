@@ -25,13 +25,30 @@ inline int grid_for(long long total, int per_block = kThreads, int max_blocks = 
   return (int)b;
 }
 
-__device__ __forceinline__ void decode(const Box& b, unsigned t, int* ci) {
-  const unsigned e2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
-  const unsigned e1 = (unsigned)(b.hi[1] - b.lo[1] + 1);
-  ci[2] = b.lo[2] + (int)(t % e2);
-  t /= e2;
-  ci[1] = b.lo[1] + (int)(t % e1);
-  ci[0] = b.lo[0] + (int)(t / e1);
+// 3D launch over a box: x -> axis 2 (contiguous), y -> axis 1, z -> axis 0.
+// No div/mod in the kernels; one point per thread.
+__device__ __forceinline__ bool box_point(const Box& b, int* ci) {
+  ci[2] = b.lo[2] + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  ci[1] = b.lo[1] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  ci[0] = b.lo[0] + (int)blockIdx.z;
+  return ci[2] <= b.hi[2] && ci[1] <= b.hi[1];
+}
+
+struct L3 {
+  dim3 g, b;
+};
+inline L3 cfg3(int e0, int e1, int e2) {
+  int bx = 32;
+  while (bx > 1 && bx / 2 >= e2) bx >>= 1;
+  int by = kThreads / bx;
+  while (by > 1 && by / 2 >= e1) by >>= 1;
+  L3 c;
+  c.b = dim3(bx, by, 1);
+  c.g = dim3((e2 + bx - 1) / bx, (e1 + by - 1) / by, e0);
+  return c;
+}
+inline L3 cfg3(const Box& b) {
+  return cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, b.hi[2] - b.lo[2] + 1);
 }
 
 inline unsigned box_count(const Box& b) {
@@ -39,7 +56,7 @@ inline unsigned box_count(const Box& b) {
          (unsigned)(b.hi[2] - b.lo[2] + 1);
 }
 
-__device__ __forceinline__ long long lin(const LevelDev& L, const int* ci) {
+__device__ __forceinline__ int lin(const LevelDev& L, const int* ci) {
   return ci[0] * L.s0 + ci[1] * L.s1 + ci[2];
 }
 
@@ -88,19 +105,19 @@ __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
   const int off = (L.bclo[A] == BC_PER) ? 0 : 1;
-  const unsigned e1 = (unsigned)(b.hi[1] - b.lo[1] + 1);
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const unsigned tt = t % half2, r = t / half2;
+  {
     int ci[3];
-    ci[1] = b.lo[1] + (int)(r % e1);
-    ci[0] = b.lo[0] + (int)(r / e1);
-    const int k = b.lo[2] + ((parity + off - ci[0] - ci[1] - b.lo[2]) & 1) + 2 * (int)tt;
-    if (k > b.hi[2]) continue;
+    const int tt = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    ci[1] = b.lo[1] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    ci[0] = b.lo[0] + (int)blockIdx.z;
+    if (ci[1] > b.hi[1]) return;
+    const int k = b.lo[2] + ((parity + off - ci[0] - ci[1] - b.lo[2]) & 1) + 2 * tt;
+    if (k > b.hi[2]) return;
     ci[2] = k;
-    const long long f = lin(L, ci);
+    const int f = lin(L, ci);
     if (PHASE == 1) {
       u.p[A][f] = tmp[f];
-      continue;
+      return;
     }
     const double* uc[3] = {u.p[0], u.p[1], u.p[2]};
     double dg;
@@ -116,19 +133,19 @@ template <int DIM, int PHASE>
 __global__ void __launch_bounds__(kThreads)
 k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
-  const unsigned e1 = (unsigned)(b.hi[1] - b.lo[1] + 1);
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const unsigned tt = t % half2, r = t / half2;
+  {
     int ci[3];
-    ci[1] = b.lo[1] + (int)(r % e1);
-    ci[0] = b.lo[0] + (int)(r / e1);
-    const int k = b.lo[2] + ((parity - ci[0] - ci[1] - b.lo[2]) & 1) + 2 * (int)tt;
-    if (k > b.hi[2]) continue;
+    const int tt = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    ci[1] = b.lo[1] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    ci[0] = b.lo[0] + (int)blockIdx.z;
+    if (ci[1] > b.hi[1]) return;
+    const int k = b.lo[2] + ((parity - ci[0] - ci[1] - b.lo[2]) & 1) + 2 * tt;
+    if (k > b.hi[2]) return;
     ci[2] = k;
-    const long long c = lin(L, ci);
+    const int c = lin(L, ci);
     if (PHASE == 1) {
       phi[c] = tmp[c];
-      continue;
+      return;
     }
     double dg;
     const double lp = cell_row<DIM>(L, phi, c, ci, dg);
@@ -146,56 +163,104 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
 template <int DIM, int FORM, int A>
 __device__ __forceinline__ double face_resid_at(const LevelDev& L, const double* const* u,
                                                 const double* rhs, const int* ci) {
-  const long long f = lin(L, ci);
+  const int f = lin(L, ci);
   double dg;
   const double au = face_row<DIM, FORM, A>(L, u, f, ci, dg);
   return __ldg(rhs + f) - au;
 }
 
+// Tangential 2^(d-1) mean of fine residuals at fine normal index fa, coarse
+// tangential indices in C (mean along B1 first, then B2: multigrid.py:112-119).
+template <int DIM, int FORM, int A>
+__device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* const* u, const double* rhs,
+                                              const int* C, int fa) {
+  using O = Others<DIM, A>;
+  int fi[3] = {2 * C[0], 2 * C[1], 2 * C[2]};
+  if (DIM == 2) fi[0] = 0;
+  fi[A] = fa;
+  if (DIM == 3) {
+    double p[2];
+#pragma unroll 1
+    for (int t2 = 0; t2 < 2; ++t2) {
+      int q0[3] = {fi[0], fi[1], fi[2]}, q1[3] = {fi[0], fi[1], fi[2]};
+      q0[O::B2] += t2;
+      q1[O::B2] += t2;
+      q1[O::B1] += 1;
+      const double m0 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q0);
+      const double m1 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q1);
+      p[t2] = 0.5 * (m0 + m1);
+    }
+    return 0.5 * (p[0] + p[1]);
+  }
+  int q1[3] = {fi[0], fi[1], fi[2]};
+  q1[O::B1] += 1;
+  const double m0 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, fi);
+  const double m1 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q1);
+  return 0.5 * (m0 + m1);
+}
+
+// Fused residual -> restriction, each fine residual evaluated once.
+// A == 2 (contiguous axis): lanes run along coarse K; t(2K-1) is the previous
+// lane's t(2K+1) (warp shuffle), lane 0 evaluates it itself.
+template <int DIM, int FORM>
+__global__ void __launch_bounds__(kThreads)
+k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
+            Box cb) {
+  constexpr int A = 2;
+  int C[3];
+  C[2] = cb.lo[2] + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  C[1] = cb.lo[1] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  C[0] = cb.lo[0] + (int)blockIdx.z;
+  const bool ok = C[2] <= cb.hi[2] && C[1] <= cb.hi[1];
+  int Cs[3] = {C[0], ok ? C[1] : cb.lo[1], ok ? C[2] : cb.lo[2]};
+  const double t0 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, 2 * Cs[A]);
+  const double t1 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, 2 * Cs[A] + 1);
+  double tm = __shfl_up_sync(0xffffffffu, t1, 1);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0 || Cs[A] == cb.lo[A]) {
+    int fa = 2 * Cs[A] - 1;
+    if (fa < 0) fa += Lf.n[A];
+    tm = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, fa);
+  }
+  if (ok) coarse[lin(Lc, C)] = (0.25 * tm + 0.5 * t0) + 0.25 * t1;
+}
+
+// A in {0, 1}: lanes along coarse axis 2 (coalesced), each thread marches a
+// chunk of coarse indices along A, carrying t(2C+1) into the next t(2C-1).
 template <int DIM, int FORM, int A>
 __global__ void __launch_bounds__(kThreads)
-k_face_rr(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs,
-          double* __restrict__ coarse, Box cb, unsigned total) {
-  using O = Others<DIM, A>;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    int C[3];
-    decode(cb, t, C);
-    double tv[3];
-#pragma unroll
-    for (int o = -1; o <= 1; ++o) {
-      int fi[3] = {2 * C[0], 2 * C[1], 2 * C[2]};
-      int fa = 2 * C[A] + o;
-      if (fa < 0) fa += Lf.n[A];  // periodic wrap (wall coarse faces start at 1)
-      fi[A] = fa;
-      if (DIM == 3) {
-        double p[2];
-#pragma unroll
-        for (int t2 = 0; t2 < 2; ++t2) {
-          int q0[3] = {fi[0], fi[1], fi[2]}, q1[3] = {fi[0], fi[1], fi[2]};
-          q0[O::B2] += t2;
-          q1[O::B2] += t2;
-          q1[O::B1] += 1;
-          const double m0 = face_resid_at<DIM, FORM, A>(Lf, u.p, rhs, q0);
-          const double m1 = face_resid_at<DIM, FORM, A>(Lf, u.p, rhs, q1);
-          p[t2] = 0.5 * (m0 + m1);
-        }
-        tv[o + 1] = 0.5 * (p[0] + p[1]);
-      } else {
-        int q1[3] = {fi[0], fi[1], fi[2]};
-        q1[O::B1] += 1;
-        const double m0 = face_resid_at<DIM, FORM, A>(Lf, u.p, rhs, fi);
-        const double m1 = face_resid_at<DIM, FORM, A>(Lf, u.p, rhs, q1);
-        tv[o + 1] = 0.5 * (m0 + m1);
-      }
-    }
-    coarse[lin(Lc, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
+k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
+            Box cb, int chunk) {
+  constexpr int T = (A == 0) ? 1 : 0;  // the other non-contiguous axis
+  int C[3];
+  C[2] = cb.lo[2] + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (DIM == 3) {
+    C[T] = cb.lo[T] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    if (C[T] > cb.hi[T]) return;
+  } else {
+    C[0] = 0;
+  }
+  if (C[2] > cb.hi[2]) return;
+  const int a0 = cb.lo[A] + (int)blockIdx.z * chunk;
+  const int a1 = min(a0 + chunk - 1, cb.hi[A]);
+  C[A] = a0;
+  int fa = 2 * a0 - 1;
+  if (fa < 0) fa += Lf.n[A];
+  double tm = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, fa);
+#pragma unroll 1
+  for (int c = a0; c <= a1; ++c) {
+    C[A] = c;
+    const double t0 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, 2 * c);
+    const double t1 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, 2 * c + 1);
+    coarse[lin(Lc, C)] = (0.25 * tm + 0.5 * t0) + 0.25 * t1;
+    tm = t1;
   }
 }
 
 template <int DIM>
 __device__ __forceinline__ double cell_resid_at(const LevelDev& L, const double* phi,
                                                 const double* rhs, const int* ci) {
-  const long long c = lin(L, ci);
+  const int c = lin(L, ci);
   double dg;
   const double lp = cell_row<DIM>(L, phi, c, ci, dg);
   return __ldg(rhs + c) - lp;
@@ -205,16 +270,16 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict__ rhs,
           double* __restrict__ coarse, Box cb, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int C[3];
-    decode(cb, t, C);
+    if (!box_point(cb, C)) return;
     double out;
     if (DIM == 3) {
       double s[2];
-#pragma unroll
+#pragma unroll 1
       for (int k = 0; k < 2; ++k) {
         double q[2];
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < 2; ++j) {
           int a0[3] = {2 * C[0], 2 * C[1] + j, 2 * C[2] + k};
           int a1[3] = {2 * C[0] + 1, 2 * C[1] + j, 2 * C[2] + k};
@@ -258,9 +323,9 @@ __global__ void __launch_bounds__(kThreads)
 k_face_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
           Box fb, unsigned total) {
   using O = Others<DIM, A>;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int F[3];
-    decode(fb, t, F);
+    if (!box_point(fb, F)) return;
     int J1, n1, J2 = 0, n2 = 0;
     tang_pair(Lc, O::B1, F[O::B1], J1, n1);
     if (DIM == 3) tang_pair(Lc, O::B2, F[O::B2], J2, n2);
@@ -296,7 +361,7 @@ k_face_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* _
       if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A]) I2 = 0;
       v = 0.5 * (T(I) + T(I2));
     }
-    const long long f = lin(Lf, F);
+    const int f = lin(Lf, F);
     fine[f] = fine[f] + v;
   }
 }
@@ -305,11 +370,11 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
           Box fb, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int F[3];
-    decode(fb, t, F);
+    if (!box_point(fb, F)) return;
     int C[3] = {DIM == 3 ? F[0] >> 1 : 0, F[1] >> 1, F[2] >> 1};
-    const long long f = lin(Lf, F);
+    const int f = lin(Lf, F);
     fine[f] = fine[f] + __ldg(coarse + lin(Lc, C));
   }
 }
@@ -335,8 +400,8 @@ __device__ __forceinline__ bool in_cell(const LevelDev& L, const int* ci) {
 
 // (G q)_A at face f (operators.py:191-198): (q(f) - q(f-1))/h, wall faces 0
 template <int A>
-__device__ __forceinline__ double grad_at(const LevelDev& L, const double* q, long long f, const int* ci) {
-  const long long dm = A == 0 ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+__device__ __forceinline__ double grad_at(const LevelDev& L, const double* q, int f, const int* ci) {
+  const int dm = A == 0 ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
   return (__ldg(q + f) - __ldg(q + f + dm)) * L.inv_h;
 }
 
@@ -344,7 +409,7 @@ template <int DIM, int FORM, int A>
 __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u, const double* p,
                                        double* out, const int* ci) {
   if (!in_face(L, A, ci)) return;
-  const long long f = lin(L, ci);
+  const int f = lin(L, ci);
   if (is_wall_face(L, A, ci)) {
     out[f] = 0.0;
     return;
@@ -358,14 +423,14 @@ template <int DIM, int FORM>
 __global__ void __launch_bounds__(kThreads)
 k_apply_M(LevelDev L, CPtr3 u, const double* __restrict__ p, Ptr3 out_u, double* __restrict__ out_p,
           Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     if (DIM == 3) m_face<3, FORM, 0>(L, u.p, p, out_u.p[0], ci);
     m_face<DIM, FORM, 1>(L, u.p, p, out_u.p[1], ci);
     m_face<DIM, FORM, 2>(L, u.p, p, out_u.p[2], ci);
     if (in_cell(L, ci)) {
-      const long long c = lin(L, ci);
+      const int c = lin(L, ci);
       out_p[c] = -(div_sum<DIM>(L, u.p, c, ci) * L.inv_h);
     }
   }
@@ -375,7 +440,7 @@ template <int DIM, int FORM, int A>
 __device__ __forceinline__ void r_face(const LevelDev& L, const double* const* x, const double* const* rhs,
                                        const double* q, double* out, const int* ci) {
   if (!in_face(L, A, ci)) return;
-  const long long f = lin(L, ci);
+  const int f = lin(L, ci);
   if (is_wall_face(L, A, ci)) {
     out[f] = 0.0;
     return;
@@ -399,9 +464,9 @@ template <int DIM, int FORM>
 __global__ void __launch_bounds__(kThreads)
 k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Ptr3 out, Box b,
                 unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     if (DIM == 3) r_face<3, FORM, 0>(L, x.p, rhs.p, q, out.p[0], ci);
     r_face<DIM, FORM, 1>(L, x.p, rhs.p, q, out.p[1], ci);
     r_face<DIM, FORM, 2>(L, x.p, rhs.p, q, out.p[2], ci);
@@ -411,10 +476,10 @@ k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Pt
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_residual(LevelDev L, const double* x, const double* rhs, double* out, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long c = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int c = lin(L, ci);
     double dg;
     const double lp = cell_row<DIM>(L, x, c, ci, dg);
     out[c] = rhs != nullptr ? __ldg(rhs + c) - lp : lp;
@@ -425,15 +490,15 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_div_add(LevelDev L, CPtr3 u, const double* __restrict__ rp, double* __restrict__ out, Box b,
           unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long c = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int c = lin(L, ci);
     out[c] = div_sum<DIM>(L, u.p, c, ci) * L.inv_h + __ldg(rp + c);
   }
 }
 
-__device__ __forceinline__ double schur_v(const LevelDev& L, int form, long long c) {
+__device__ __forceinline__ double schur_v(const LevelDev& L, int form, int c) {
   const double mu = __ldg(L.mu_c + c);
   if (form == F_LAP) return mu;
   if (form == F_STRESS) return 2.0 * mu;
@@ -443,7 +508,7 @@ __device__ __forceinline__ double schur_v(const LevelDev& L, int form, long long
 template <int A>
 __device__ __forceinline__ void glue_face(const LevelDev& L, double* xu, const double* phi, const int* ci) {
   if (!in_face(L, A, ci) || is_wall_face(L, A, ci)) return;
-  const long long f = lin(L, ci);
+  const int f = lin(L, ci);
   xu[f] = xu[f] - grad_at<A>(L, phi, f, ci) * __ldg(L.beta_f[A] + f);
 }
 
@@ -451,14 +516,14 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_p1_glue(LevelDev L, int form, Ptr3 xu, const double* __restrict__ phi, const double* __restrict__ bc,
           double* __restrict__ xp, double sign, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     if (DIM == 3) glue_face<0>(L, xu.p[0], phi, ci);
     glue_face<1>(L, xu.p[1], phi, ci);
     glue_face<2>(L, xu.p[2], phi, ci);
     if (in_cell(L, ci)) {
-      const long long c = lin(L, ci);
+      const int c = lin(L, ci);
       const double s = schur_v(L, form, c) * __ldg(bc + c) - L.theta * __ldg(phi + c);
       xp[c] = s * sign;
     }
@@ -468,10 +533,10 @@ k_p1_glue(LevelDev L, int form, Ptr3 xu, const double* __restrict__ phi, const d
 __global__ void __launch_bounds__(kThreads)
 k_schur(LevelDev L, int form, const double* __restrict__ r, const double* __restrict__ phi,
         double* __restrict__ out, double sign, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long c = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int c = lin(L, ci);
     double s;
     if (phi != nullptr) s = (-L.theta) * __ldg(phi + c) + schur_v(L, form, c) * __ldg(r + c);
     else s = schur_v(L, form, c) * __ldg(r + c);
@@ -483,7 +548,7 @@ template <int A>
 __device__ __forceinline__ void subg_face(const LevelDev& L, const double* ru, const double* q, double* out,
                                           const int* ci) {
   if (!in_face(L, A, ci)) return;
-  const long long f = lin(L, ci);
+  const int f = lin(L, ci);
   if (is_wall_face(L, A, ci)) {
     out[f] = 0.0;
     return;
@@ -494,9 +559,9 @@ __device__ __forceinline__ void subg_face(const LevelDev& L, const double* ru, c
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_face_sub_grad(LevelDev L, CPtr3 ru, const double* __restrict__ q, Ptr3 out, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     if (DIM == 3) subg_face<0>(L, ru.p[0], q, out.p[0], ci);
     subg_face<1>(L, ru.p[1], q, out.p[1], ci);
     subg_face<2>(L, ru.p[2], q, out.p[2], ci);
@@ -510,9 +575,9 @@ k_face_sub_grad(LevelDev L, CPtr3 ru, const double* __restrict__ q, Ptr3 out, Bo
 template <int DIM>
 __global__ void k_coarsen_cellmean(LevelDev Lf, LevelDev Lc, const double* __restrict__ fine,
                                    double* __restrict__ coarse, Box cb, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int C[3];
-    decode(cb, t, C);
+    if (!box_point(cb, C)) return;
     auto at = [&](int i, int j, int k) {
       int q[3] = {DIM == 3 ? 2 * C[0] + i : 0, 2 * C[1] + j, 2 * C[2] + k};
       return __ldg(fine + lin(Lf, q));
@@ -540,9 +605,9 @@ template <int DIM, int A>
 __global__ void k_coarsen_face(LevelDev Lf, LevelDev Lc, const double* __restrict__ fine,
                                double* __restrict__ coarse, Box cb, unsigned total) {
   using O = Others<DIM, A>;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int C[3];
-    decode(cb, t, C);
+    if (!box_point(cb, C)) return;
     int q[3] = {2 * C[0], 2 * C[1], 2 * C[2]};
     double out;
     if (DIM == 3) {
@@ -571,9 +636,9 @@ __global__ void k_coarsen_face(LevelDev Lf, LevelDev Lc, const double* __restric
 template <int DIM>
 __global__ void k_coarsen_edge(LevelDev Lf, LevelDev Lc, int e, const double* __restrict__ fine,
                                double* __restrict__ coarse, Box cb, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int C[3];
-    decode(cb, t, C);
+    if (!box_point(cb, C)) return;
     int q[3] = {2 * C[0], 2 * C[1], 2 * C[2]};
     if (DIM == 2) q[0] = 0;
     double out;
@@ -591,10 +656,10 @@ __global__ void k_coarsen_edge(LevelDev Lf, LevelDev Lc, int e, const double* __
 
 __global__ void k_beta(LevelDev L, int A, const double* __restrict__ rho, double* __restrict__ beta,
                        int* flag, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long f = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int f = lin(L, ci);
     const double r = rho[f];
     if (!(r > 0.0)) atomicOr(flag, 1);
     const bool wall = L.bclo[A] != BC_PER && (ci[A] == 0 || ci[A] == L.n[A]);
@@ -614,9 +679,9 @@ __device__ __forceinline__ void chk_face(const LevelDev& L, const int* ci, int* 
 
 template <int DIM, int FORM>
 __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     if (DIM == 3) chk_face<3, FORM, 0>(L, ci, flags);
     chk_face<DIM, FORM, 1>(L, ci, flags);
     chk_face<DIM, FORM, 2>(L, ci, flags);
@@ -629,9 +694,9 @@ __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
 }
 
 __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
+    if (!box_point(b, ci)) return;
     x[lin(L, ci)] = v;
   }
 }
@@ -639,19 +704,19 @@ __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned tota
 __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double inv_count, Box b,
                                unsigned total) {
   const double m = sum[0] * inv_count;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long i = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int i = lin(L, ci);
     x[i] = x[i] - m;
   }
 }
 
 __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, Box b, unsigned total) {
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  {
     int ci[3];
-    decode(b, t, ci);
-    const long long i = lin(L, ci);
+    if (!box_point(b, ci)) return;
+    const int i = lin(L, ci);
     y[i] = y[i] + x[i];
   }
 }
@@ -660,7 +725,7 @@ __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, 
 // flat-vector kernels for GMRES (deterministic two-stage reductions)
 // ---------------------------------------------------------------------------
 
-constexpr int kRedBlocks = kSMs * 2;   // partial-sum slots per reduction
+constexpr int kRedBlocks = kSMs * 8;   // partial-sum slots per reduction (8 CTAs/SM)
 constexpr int kMaxVec = 128;           // max basis vectors in one multi-dot
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -670,6 +735,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // partials[i*kRedBlocks + block] = sum over this block's elements of V_i . w
+// (each thread keeps two double2 of w in registers: 2 x 16 B loads in flight per V_i)
 __global__ void __launch_bounds__(kThreads)
 k_multi_dot(const double* __restrict__ V, long long vstride, int nv, const double* __restrict__ w,
             long long n2, double* __restrict__ partials) {
@@ -678,13 +744,17 @@ k_multi_dot(const double* __restrict__ V, long long vstride, int nv, const doubl
   for (int i = threadIdx.x; i < nv * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
   __syncthreads();
   const double2* w2 = reinterpret_cast<const double2*>(w);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2;
-       e += (long long)gridDim.x * blockDim.x) {
-    double2 wv = e < n2 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    const double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    const double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
     for (int i = 0; i < nv; ++i) {
       const double2* v2 = reinterpret_cast<const double2*>(V + i * vstride);
-      double2 vv = e < n2 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
-      double s = warp_sum(vv.x * wv.x + vv.y * wv.y);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      double s = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
       if (lane == 0) acc[i][warp] += s;
     }
   }
@@ -696,7 +766,9 @@ k_multi_dot(const double* __restrict__ V, long long vstride, int nv, const doubl
   }
 }
 
-// w -= sum_i h_i V_i ; then partials of V_i . w (mode 0) or w . w (mode 1)
+// w -= sum_i h_i V_i ; then partials of V_i . w (mode 0) or w . w (mode 1).
+// The second read of V_i (mode 0) follows the first within the same thread
+// and hits L1/L2; DRAM sees each V_i once.
 __global__ void __launch_bounds__(kThreads)
 k_update_dot(const double* __restrict__ V, long long vstride, int nv, const double* __restrict__ h,
              double* __restrict__ w, long long n2, double* __restrict__ partials, int mode) {
@@ -708,26 +780,34 @@ k_update_dot(const double* __restrict__ V, long long vstride, int nv, const doub
   for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
   double2* w2 = reinterpret_cast<double2*>(w);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2;
-       e += (long long)gridDim.x * blockDim.x) {
-    const bool ok = e < n2;
-    double2 wv = ok ? w2[e] : make_double2(0.0, 0.0);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    double2 w0 = ok0 ? w2[e] : make_double2(0.0, 0.0);
+    double2 wv1 = ok1 ? w2[e1] : make_double2(0.0, 0.0);
     for (int i = 0; i < nv; ++i) {
       const double2* v2 = reinterpret_cast<const double2*>(V + i * vstride);
-      double2 vv = ok ? __ldg(v2 + e) : make_double2(0.0, 0.0);
-      wv.x -= hs[i] * vv.x;
-      wv.y -= hs[i] * vv.y;
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double hi = hs[i];
+      w0.x -= hi * a.x;
+      w0.y -= hi * a.y;
+      wv1.x -= hi * b.x;
+      wv1.y -= hi * b.y;
     }
-    if (ok) w2[e] = wv;
+    if (ok0) w2[e] = w0;
+    if (ok1) w2[e1] = wv1;
     if (mode == 0) {
       for (int i = 0; i < nv; ++i) {
         const double2* v2 = reinterpret_cast<const double2*>(V + i * vstride);
-        double2 vv = ok ? __ldg(v2 + e) : make_double2(0.0, 0.0);
-        double s = warp_sum(vv.x * wv.x + vv.y * wv.y);
+        const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+        const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+        double s = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
         if (lane == 0) acc[i][warp] += s;
       }
     } else {
-      double s = warp_sum(wv.x * wv.x + wv.y * wv.y);
+      double s = warp_sum((w0.x * w0.x + w0.y * w0.y) + (wv1.x * wv1.x + wv1.y * wv1.y));
       if (lane == 0) acc[0][warp] += s;
     }
   }
@@ -859,15 +939,15 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
   Box b = face_box(L, DIM, A);
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
-  const unsigned rows = (unsigned)(b.hi[0] - b.lo[0] + 1) * (unsigned)(b.hi[1] - b.lo[1] + 1);
-  const unsigned total = rows * half2;
-  const int g = grid_for(total);
+  const unsigned total = half2;
+  const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
+  const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    k_face_colour<DIM, FM, A, 0><<<g, kThreads, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    k_face_colour<DIM, FM, A, 0><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
   } else {
     ++g_kernel_launches;
-    k_face_colour<DIM, FM, A, 2><<<g, kThreads, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
-    k_face_colour<DIM, FM, A, 1><<<g, kThreads, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
+    k_face_colour<DIM, FM, A, 2><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
+    k_face_colour<DIM, FM, A, 1><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -910,15 +990,15 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
   Box b = cell_box(L);
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
-  const unsigned rows = (unsigned)L.n[0] * (unsigned)L.n[1];
-  const unsigned total = rows * half2;
-  const int g = grid_for(total);
+  const unsigned total = half2;
+  const L3 c3 = cfg3(L.n[0], L.n[1], (int)half2);
+  const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    k_cell_colour<DIM, 0><<<g, kThreads, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
+    k_cell_colour<DIM, 0><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
   } else {
     ++g_kernel_launches;
-    k_cell_colour<DIM, 2><<<g, kThreads, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
-    k_cell_colour<DIM, 1><<<g, kThreads, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
+    k_cell_colour<DIM, 2><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
+    k_cell_colour<DIM, 1><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -942,8 +1022,29 @@ template <int DIM, int FM, int A>
 static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CPtr3 u, const double* rhs,
                       double* coarse) {
   Box cb = face_box(Lc, DIM, A);
-  const unsigned total = box_count(cb);
-  k_face_rr<DIM, FM, A><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, total);
+  if (A == 2) {
+    const L3 c3 = cfg3(cb.hi[0] - cb.lo[0] + 1, cb.hi[1] - cb.lo[1] + 1, cb.hi[2] - cb.lo[2] + 1);
+    dim3 b = c3.b, g = c3.g;
+    if (b.x < 32) {  // the shuffle needs whole warps along K
+      b = dim3(32, kThreads / 32, 1);
+      g = dim3((cb.hi[2] - cb.lo[2] + 32) / 32, (cb.hi[1] - cb.lo[1] + b.y) / b.y, cb.hi[0] - cb.lo[0] + 1);
+    }
+    k_face_rr_c<DIM, FM><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
+  } else {
+    constexpr int T = (A == 0) ? 1 : 0;
+    const int e2 = cb.hi[2] - cb.lo[2] + 1;
+    const int eT = DIM == 3 ? cb.hi[T] - cb.lo[T] + 1 : 1;
+    const int eA = cb.hi[A] - cb.lo[A] + 1;
+    const L3 c3 = cfg3(1, eT, e2);
+    // chunk along A: enough CTAs to fill the machine, at least 4 coarse faces per thread
+    long long cols = (long long)c3.g.x * c3.g.y;
+    int nchunk = (int)std::max<long long>(1, std::min<long long>(eA / 4, (kSMs * 8 + cols - 1) / cols));
+    if (nchunk < 1) nchunk = 1;
+    const int chunk = (eA + nchunk - 1) / nchunk;
+    nchunk = (eA + chunk - 1) / chunk;
+    dim3 g(c3.g.x, c3.g.y, nchunk);
+    k_face_rr_m<DIM, FM, A><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
+  }
 }
 
 void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int form,
@@ -966,8 +1067,8 @@ void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
   ++g_kernel_launches;
   Box cb = cell_box(Lc);
   const unsigned total = box_count(cb);
-  if (dim == 3) k_cell_rr<3><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
-  else k_cell_rr<2><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+  if (dim == 3) k_cell_rr<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+  else k_cell_rr<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
 }
 
 void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
@@ -975,14 +1076,13 @@ void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   ++g_kernel_launches;
   Box fb = face_box(Lf, dim, A);
   const unsigned total = box_count(fb);
-  const int g = grid_for(total);
   if (dim == 3) {
-    if (A == 0) k_face_pa<3, 0><<<g, kThreads, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else if (A == 1) k_face_pa<3, 1><<<g, kThreads, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else k_face_pa<3, 2><<<g, kThreads, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    if (A == 0) k_face_pa<3, 0><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    else if (A == 1) k_face_pa<3, 1><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    else k_face_pa<3, 2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
   } else {
-    if (A == 1) k_face_pa<2, 1><<<g, kThreads, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else k_face_pa<2, 2><<<g, kThreads, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    if (A == 1) k_face_pa<2, 1><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    else k_face_pa<2, 2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
   }
 }
 
@@ -991,8 +1091,8 @@ void launch_cell_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   ++g_kernel_launches;
   Box fb = cell_box(Lf);
   const unsigned total = box_count(fb);
-  if (dim == 3) k_cell_pa<3><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
-  else k_cell_pa<2><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
+  if (dim == 3) k_cell_pa<3><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
+  else k_cell_pa<2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
 }
 
 // padded box covering every array of the level
@@ -1010,10 +1110,9 @@ void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 
   ++g_kernel_launches;
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  const int g = grid_for(total);
   SB_DISPATCH_FORM(form, {
-    if (dim == 3) k_apply_M<3, FM><<<g, kThreads, 0, s>>>(L, u, p, out_u, out_p, b, total);
-    else k_apply_M<2, FM><<<g, kThreads, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    if (dim == 3) k_apply_M<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    else k_apply_M<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
   });
 }
 
@@ -1022,10 +1121,9 @@ void launch_face_residual(cudaStream_t s, const LevelDev& L, int dim, int form, 
   ++g_kernel_launches;
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  const int g = grid_for(total);
   SB_DISPATCH_FORM(form, {
-    if (dim == 3) k_face_residual<3, FM><<<g, kThreads, 0, s>>>(L, x, rhs, q, out, b, total);
-    else k_face_residual<2, FM><<<g, kThreads, 0, s>>>(L, x, rhs, q, out, b, total);
+    if (dim == 3) k_face_residual<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, q, out, b, total);
+    else k_face_residual<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, q, out, b, total);
   });
 }
 
@@ -1034,15 +1132,15 @@ void launch_cell_residual(cudaStream_t s, const LevelDev& L, int dim, const doub
   ++g_kernel_launches;
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_cell_residual<3><<<grid_for(total), kThreads, 0, s>>>(L, x, rhs, out, b, total);
-  else k_cell_residual<2><<<grid_for(total), kThreads, 0, s>>>(L, x, rhs, out, b, total);
+  if (dim == 3) k_cell_residual<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b, total);
+  else k_cell_residual<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b, total);
 }
 
 void launch_div_add(cudaStream_t s, const LevelDev& L, int dim, CPtr3 u, const double* rp, double* out) {
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_div_add<3><<<grid_for(total), kThreads, 0, s>>>(L, u, rp, out, b, total);
-  else k_div_add<2><<<grid_for(total), kThreads, 0, s>>>(L, u, rp, out, b, total);
+  if (dim == 3) k_div_add<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, rp, out, b, total);
+  else k_div_add<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, rp, out, b, total);
 }
 
 void launch_p1_glue(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 xu, const double* phi,
@@ -1050,8 +1148,8 @@ void launch_p1_glue(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 x
   ++g_kernel_launches;
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_p1_glue<3><<<grid_for(total), kThreads, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
-  else k_p1_glue<2><<<grid_for(total), kThreads, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
+  if (dim == 3) k_p1_glue<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
+  else k_p1_glue<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
 }
 
 void launch_schur(cudaStream_t s, const LevelDev& L, int form, const double* r, const double* phi,
@@ -1059,14 +1157,14 @@ void launch_schur(cudaStream_t s, const LevelDev& L, int form, const double* r, 
   ++g_kernel_launches;
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  k_schur<<<grid_for(total), kThreads, 0, s>>>(L, form, r, phi, out, sign, b, total);
+  k_schur<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, r, phi, out, sign, b, total);
 }
 
 void launch_face_sub_grad(cudaStream_t s, const LevelDev& L, int dim, CPtr3 ru, const double* q, Ptr3 out) {
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_face_sub_grad<3><<<grid_for(total), kThreads, 0, s>>>(L, ru, q, out, b, total);
-  else k_face_sub_grad<2><<<grid_for(total), kThreads, 0, s>>>(L, ru, q, out, b, total);
+  if (dim == 3) k_face_sub_grad<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, ru, q, out, b, total);
+  else k_face_sub_grad<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, ru, q, out, b, total);
 }
 
 void launch_coarsen_cellmean(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
@@ -1074,8 +1172,8 @@ void launch_coarsen_cellmean(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   ++g_kernel_launches;
   Box cb = cell_box(Lc);
   const unsigned total = box_count(cb);
-  if (dim == 3) k_coarsen_cellmean<3><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-  else k_coarsen_cellmean<2><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+  if (dim == 3) k_coarsen_cellmean<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+  else k_coarsen_cellmean<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
 }
 
 void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
@@ -1084,14 +1182,13 @@ void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
   Box cb = cell_box(Lc);
   if (Lc.bclo[A] != BC_PER) cb.hi[A] = Lc.n[A];  // all faces incl. wall boundary
   const unsigned total = box_count(cb);
-  const int g = grid_for(total);
   if (dim == 3) {
-    if (A == 0) k_coarsen_face<3, 0><<<g, kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else if (A == 1) k_coarsen_face<3, 1><<<g, kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else k_coarsen_face<3, 2><<<g, kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    if (A == 0) k_coarsen_face<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    else if (A == 1) k_coarsen_face<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    else k_coarsen_face<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
   } else {
-    if (A == 1) k_coarsen_face<2, 1><<<g, kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else k_coarsen_face<2, 2><<<g, kThreads, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    if (A == 1) k_coarsen_face<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    else k_coarsen_face<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
   }
 }
 
@@ -1102,44 +1199,43 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
   for (int a = 3 - dim; a < 3; ++a)
     if (a != e && Lc.bclo[a] != BC_PER) cb.hi[a] = Lc.n[a];
   const unsigned total = box_count(cb);
-  if (dim == 3) k_coarsen_edge<3><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
-  else k_coarsen_edge<2><<<grid_for(total), kThreads, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
+  if (dim == 3) k_coarsen_edge<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
+  else k_coarsen_edge<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
 }
 
 void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag) {
   Box b = cell_box(L);
   if (L.bclo[A] != BC_PER) b.hi[A] = L.n[A];
   const unsigned total = box_count(b);
-  k_beta<<<grid_for(total), kThreads, 0, s>>>(L, A, rho, beta, flag, b, total);
+  k_beta<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, rho, beta, flag, b, total);
 }
 
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags) {
   ++g_kernel_launches;
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  const int g = grid_for(total);
   SB_DISPATCH_FORM(form, {
   ++g_kernel_launches;
-    if (dim == 3) k_check_diag<3, FM><<<g, kThreads, 0, s>>>(L, flags, b, total);
-    else k_check_diag<2, FM><<<g, kThreads, 0, s>>>(L, flags, b, total);
+    if (dim == 3) k_check_diag<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
+    else k_check_diag<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
   });
 }
 
 void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double v) {
   const unsigned total = box_count(b);
-  k_box_fill<<<grid_for(total), kThreads, 0, s>>>(L, x, v, b, total);
+  k_box_fill<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, v, b, total);
 }
 
 void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, const double* sum,
                            double inv_count) {
   ++g_kernel_launches;
   const unsigned total = box_count(b);
-  k_box_sub_mean<<<grid_for(total), kThreads, 0, s>>>(L, x, sum, inv_count, b, total);
+  k_box_sub_mean<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, sum, inv_count, b, total);
 }
 
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x) {
   const unsigned total = box_count(b);
-  k_box_axpy<<<grid_for(total), kThreads, 0, s>>>(L, y, x, b, total);
+  k_box_axpy<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, y, x, b, total);
 }
 
 void launch_multi_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* w,

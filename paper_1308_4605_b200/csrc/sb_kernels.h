@@ -23,6 +23,12 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
                             double* tmp, int parity, double omega);
 bool level_needs_two_phase(const LevelDev& L, int dim);
+// fused two-colour sweeps, out of place (sb_sweep.cu); 3D, non-bulk, even periodic extents
+bool sweep2_supported(const LevelDev& L, int dim, int form);
+void launch_face_sweep2(cudaStream_t s, const LevelDev& L, int form, int A, CPtr3 u, double* unew,
+                        const double* rhsA, double omega);
+void launch_cell_sweep2(cudaStream_t s, const LevelDev& L, const double* phi, double* pnew, const double* rhs,
+                        double omega);
 // fused residual -> restriction (multigrid.py:403-406 + :177-233)
 void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
                                 int form, int A, CPtr3 u, const double* rhsA, double* coarseA);

@@ -9,10 +9,12 @@
 // Hessenberg column.
 #include <cuda_runtime.h>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 #include <stdexcept>
+#include <utility>
 #include "../../include/stokesb200.h"
 #include "sb_kernels.h"
 
@@ -50,6 +52,8 @@ struct Level {
   bool two_phase = false;
   double *mu_c = nullptr, *gam_c = nullptr, *mu_e[3]{}, *rho_f[3]{}, *beta_f[3]{};
   double *fx[3]{}, *frhs[3]{}, *cx = nullptr, *crhs = nullptr, *tmp = nullptr;
+  bool fused = false;                         // two-colour streaming sweeps (sb_sweep.cu)
+  double *fxa[3]{}, *cxa = nullptr;           // ping-pong partners of the iterate
 };
 
 struct ProfEv {
@@ -137,6 +141,13 @@ void make_level(sb_ctx* c, const int* n, double h) {
   L.d.inv_h2 = 1.0 / (h * h);
   L.d.theta = 0.0;
   L.two_phase = level_needs_two_phase(L.d, c->dim);
+  // streaming two-colour sweeps: opt-in (SB_FUSED_SWEEPS=1) until they beat
+  // the per-colour kernels
+  static const bool fused_on = [] {
+    const char* e = std::getenv("SB_FUSED_SWEEPS");
+    return e && e[0] == '1';
+  }();
+  L.fused = fused_on && !L.two_phase && sweep2_supported(L.d, c->dim, c->form);
   c->lv.push_back(L);
 }
 
@@ -162,6 +173,10 @@ void alloc_level(sb_ctx* c, Level& L, bool first) {
     L.crhs = dalloc(c, B);
   }
   if (L.two_phase) L.tmp = dalloc(c, B);
+  if (L.fused) {
+    for (int a = 3 - c->dim; a < 3; ++a) L.fxa[a] = dalloc(c, B);
+    L.cxa = dalloc(c, B);
+  }
   L.d.mu_c = L.mu_c;
   L.d.gam_c = L.gam_c;
   for (int a = 0; a < 3; ++a) {
@@ -304,41 +319,57 @@ double cell_pass_bytes(const sb_ctx* c, const Level& L) {
 
 // ---- multigrid ---------------------------------------------------------------
 
-void sweep_face(sb_ctx* c, int l, double* const* x, const double* const* rhs, double omega) {
+// One smoother sweep on level l.  cur[] holds the iterate; fused levels
+// sweep out of place into alt[] and swap the pointers (ping-pong).
+void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* const* rhs, double omega) {
   Level& L = c->lv[l];
-  Ptr3 u{{x[0], x[1], x[2]}};
+  const int per_launch = L.fused ? 2 : 1;
   for (int A = 3 - c->dim; A < 3; ++A) {
-    for (int parity = 0; parity < 2; ++parity) {
+    for (int parity = 0; parity < 2; parity += per_launch) {
       cudaEvent_t ea = nullptr;
       if (c->profiling) {
         ea = next_event(c);
         CK(cudaEventRecord(ea, c->st));
       }
-      if (L.two_phase) launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
-      else launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega);
+      if (L.fused) {
+        CPtr3 u{{cur[0], cur[1], cur[2]}};
+        launch_face_sweep2(c->st, L.d, c->form, A, u, alt[A], rhs[A], omega);
+        std::swap(cur[A], alt[A]);
+      } else {
+        Ptr3 u{{cur[0], cur[1], cur[2]}};
+        if (L.two_phase) launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
+        else launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega);
+      }
       if (c->profiling) {
         cudaEvent_t eb = next_event(c);
         CK(cudaEventRecord(eb, c->st));
-        c->prof.push_back({ea, eb, 0, l == 0, face_pass_bytes(c, L)});
+        c->prof.push_back({ea, eb, 0, l == 0, per_launch * face_pass_bytes(c, L)});
       }
     }
   }
 }
 
-void sweep_cell(sb_ctx* c, int l, double* x, const double* rhs, double omega) {
+void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs, double omega) {
   Level& L = c->lv[l];
-  for (int parity = 0; parity < 2; ++parity) {
+  const int per_launch = L.fused ? 2 : 1;
+  for (int parity = 0; parity < 2; parity += per_launch) {
     cudaEvent_t ea = nullptr;
     if (c->profiling) {
       ea = next_event(c);
       CK(cudaEventRecord(ea, c->st));
     }
-    if (L.two_phase) launch_cell_colour_tmp(c->st, L.d, c->dim, x, rhs, L.tmp, parity, omega);
-    else launch_cell_colour(c->st, L.d, c->dim, x, rhs, parity, omega);
+    if (L.fused) {
+      launch_cell_sweep2(c->st, L.d, cur, alt, rhs, omega);
+      std::swap(cur, alt);
+    } else if (L.two_phase) {
+      launch_cell_colour_tmp(c->st, L.d, c->dim, cur, rhs, L.tmp, parity, omega);
+    } else {
+      launch_cell_colour(c->st, L.d, c->dim, cur, rhs, parity, omega);
+    }
     if (c->profiling) {
       cudaEvent_t eb = next_event(c);
       CK(cudaEventRecord(eb, c->st));
-      c->prof.push_back({ea, eb, 1, l == 0, cell_pass_bytes(c, L)});
+      c->prof.push_back({ea, eb, 1, l == 0, per_launch * cell_pass_bytes(c, L)});
     }
   }
 }
@@ -346,37 +377,44 @@ void sweep_cell(sb_ctx* c, int l, double* x, const double* rhs, double omega) {
 // multigrid.py:409-439 -- x is written (zero initial guess)
 void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, const sb_smoother& sm) {
   Level& L = c->lv[l];
-  for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(x[A], 0, L.block * 8, c->st));
+  double* cur[3] = {x[0], x[1], x[2]};
+  double* alt[3] = {L.fxa[0], L.fxa[1], L.fxa[2]};
+  for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(cur[A], 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, x, rhs, sm.omega);
-    return;
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
+  } else {
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
+    Level& Lc = c->lv[l + 1];
+    CPtr3 xc{{cur[0], cur[1], cur[2]}};
+    for (int A = 3 - c->dim; A < 3; ++A)
+      launch_face_resid_restrict(c->st, L.d, Lc.d, c->dim, c->form, A, xc, rhs[A], Lc.frhs[A]);
+    vcycle_face(c, l + 1, Lc.frhs, Lc.fx, sm);
+    for (int A = 3 - c->dim; A < 3; ++A)
+      launch_face_prolong_add(c->st, L.d, Lc.d, c->dim, A, Lc.fx[A], cur[A]);
+    for (int s = 0; s < sm.sweeps_up; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
   }
-  for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, x, rhs, sm.omega);
-  Level& Lc = c->lv[l + 1];
-  CPtr3 xc{{x[0], x[1], x[2]}};
-  for (int A = 3 - c->dim; A < 3; ++A)
-    launch_face_resid_restrict(c->st, L.d, Lc.d, c->dim, c->form, A, xc, rhs[A], Lc.frhs[A]);
-  vcycle_face(c, l + 1, Lc.frhs, Lc.fx, sm);
-  for (int A = 3 - c->dim; A < 3; ++A)
-    launch_face_prolong_add(c->st, L.d, Lc.d, c->dim, A, Lc.fx[A], x[A]);
-  for (int s = 0; s < sm.sweeps_up; ++s) sweep_face(c, l, x, rhs, sm.omega);
+  for (int A = 3 - c->dim; A < 3; ++A)  // odd sweep counts leave the iterate in the partner buffer
+    if (cur[A] != x[A]) CK(cudaMemcpyAsync(x[A], cur[A], L.block * 8, cudaMemcpyDeviceToDevice, c->st));
 }
 
 void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smoother& sm) {
   Level& L = c->lv[l];
-  CK(cudaMemsetAsync(x, 0, L.block * 8, c->st));
+  double* cur = x;
+  double* alt = L.cxa;
+  CK(cudaMemsetAsync(cur, 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, x, rhs, sm.omega);
-    return;
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
+  } else {
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
+    Level& Lc = c->lv[l + 1];
+    launch_cell_resid_restrict(c->st, L.d, Lc.d, c->dim, cur, rhs, Lc.crhs);
+    vcycle_cell(c, l + 1, Lc.crhs, Lc.cx, sm);
+    launch_cell_prolong_add(c->st, L.d, Lc.d, c->dim, Lc.cx, cur);
+    for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
   }
-  for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, x, rhs, sm.omega);
-  Level& Lc = c->lv[l + 1];
-  launch_cell_resid_restrict(c->st, L.d, Lc.d, c->dim, x, rhs, Lc.crhs);
-  vcycle_cell(c, l + 1, Lc.crhs, Lc.cx, sm);
-  launch_cell_prolong_add(c->st, L.d, Lc.d, c->dim, Lc.cx, x);
-  for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, x, rhs, sm.omega);
+  if (cur != x) CK(cudaMemcpyAsync(x, cur, L.block * 8, cudaMemcpyDeviceToDevice, c->st));
 }
 
 // multigrid.py:442-460 on level-0 device buffers
@@ -1149,13 +1187,18 @@ int sb_smooth(sb_ctx* c, int kind, int level, double omega, double* const* x, co
         copy_in(c, L, A, x[r], bx[A]);
         copy_in(c, L, A, rhs[r], br[A]);
       }
-      sweep_face(c, level, bx, br, omega);
-      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, bx[r + c->off], x[r]);
+      Level& Lw = c->lv[level];
+      double* cur[3] = {bx[0], bx[1], bx[2]};
+      double* alt[3] = {Lw.fxa[0], Lw.fxa[1], Lw.fxa[2]};
+      sweep_face(c, level, cur, alt, br, omega);
+      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, cur[r + c->off], x[r]);
     } else {
       copy_in(c, L, -1, x[0], bx[0]);
       copy_in(c, L, -1, rhs[0], br[0]);
-      sweep_cell(c, level, bx[0], br[0], omega);
-      copy_out(c, L, -1, bx[0], x[0]);
+      double* cur = bx[0];
+      double* alt = c->lv[level].cxa;
+      sweep_cell(c, level, cur, alt, br[0], omega);
+      copy_out(c, L, -1, cur, x[0]);
     }
     sync(c);
     return SB_OK;
