@@ -819,6 +819,110 @@ k_update_dot(const double* __restrict__ V, long long vstride, int nv, const doub
   }
 }
 
+// Delayed-reorthogonalisation Arnoldi, pass A: finish the previous basis
+// vector and project the new operator output on the whole basis in ONE read
+// of the basis.  q_k = (s_k - sum_{i<k} c_i Q_i) * inv_gamma is written over
+// the provisional s_k (slot k); partials of Q_i . w for i <= k.
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_a(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+         const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[kMaxVec][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = k + 1;
+  for (int i = threadIdx.x; i < nv * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    const double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    const double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    double2 q0 = ok0 ? s2[e] : make_double2(0.0, 0.0);
+    double2 q1 = ok1 ? s2[e1] : make_double2(0.0, 0.0);
+    for (int i = 0; i < k; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double ci = cs[i];
+      q0.x -= ci * a.x;
+      q0.y -= ci * a.y;
+      q1.x -= ci * b.x;
+      q1.y -= ci * b.y;
+      const double sdot = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
+      if (lane == 0) acc[i][warp] += sdot;
+    }
+    if (k > 0) {
+      q0.x *= inv_gamma;
+      q0.y *= inv_gamma;
+      q1.x *= inv_gamma;
+      q1.y *= inv_gamma;
+      if (ok0) s2[e] = q0;
+      if (ok1) s2[e1] = q1;
+    }
+    const double sdot = warp_sum((q0.x * w0.x + q0.y * w0.y) + (q1.x * wv1.x + q1.y * wv1.y));
+    if (lane == 0) acc[k][warp] += sdot;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
+// pass B: w' = w - sum_i d_i Q_i written to `out`, partials of Q_i . w' (slots
+// 0..nv-1) and ||w'||^2 (slot nv).  The second read of Q_i hits L1/L2.
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_b(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
+         const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[kMaxVec + 1][kThreads / 32];
+  __shared__ double ds[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (nv + 1) * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) ds[i] = d[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    for (int i = 0; i < nv; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double di = ds[i];
+      w0.x -= di * a.x;
+      w0.y -= di * a.y;
+      wv1.x -= di * b.x;
+      wv1.y -= di * b.y;
+    }
+    if (ok0) o2[e] = w0;
+    if (ok1) o2[e1] = wv1;
+    for (int i = 0; i < nv; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double sdot = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
+      if (lane == 0) acc[i][warp] += sdot;
+    }
+    const double nn = warp_sum((w0.x * w0.x + w0.y * w0.y) + (wv1.x * wv1.x + wv1.y * wv1.y));
+    if (lane == 0) acc[nv][warp] += nn;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // out[i] = sum_b partials[i*kRedBlocks + b], fixed-order tree (deterministic)
 __global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out) {
   __shared__ double s[kThreads];
@@ -1248,6 +1352,18 @@ void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int n
                        double* w, long long n, double* partials, int mode) {
   ++g_kernel_launches;
   k_update_dot<<<kRedBlocks, kThreads, 0, s>>>(V, vstride, nv, h, w, n / 2, partials, mode);
+}
+
+void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
+                   const double* w, long long n, double* partials) {
+  ++g_kernel_launches;
+  k_dcgs_a<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+}
+
+void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
+                   double* out, long long n, double* partials) {
+  ++g_kernel_launches;
+  k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {

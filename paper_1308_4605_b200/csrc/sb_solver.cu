@@ -774,7 +774,12 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
   const double target = gc.rtol * rp0 + gc.atol;
   const double bd_tol = std::max(gc.atol, 1e-14 * rp0);
 
-  std::vector<double> H((m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1);
+  std::vector<double> H((m + 1) * m), Horig((m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1), cpend(m + 1);
+  static const bool cgs2 = [] {
+    const char* e = std::getenv("SB_ORTHO");
+    return e && std::strcmp(e, "cgs2") == 0;
+  }();
+  double gam = 1.0;
   int k = 0;
   bool first = true;
   const double* r = c->vz0;
@@ -786,6 +791,8 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     }
     if (beta == 0.0) return finish(SB_STATUS_CONVERGED);
     std::fill(H.begin(), H.end(), 0.0);
+    std::fill(Horig.begin(), Horig.end(), 0.0);
+    gam = 1.0;  // q_0 = r / beta is final: no pending correction
     std::fill(cs.begin(), cs.end(), 0.0);
     std::fill(sn.begin(), sn.end(), 0.0);
     std::fill(g.begin(), g.end(), 0.0);
@@ -799,18 +806,53 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
       precond_apply_graph(c, pc, sm);
       *vcyc += precond_cost(c, pc);
       ++k;
-      // CGS2 Arnoldi (parity-safe replacement of MGS)
-      const int nv = j + 1;
-      launch_multi_dot(c->st, V, vl, nv, c->vw, vl, c->dpart);
-      launch_finalize(c->st, c->dpart, nv, dh1(c));
-      launch_update_dot(c->st, V, vl, nv, dh1(c), c->vw, vl, c->dpart, 0);
-      launch_finalize(c->st, c->dpart, nv, dh2(c));
-      launch_update_dot(c->st, V, vl, nv, dh2(c), c->vw, vl, c->dpart, 1);
-      launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
-      CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
-      sync(c);
-      for (int i = 0; i <= j; ++i) H[i * m + j] = hh1(c)[i] + hh2(c)[i];
-      const double hn = std::sqrt(hmisc(c)[1]);
+      double hn;
+      if (cgs2) {
+        // CGS2 Arnoldi (parity-safe replacement of MGS)
+        const int nv = j + 1;
+        launch_multi_dot(c->st, V, vl, nv, c->vw, vl, c->dpart);
+        launch_finalize(c->st, c->dpart, nv, dh1(c));
+        launch_update_dot(c->st, V, vl, nv, dh1(c), c->vw, vl, c->dpart, 0);
+        launch_finalize(c->st, c->dpart, nv, dh2(c));
+        launch_update_dot(c->st, V, vl, nv, dh2(c), c->vw, vl, c->dpart, 1);
+        launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
+        CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        for (int i = 0; i <= j; ++i) H[i * m + j] = hh1(c)[i] + hh2(c)[i];
+        hn = std::sqrt(hmisc(c)[1]);
+      } else {
+        // CGS2 with delayed reorthogonalisation: two passes over the basis.
+        // Slot j holds s_j = gam_j q_j + Q_j cpend; w = P^-1 M s_j.
+        //  A: q_j = (s_j - Q_j cpend)/gam_j written in place, d = [Q_j q_j]^T w
+        //  B: w' = w - Q_{j+1} d -> slot j+1, c' = Q_{j+1}^T w', ||w'||^2
+        // Using P^-1 M Q_j = Q_{j+1} Horig (Arnoldi relation):
+        //  H[:j+1, j] = (d - Horig cpend + c')/gam_j,
+        //  H[j+1, j]  = sqrt(||w'||^2 - ||c'||^2)/gam_j, and slot j+1 becomes
+        //  s_{j+1} = w' with cpend = c', gam_{j+1} = sqrt(||w'||^2 - ||c'||^2).
+        for (int i = 0; i < j; ++i) hy(c)[i] = cpend[i];
+        if (j > 0) CK(cudaMemcpyAsync(dh2(c), hy(c), j * 8, cudaMemcpyHostToDevice, c->st));
+        launch_dcgs_a(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
+        launch_finalize(c->st, c->dpart, j + 1, dh1(c));
+        launch_dcgs_b(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
+        launch_finalize(c->st, c->dpart, j + 2, dh2(c));
+        CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        double cc = 0.0;
+        for (int i = 0; i <= j; ++i) cc += hh2(c)[i] * hh2(c)[i];
+        const double ww = hh2(c)[j + 1];
+        const double g2 = std::max(ww - cc, 0.0);
+        const double gnext = std::sqrt(g2);
+        for (int i = 0; i <= j; ++i) {
+          double e = 0.0;
+          for (int t = 0; t < j; ++t) e += Horig[i * m + t] * cpend[t];
+          H[i * m + j] = ((hh1(c)[i] - e) + hh2(c)[i]) / gam;
+        }
+        hn = gnext / gam;
+        for (int i = 0; i <= j; ++i) Horig[i * m + j] = H[i * m + j];
+        Horig[(j + 1) * m + j] = hn;
+        for (int i = 0; i <= j; ++i) cpend[i] = hh2(c)[i];
+        gam = gnext;
+      }
       H[(j + 1) * m + j] = hn;
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
@@ -851,7 +893,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         launch_combo(c->st, c->vx, c->vx, V, vl, ydim, dy(c), vl);
         return finish(conv ? SB_STATUS_CONVERGED : SB_STATUS_BREAKDOWN);
       }
-      launch_scale_div(c->st, c->vw, hn, V + (long long)(j + 1) * vl, vl);
+      if (cgs2) launch_scale_div(c->st, c->vw, hn, V + (long long)(j + 1) * vl, vl);
       ++j;
     }
     // x = x + V[:j] y  (the last iteration's least-squares solution)
