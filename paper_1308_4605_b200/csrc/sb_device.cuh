@@ -90,20 +90,56 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
   return s;
 }
 
+// Operand accessors for the face row.  Every array a face row reads, at the
+// offsets it reads them: mu_c at f and f-e_A, mu_e(A,B) at f and f+e_B, u_B at
+// (f | f+e_B) (- e_A), rho_A and rhs at f, plus the u_A neighbourhood.
+// GAcc gathers from global memory with periodic wraps; the streaming sweep
+// kernels (sb_sweep.cu) provide a shared-memory accessor with the same API.
+template <int DIM, int A>
+struct GAcc {
+  const LevelDev& L;
+  const double* const* u;
+  int f;
+  const int* ci;
+  int dmA;
+  __device__ __forceinline__ GAcc(const LevelDev& L_, const double* const* u_, int f_, const int* ci_)
+      : L(L_), u(u_), f(f_), ci(ci_) {
+    dmA = (A == 0) ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+  }
+  template <int B>
+  __device__ __forceinline__ int eB() const {
+    return B == 0 ? dplus<0>(L, ci[0]) : (B == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+  }
+  __device__ __forceinline__ double mu(bool lo) const { return ld(L.mu_c, lo ? f + dmA : f); }
+  __device__ __forceinline__ double gam(bool lo) const { return ld(L.gam_c, lo ? f + dmA : f); }
+  template <int B>
+  __device__ __forceinline__ double mue(bool hi) const { return ld(L.mu_e[edge_of(A, B)], hi ? f + eB<B>() : f); }
+  template <int B>
+  __device__ __forceinline__ double ub(bool hi, bool lowA) const {
+    const int e = hi ? f + eB<B>() : f;
+    return ld(u[B], lowA ? e + dmA : e);
+  }
+  __device__ __forceinline__ double rho() const { return ld(L.rho_f[A], f); }
+  // (D u) h at the cells c_hi = f / c_lo = f - e_A (stress+bulk form only)
+  __device__ __forceinline__ double divh(bool lo) const {
+    if (!lo) return div_sum<DIM>(L, u, f, ci);
+    int clo[3] = {ci[0], ci[1], ci[2]};
+    clo[A] = (per(L, A) && ci[A] == 0) ? L.n[A] - 1 : ci[A] - 1;
+    return div_sum<DIM>(L, u, f + dmA, clo);
+  }
+};
+
 // One tangential flux of row A across the edge at B-position jj (lo edge
 // jj = cB, hi edge jj = cB+1) and the matching diagonal weight
 // (operators.py:267-300, 331-340; diag :424-434).  u_hi/u_lo are u_A on the
 // two sides of the edge along B.
-template <int FORM, int A, int B>
-__device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const* u, int f, int cB, int jj,
-                                          int am_d, double u_hi, double u_lo, double& flux, double& w) {
-  const int sB = stride<B>(L);
+template <int FORM, int A, int B, class ACC>
+__device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int cB, bool hi_edge, double u_hi,
+                                          double u_lo, double& flux, double& w) {
   const int nB = L.n[B];
   const bool pB = per(L, B);
-  // edge index: same point with B-coordinate jj (wrapped jj==nB -> 0 on periodic axes)
-  const int jw = (pB && jj == nB) ? 0 : jj;
-  const int e = f + (jw - cB) * sB;
-  const double mue = ld(L.mu_e[edge_of(A, B)], e);
+  const int jj = hi_edge ? cB + 1 : cB;
+  const double mue = acc.template mue<B>(hi_edge);
   double tang;
   int side = -1;  // 0: low wall, 1: high wall
   if (!pB && jj == 0) {
@@ -117,7 +153,7 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const
   }
   double ft = tang;
   if (FORM != F_LAP) {
-    const double cross = (ld(u[B], e) - ld(u[B], e + am_d)) * L.inv_h;
+    const double cross = (acc.template ub<B>(hi_edge, false) - acc.template ub<B>(hi_edge, true)) * L.inv_h;
     ft = tang + cross;
   }
   ft = mue * ft;
@@ -135,33 +171,28 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const double* const
 }
 
 // (A u)_A at unknown face f (coords ci) from the u_A neighbourhood s and the
-// other components u[B] (global), plus the smoother diagonal of that row.
+// accessor, plus the smoother diagonal of that row.
 // operators.py:303-360 (row form multigrid.py:343-383), diag operators.py:408-439.
-template <int DIM, int FORM, int A>
-__device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
-                                                const int* ci, double& diag) {
-  const int dmA = (A == 0) ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+template <int DIM, int FORM, int A, class ACC>
+__device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, const ACC& acc, const int* ci,
+                                             double& diag) {
   const double uf = s.c, up = s.p[A], um = s.m[A];
-  // cells c_hi = f, c_lo = f + dmA share the face's index (uniform strides)
-  const double mu_hi = ld(L.mu_c, f), mu_lo = ld(L.mu_c, f + dmA);
+  const double mu_hi = acc.mu(false), mu_lo = acc.mu(true);
   const double nc_hi = FORM == F_LAP ? mu_hi : 2.0 * mu_hi;
   const double nc_lo = FORM == F_LAP ? mu_lo : 2.0 * mu_lo;
   double fn_hi = nc_hi * (up - uf) * L.inv_h;
   double fn_lo = nc_lo * (uf - um) * L.inv_h;
   double ncd_hi = nc_hi, ncd_lo = nc_lo;
   if (FORM == F_BULK) {
-    const double g_hi = ld(L.gam_c, f), g_lo = ld(L.gam_c, f + dmA);
-    const double bk_hi = g_hi - (2.0 / 3.0) * mu_hi;
-    const double bk_lo = g_lo - (2.0 / 3.0) * mu_lo;
-    int clo[3] = {ci[0], ci[1], ci[2]};
-    clo[A] = (per(L, A) && ci[A] == 0) ? L.n[A] - 1 : ci[A] - 1;
-    fn_hi = fn_hi + bk_hi * (div_sum<DIM>(L, u, f, ci) * L.inv_h);
-    fn_lo = fn_lo + bk_lo * (div_sum<DIM>(L, u, f + dmA, clo) * L.inv_h);
+    const double bk_hi = acc.gam(false) - (2.0 / 3.0) * mu_hi;
+    const double bk_lo = acc.gam(true) - (2.0 / 3.0) * mu_lo;
+    fn_hi = fn_hi + bk_hi * (acc.divh(false) * L.inv_h);
+    fn_lo = fn_lo + bk_lo * (acc.divh(true) * L.inv_h);
     ncd_hi = nc_hi + bk_hi;
     ncd_lo = nc_lo + bk_lo;
   }
   double res = (fn_hi - fn_lo) * L.inv_h;
-  double dg = L.theta == 0.0 ? 0.0 : L.theta * ld(L.rho_f[A], f);
+  double dg = L.theta == 0.0 ? 0.0 : L.theta * acc.rho();
   dg = dg + (ncd_hi + ncd_lo) * L.inv_h2;
 #pragma unroll
   for (int B = 3 - DIM; B < 3; ++B) {
@@ -169,21 +200,27 @@ __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s,
     double f_lo, f_hi, w_lo, w_hi;
     const int cB = ci[B];
     if (B == 0) {
-      tang_flux<FORM, A, 0>(L, u, f, cB, cB, dmA, uf, s.m[0], f_lo, w_lo);
-      tang_flux<FORM, A, 0>(L, u, f, cB, cB + 1, dmA, s.p[0], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 0>(L, acc, cB, false, uf, s.m[0], f_lo, w_lo);
+      tang_flux<FORM, A, 0>(L, acc, cB, true, s.p[0], uf, f_hi, w_hi);
     } else if (B == 1) {
-      tang_flux<FORM, A, 1>(L, u, f, cB, cB, dmA, uf, s.m[1], f_lo, w_lo);
-      tang_flux<FORM, A, 1>(L, u, f, cB, cB + 1, dmA, s.p[1], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 1>(L, acc, cB, false, uf, s.m[1], f_lo, w_lo);
+      tang_flux<FORM, A, 1>(L, acc, cB, true, s.p[1], uf, f_hi, w_hi);
     } else {
-      tang_flux<FORM, A, 2>(L, u, f, cB, cB, dmA, uf, s.m[2], f_lo, w_lo);
-      tang_flux<FORM, A, 2>(L, u, f, cB, cB + 1, dmA, s.p[2], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 2>(L, acc, cB, false, uf, s.m[2], f_lo, w_lo);
+      tang_flux<FORM, A, 2>(L, acc, cB, true, s.p[2], uf, f_hi, w_hi);
     }
     res = res + (f_hi - f_lo) * L.inv_h;
     dg = dg + (w_lo + w_hi) * L.inv_h2;
   }
   diag = dg;
-  const double tr = L.theta == 0.0 ? 0.0 : (L.theta * ld(L.rho_f[A], f)) * uf;
+  const double tr = L.theta == 0.0 ? 0.0 : (L.theta * acc.rho()) * uf;
   return tr - res;
+}
+
+template <int DIM, int FORM, int A>
+__device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
+                                                const int* ci, double& diag) {
+  return face_row_t<DIM, FORM, A>(L, s, GAcc<DIM, A>(L, u, f, ci), ci, diag);
 }
 
 template <int DIM, int FORM, int A>
@@ -192,25 +229,43 @@ __device__ __forceinline__ double face_row(const LevelDev& L, const double* cons
   return face_row_core<DIM, FORM, A>(L, gather_ua<DIM, A>(L, u[A], f, ci), u, f, ci, diag);
 }
 
+// beta = 1/rho_face accessor for the cell row: beta_a at the low face (c) or
+// the high face (c + e_a, wrapped) of cell c.
+struct GBeta {
+  const LevelDev& L;
+  int c;
+  const int* ci;
+  __device__ __forceinline__ GBeta(const LevelDev& L_, int c_, const int* ci_) : L(L_), c(c_), ci(ci_) {}
+  template <int AX>
+  __device__ __forceinline__ double beta(bool hi) const {
+    return ld(L.beta_f[AX], hi ? c + dplus<AX>(L, ci[AX]) : c);
+  }
+};
+
 // (L_rho phi)(c) and its diagonal from the 7-point phi neighbourhood s
 // (operators.py:206-215, 396-405).
-template <int DIM>
-__device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s, int c, const int* ci,
-                                                double& diag) {
+template <int DIM, class BA>
+__device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, const BA& ba, const int* ci,
+                                             double& diag) {
   const double pc = s.c;
   double acc = 0.0, dacc = 0.0;
   bool first = true;
 #pragma unroll
   for (int a = 3 - DIM; a < 3; ++a) {
-    const int st = a == 0 ? L.s0 : (a == 1 ? L.s1 : 1);
     const int n = L.n[a];
     const bool p = per(L, a);
-    const double* beta = L.beta_f[a];
-    // low face of c is c (index c); high face c+1 (wrapped)
+    double b_lo, b_hi;
+    if (a == 0) {
+      b_lo = ba.template beta<0>(false);
+      b_hi = ba.template beta<0>(true);
+    } else if (a == 1) {
+      b_lo = ba.template beta<1>(false);
+      b_hi = ba.template beta<1>(true);
+    } else {
+      b_lo = ba.template beta<2>(false);
+      b_hi = ba.template beta<2>(true);
+    }
     double g_lo = 0.0, g_hi = 0.0;
-    const int hi_f = (p && ci[a] == n - 1) ? -(n - 1) * st : st;
-    const double b_lo = ld(beta, c);
-    const double b_hi = ld(beta, c + hi_f);
     if (p || ci[a] > 0) g_lo = ((pc - s.m[a]) * L.inv_h) * b_lo;
     if (p || ci[a] < n - 1) g_hi = ((s.p[a] - pc) * L.inv_h) * b_hi;
     const double d = g_hi - g_lo;
@@ -220,6 +275,12 @@ __device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s,
   }
   diag = dacc * L.inv_h2;
   return acc * L.inv_h;
+}
+
+template <int DIM>
+__device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s, int c, const int* ci,
+                                                double& diag) {
+  return cell_row_t<DIM>(L, s, GBeta(L, c, ci), ci, diag);
 }
 
 template <int DIM>

@@ -923,6 +923,50 @@ k_dcgs_b(const double* __restrict__ Q, long long vstride, int nv, const double* 
   }
 }
 
+// pass B with the basis values of the current tile stashed in shared memory:
+// every Q_i streams from HBM exactly once (the dots re-read the stash).
+constexpr int kStashThreads = 128;
+__global__ void __launch_bounds__(kStashThreads)
+k_dcgs_b_stash(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
+               const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  extern __shared__ double2 stash[];  // [nv][kStashThreads]
+  __shared__ double acc[kMaxVec + 1][kStashThreads / 32];
+  __shared__ double ds[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (nv + 1) * (kStashThreads / 32); i += blockDim.x)
+    acc[i / (kStashThreads / 32)][i % (kStashThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) ds[i] = d[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += step) {
+    const bool ok = e < n2;
+    double2 wv = ok ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    for (int i = 0; i < nv; ++i) {
+      const double2 a = ok ? __ldg(reinterpret_cast<const double2*>(Q + i * vstride) + e) : make_double2(0.0, 0.0);
+      stash[i * kStashThreads + threadIdx.x] = a;
+      const double di = ds[i];
+      wv.x -= di * a.x;
+      wv.y -= di * a.y;
+    }
+    if (ok) o2[e] = wv;
+    for (int i = 0; i < nv; ++i) {
+      const double2 a = stash[i * kStashThreads + threadIdx.x];
+      const double sdot = warp_sum(a.x * wv.x + a.y * wv.y);
+      if (lane == 0) acc[i][warp] += sdot;
+    }
+    const double nn = warp_sum(wv.x * wv.x + wv.y * wv.y);
+    if (lane == 0) acc[nv][warp] += nn;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kStashThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // out[i] = sum_b partials[i*kRedBlocks + b], fixed-order tree (deterministic)
 __global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out) {
   __shared__ double s[kThreads];
@@ -1363,7 +1407,17 @@ void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const do
 void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
                    double* out, long long n, double* partials) {
   ++g_kernel_launches;
-  k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+  const size_t stash = (size_t)nv * kStashThreads * sizeof(double2);
+  if (stash <= 160 * 1024) {
+    static size_t configured = 0;
+    if (stash > configured) {
+      cudaFuncSetAttribute(k_dcgs_b_stash, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      configured = 160 * 1024;
+    }
+    k_dcgs_b_stash<<<kRedBlocks, kStashThreads, stash, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+  } else {
+    k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+  }
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {

@@ -4,19 +4,23 @@
 // for a face component, :321-324 for cells) out of place: it reads the
 // current iterate x (never modified during the launch) and writes the swept
 // iterate to a second buffer.  A CTA owns a TJ x TK tile of the (axis-1,
-// axis-2) plane and marches along axis 0 over a chunk of planes:
+// axis-2) plane and marches along axis 0 over a chunk of planes.  Every
+// operand (the iterate, the other velocity components, mu_c, mu_e, rho, rhs,
+// 1/rho) is staged plane by plane into a per-array shared-memory ring with
+// cp.async (LDGSTS), one plane ahead of use, so the relaxation phases read
+// shared memory only:
 //
-//   step p:  prefetch old plane p+2 (cp.async, ring of 4 planes, halo 2)
+//   step p:  prefetch the next plane of every operand
 //            R_p   = old plane p with its RED unknowns relaxed   (tile + ring 1)
 //            black = relax the BLACK unknowns of plane p-1 from R_{p-2..p}
 //            write plane p-1 (both colours) to the output buffer
 //
 // Red faces never neighbour red faces (even periodic extents), so R_p depends
-// on old values only and the redundant ring computed by neighbouring CTAs is
+// on old values only and the ring recomputed by neighbouring CTAs is
 // bit-identical; black reads only red neighbours and its own old value.  The
-// result therefore equals the reference's sequential red-then-black pass to the
-// bit, while every array streams through HBM once per component sweep (64 B per
-// face instead of 2 x 56 B for two colour passes).  Levels with an
+// result equals the reference's sequential red-then-black pass to the bit,
+// while every array streams from HBM once per component sweep (64 B per face
+// instead of 2 x 56 B for two colour passes).  Levels with an
 // odd periodic extent, 2D grids and the stress+bulk form use the per-colour
 // kernels instead.
 #include <cuda_runtime.h>
@@ -29,9 +33,11 @@ extern long long g_kernel_launches;
 namespace {
 
 constexpr int NT = 256;
-constexpr int TJ = 16, TK = 32;
-constexpr int RJ = TJ + 4, RK = TK + 4;  // old planes: halo 2
+constexpr int TJ = 8, TK = 32;
+constexpr int RJ = TJ + 4, RK = TK + 4;  // staged planes: halo 2
 constexpr int QJ = TJ + 2, QK = TK + 2;  // relaxed planes: halo 1
+constexpr int PL = RJ * RK;              // doubles per staged plane
+constexpr int QL = QJ * QK;
 constexpr int RED_PER_ROW = QK / 2;      // 17
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
@@ -45,23 +51,27 @@ __device__ __forceinline__ int wrapc(int x, int n) {
   x %= n;
   return x < 0 ? x + n : x;
 }
+__device__ __forceinline__ int pmod(int x, int m) {
+  x %= m;
+  return x < 0 ? x + m : x;
+}
 
 struct Ext {
   int e[3];
   bool p[3];
 };
 
-// absolute coordinate -> array coordinate (wrapped), or -1 if outside a wall axis
+// absolute coordinate -> array coordinate (wrapped), or -1 outside a wall axis
 __device__ __forceinline__ int acoord(const Ext& E, const LevelDev& L, int a, int x) {
   if (E.p[a]) return wrapc(x, L.n[a]);
   return (x >= 0 && x < E.e[a]) ? x : -1;
 }
 
-// stage plane q (ring-2 halo) of x into a shared slot
+// stage plane q (halo 2) of x into a shared slot; outside the array -> 0
 __device__ __forceinline__ void stage(const LevelDev& L, const Ext& E, const double* x, double* slot, int q,
                                      int j0, int k0) {
   const int qa = acoord(E, L, 0, q);
-  for (int t = threadIdx.x; t < RJ * RK; t += NT) {
+  for (int t = threadIdx.x; t < PL; t += NT) {
     const int jj = t / RK, kk = t - jj * RK;
     const int ja = acoord(E, L, 1, j0 - 2 + jj), ka = acoord(E, L, 2, k0 - 2 + kk);
     if (qa >= 0 && ja >= 0 && ka >= 0) cp_async8(slot + t, x + qa * L.s0 + ja * L.s1 + ka);
@@ -69,60 +79,163 @@ __device__ __forceinline__ void stage(const LevelDev& L, const Ext& E, const dou
   }
 }
 
-__device__ __forceinline__ int mod3(int p) { return ((p % 3) + 3) % 3; }
+// A staged operand: ring of NS planes; at step p its window is planes
+// [p-1+LO, p+HI] and plane p+1+HI is in flight.
+template <int LO, int HI>
+struct Ring {
+  static constexpr int NS = HI - LO + 3;
+  double* base;
+  const double* src;
+  __device__ __forceinline__ double* slot(int q) const { return base + pmod(q, NS) * PL; }
+};
 
-template <int FORM, int A>
+// in-plane offset of +e_ax in the staged layout (axis 0 is the plane axis)
+template <int AX>
+__device__ __forceinline__ constexpr int inplane() { return AX == 1 ? RK : (AX == 2 ? 1 : 0); }
+
+// Shared-memory accessor with the GAcc interface (sb_device.cuh) for a face
+// of component A on plane pp at staged-layout index o.
+template <int A, class RUB1, class RUB2, class RMU, class RME1, class RME2>
+struct SAcc {
+  static constexpr int B1 = A == 0 ? 1 : 0, B2 = A == 2 ? 1 : 2;
+  const RUB1& ub1;
+  const RUB2& ub2;
+  const RMU& rmu;
+  const RME1& me1;
+  const RME2& me2;
+  const double* rho0;
+  int pp, o;
+  // value of ring R at (plane pp + dp, index o + di)
+  template <class R>
+  __device__ __forceinline__ double at(const R& r, int dp, int di) const {
+    return r.slot(pp + dp)[o + di];
+  }
+  __device__ __forceinline__ double mu(bool lo) const {
+    return lo ? (A == 0 ? at(rmu, -1, 0) : at(rmu, 0, -inplane<A>())) : at(rmu, 0, 0);
+  }
+  __device__ __forceinline__ double gam(bool) const { return 0.0; }  // stress+bulk not staged
+  __device__ __forceinline__ double divh(bool) const { return 0.0; }
+  template <int B>
+  __device__ __forceinline__ double mue(bool hi) const {
+    const int dp = (hi && B == 0) ? 1 : 0, di = hi ? inplane<B>() : 0;
+    return B == B1 ? at(me1, dp, di) : at(me2, dp, di);
+  }
+  template <int B>
+  __device__ __forceinline__ double ub(bool hi, bool lowA) const {
+    const int dp = ((hi && B == 0) ? 1 : 0) + ((lowA && A == 0) ? -1 : 0);
+    const int di = (hi ? inplane<B>() : 0) - (lowA ? inplane<A>() : 0);
+    return B == B1 ? at(ub1, dp, di) : at(ub2, dp, di);
+  }
+  __device__ __forceinline__ double rho() const { return rho0[o]; }
+};
+
+template <int AX, int BB>
+struct LoOf {  // window low offset of u_B / mu_c for component AX (A==0 reads plane -1)
+  static constexpr int v = AX == 0 ? -1 : 0;
+};
+
+template <int FORM, int A, bool TH>
 __global__ void __launch_bounds__(NT)
 k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __restrict__ rhs, double omega,
               int chunk) {
-  __shared__ double so[4][RJ * RK];
-  __shared__ double sr[3][QJ * QK];
+  constexpr int B1 = A == 0 ? 1 : 0, B2 = A == 2 ? 1 : 2;
+  constexpr int LA = A == 0 ? -1 : 0;
+  extern __shared__ double smem[];
+  Ring<0, 1> rx;                            // u_A (old), red window [p-1, p+1]
+  Ring<LA, B1 == 0 ? 1 : 0> rb1;            // u_B1
+  Ring<LA, 0> rb2;                          // u_B2 (B2 is never axis 0)
+  Ring<LA, 0> rmu;                          // mu_c
+  Ring<0, B1 == 0 ? 1 : 0> re1;             // mu_e(A, B1)
+  Ring<0, 0> re2;                           // mu_e(A, B2)
+  Ring<0, 0> rrhs;                          // rhs_A
+  Ring<0, 0> rrho;                          // rho_A (theta > 0)
+  double* sp = smem;
+  rx.base = sp; sp += decltype(rx)::NS * PL;
+  rb1.base = sp; sp += decltype(rb1)::NS * PL;
+  rb2.base = sp; sp += decltype(rb2)::NS * PL;
+  rmu.base = sp; sp += decltype(rmu)::NS * PL;
+  re1.base = sp; sp += decltype(re1)::NS * PL;
+  re2.base = sp; sp += decltype(re2)::NS * PL;
+  rrhs.base = sp; sp += decltype(rrhs)::NS * PL;
+  rrho.base = sp; if (TH) sp += decltype(rrho)::NS * PL;
+  double* sr = sp;  // 3 relaxed planes (halo 1)
+  rx.src = u.p[A];
+  rb1.src = u.p[B1];
+  rb2.src = u.p[B2];
+  rmu.src = L.mu_c;
+  re1.src = L.mu_e[edge_of(A, B1)];
+  re2.src = L.mu_e[edge_of(A, B2)];
+  rrhs.src = rhs;
+  rrho.src = L.rho_f[A];
+
   Ext E;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     E.p[a] = per(L, a);
     E.e[a] = L.n[a] + ((a == A && !E.p[a]) ? 1 : 0);
   }
+  // staging extents: face arrays of B carry +1 along their own wall axis; the
+  // other operands are cell/edge shaped -- the pitched box covers them all, so
+  // stage with the extents of the array actually read.
+  Ext EB1 = E, EB2 = E, EC = E, EE1 = E, EE2 = E;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    EB1.e[a] = L.n[a] + ((a == B1 && !E.p[a]) ? 1 : 0);
+    EB2.e[a] = L.n[a] + ((a == B2 && !E.p[a]) ? 1 : 0);
+    EC.e[a] = L.n[a];
+    EE1.e[a] = L.n[a] + (((a == A || a == B1) && !E.p[a]) ? 1 : 0);
+    EE2.e[a] = L.n[a] + (((a == A || a == B2) && !E.p[a]) ? 1 : 0);
+  }
   const int off = E.p[A] ? 0 : 1;  // interior-relative parity offset (multigrid.py:335-339)
   const int k0 = blockIdx.x * TK, j0 = blockIdx.y * TJ;
   const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, E.e[0]) - 1;
-  const double* ua = u.p[A];
-  auto unknown = [&](const int* ca) {  // array coordinates of a face of A
-    if (!E.p[A] && (ca[A] == 0 || ca[A] == L.n[A])) return false;
-    return true;
-  };
+  auto unknown = [&](const int* ca) { return E.p[A] || (ca[A] != 0 && ca[A] != L.n[A]); };
 
-  stage(L, E, ua, so[(i0 - 2) & 3], i0 - 2, j0, k0);
-  stage(L, E, ua, so[(i0 - 1) & 3], i0 - 1, j0, k0);
-  stage(L, E, ua, so[i0 & 3], i0, j0, k0);
-  cp_commit();
-  stage(L, E, ua, so[(i0 + 1) & 3], i0 + 1, j0, k0);
+  auto stage_plane = [&](int q, auto& r, const Ext& Ex) { stage(L, Ex, r.src, r.slot(q), q, j0, k0); };
+  // prologue: window of step i0-1
+  for (int q = i0 - 2 + 0; q <= i0 - 1 + 1; ++q) stage_plane(q, rx, E);
+  for (int q = i0 - 2 + LA; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, rb1, EB1);
+  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rb2, EB2);
+  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rmu, EC);
+  for (int q = i0 - 2; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, re1, EE1);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, re2, EE2);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E);
+  if (TH)
+    for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrho, E);
   cp_commit();
 
   for (int p = i0 - 1; p <= i1 + 1; ++p) {
-    if (p + 2 <= i1 + 2) stage(L, E, ua, so[(p + 2) & 3], p + 2, j0, k0);
+    // prefetch the newest plane of every window for step p+1
+    stage_plane(p + 2, rx, E);
+    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), rb1, EB1);
+    stage_plane(p + 1, rb2, EB2);
+    stage_plane(p + 1, rmu, EC);
+    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), re1, EE1);
+    stage_plane(p + 1, re2, EE2);
+    stage_plane(p + 1, rrhs, E);
+    if (TH) stage_plane(p + 1, rrho, E);
     cp_commit();
     cp_wait1();
     __syncthreads();
     // ---- R_p: relax the red unknowns of plane p on the tile + ring 1 ----
+    double* R = sr + pmod(p, 3) * QL;
     {
-      double* R = sr[mod3(p)];
-      const double* O0 = so[(p - 1) & 3];
-      const double* O1 = so[p & 3];
-      const double* O2 = so[(p + 1) & 3];
-      const int pa = acoord(E, L, 0, p);
-      for (int q = threadIdx.x; q < QJ * QK; q += NT) {  // start from the old plane
+      const double* O0 = rx.slot(p - 1);
+      const double* O1 = rx.slot(p);
+      const double* O2 = rx.slot(p + 1);
+      for (int q = threadIdx.x; q < QL; q += NT) {  // start from the old plane
         const int jj = q / QK, kk = q - jj * QK;
         R[q] = O1[(jj + 1) * RK + (kk + 1)];
       }
       __syncthreads();
+      const int pa = acoord(E, L, 0, p);
       if (pa >= 0) {
         for (int q = threadIdx.x; q < QJ * RED_PER_ROW; q += NT) {  // lanes on red faces only
           const int jj = q / RED_PER_ROW, m = q - jj * RED_PER_ROW;
           const int j = j0 - 1 + jj;
           const int kk = ((off - p - j - (k0 - 1)) & 1) + 2 * m;
           const int k = k0 - 1 + kk;
-          int ca[3] = {pa, acoord(E, L, 1, j), acoord(E, L, 2, k)};
+          const int ca[3] = {pa, acoord(E, L, 1, j), acoord(E, L, 2, k)};
           if (ca[1] < 0 || ca[2] < 0 || !unknown(ca)) continue;
           const int o = (jj + 1) * RK + (kk + 1);
           UA7 s;
@@ -133,10 +246,11 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
           s.m[1] = O1[o - RK];
           s.p[2] = O1[o + 1];
           s.m[2] = O1[o - 1];
-          const int f = ca[0] * L.s0 + ca[1] * L.s1 + ca[2];
+          const SAcc<A, decltype(rb1), decltype(rb2), decltype(rmu), decltype(re1), decltype(re2)> acc{
+              rb1, rb2, rmu, re1, re2, rrho.slot(p), p, o};
           double dg;
-          const double au = face_row_core<3, FORM, A>(L, s, u.p, f, ca, dg);
-          const double res = __ldg(rhs + f) - au;
+          const double au = face_row_t<3, FORM, A>(L, s, acc, ca, dg);
+          const double res = rrhs.slot(p)[o] - au;
           R[jj * QK + kk] = s.c + omega * (res / dg);
         }
       }
@@ -145,9 +259,9 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
     // ---- black unknowns of plane p-1 (tile) from R_{p-2}, R_{p-1}, R_p ----
     const int pb = p - 1;
     if (pb >= i0 && pb <= i1) {
-      double* Rm = sr[mod3(pb)];
-      const double* Rlo = sr[mod3(pb - 1)];
-      const double* Rhi = sr[mod3(pb + 1)];
+      double* Rm = sr + pmod(pb, 3) * QL;
+      const double* Rlo = sr + pmod(pb - 1, 3) * QL;
+      const double* Rhi = sr + pmod(pb + 1, 3) * QL;
       const int pa = acoord(E, L, 0, pb);
       for (int q = threadIdx.x; q < TJ * (TK / 2); q += NT) {
         const int jj = q / (TK / 2), m = q - jj * (TK / 2);
@@ -155,24 +269,25 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
         const int k = k0 + ((1 + off - pb - j - k0) & 1) + 2 * m;  // black: parity 1
         const int ca[3] = {pa, j, k};
         if (j >= E.e[1] || k >= E.e[2] || !unknown(ca)) continue;
-        const int o = (jj + 1) * QK + (k - k0 + 1);
+        const int oq = (jj + 1) * QK + (k - k0 + 1);
         UA7 s;
-        s.c = Rm[o];
-        s.p[0] = Rhi[o];
-        s.m[0] = Rlo[o];
-        s.p[1] = Rm[o + QK];
-        s.m[1] = Rm[o - QK];
-        s.p[2] = Rm[o + 1];
-        s.m[2] = Rm[o - 1];
-        const int f = ca[0] * L.s0 + ca[1] * L.s1 + ca[2];
+        s.c = Rm[oq];
+        s.p[0] = Rhi[oq];
+        s.m[0] = Rlo[oq];
+        s.p[1] = Rm[oq + QK];
+        s.m[1] = Rm[oq - QK];
+        s.p[2] = Rm[oq + 1];
+        s.m[2] = Rm[oq - 1];
+        const int o = (jj + 2) * RK + (k - k0 + 2);
+        const SAcc<A, decltype(rb1), decltype(rb2), decltype(rmu), decltype(re1), decltype(re2)> acc{
+            rb1, rb2, rmu, re1, re2, rrho.slot(pb), pb, o};
         double dg;
-        const double au = face_row_core<3, FORM, A>(L, s, u.p, f, ca, dg);
-        const double res = __ldg(rhs + f) - au;
-        Rm[o] = s.c + omega * (res / dg);
+        const double au = face_row_t<3, FORM, A>(L, s, acc, ca, dg);
+        const double res = rrhs.slot(pb)[o] - au;
+        Rm[oq] = s.c + omega * (res / dg);
       }
       __syncthreads();
-      // write plane pb (both colours) -- coalesced along k
-      for (int q = threadIdx.x; q < TJ * TK; q += NT) {
+      for (int q = threadIdx.x; q < TJ * TK; q += NT) {  // write plane pb, coalesced along k
         const int jj = q / TK, kk = q - jj * TK;
         const int j = j0 + jj, k = k0 + kk;
         if (j < E.e[1] && k < E.e[2]) unew[pa * L.s0 + j * L.s1 + k] = Rm[(jj + 1) * QK + kk + 1];
@@ -181,51 +296,89 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
   }
 }
 
-template <int DIM>
+// beta accessor over staged rings: beta_a at the low / high face of cell (pp, o)
+template <class R0, class R1, class R2>
+struct SBeta {
+  const R0& b0;
+  const R1& b1;
+  const R2& b2;
+  int pp, o;
+  template <int AX>
+  __device__ __forceinline__ double beta(bool hi) const {
+    if (AX == 0) return b0.slot(pp + (hi ? 1 : 0))[o];
+    if (AX == 1) return b1.slot(pp)[o + (hi ? RK : 0)];
+    return b2.slot(pp)[o + (hi ? 1 : 0)];
+  }
+};
+
 __global__ void __launch_bounds__(NT)
 k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ pnew,
               const double* __restrict__ rhs, double omega, int chunk) {
-  __shared__ double so[4][RJ * RK];
-  __shared__ double sr[3][QJ * QK];
-  Ext E;
+  extern __shared__ double smem[];
+  Ring<0, 1> rx;    // phi (old)
+  Ring<0, 1> rb0;   // beta_0 (reads plane +1)
+  Ring<0, 0> rb1;   // beta_1
+  Ring<0, 0> rb2;   // beta_2
+  Ring<0, 0> rrhs;
+  double* sp = smem;
+  rx.base = sp; sp += decltype(rx)::NS * PL;
+  rb0.base = sp; sp += decltype(rb0)::NS * PL;
+  rb1.base = sp; sp += decltype(rb1)::NS * PL;
+  rb2.base = sp; sp += decltype(rb2)::NS * PL;
+  rrhs.base = sp; sp += decltype(rrhs)::NS * PL;
+  double* sr = sp;
+  rx.src = phi;
+  rb0.src = L.beta_f[0];
+  rb1.src = L.beta_f[1];
+  rb2.src = L.beta_f[2];
+  rrhs.src = rhs;
+  Ext E, F0, F1, F2;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     E.p[a] = per(L, a);
     E.e[a] = L.n[a];
   }
+  F0 = F1 = F2 = E;
+  if (!E.p[0]) F0.e[0] += 1;
+  if (!E.p[1]) F1.e[1] += 1;
+  if (!E.p[2]) F2.e[2] += 1;
   const int k0 = blockIdx.x * TK, j0 = blockIdx.y * TJ;
   const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, E.e[0]) - 1;
-
-  stage(L, E, phi, so[(i0 - 2) & 3], i0 - 2, j0, k0);
-  stage(L, E, phi, so[(i0 - 1) & 3], i0 - 1, j0, k0);
-  stage(L, E, phi, so[i0 & 3], i0, j0, k0);
-  cp_commit();
-  stage(L, E, phi, so[(i0 + 1) & 3], i0 + 1, j0, k0);
+  auto stage_plane = [&](int q, auto& r, const Ext& Ex) { stage(L, Ex, r.src, r.slot(q), q, j0, k0); };
+  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rx, E);
+  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rb0, F0);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb1, F1);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb2, F2);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E);
   cp_commit();
 
   for (int p = i0 - 1; p <= i1 + 1; ++p) {
-    if (p + 2 <= i1 + 2) stage(L, E, phi, so[(p + 2) & 3], p + 2, j0, k0);
+    stage_plane(p + 2, rx, E);
+    stage_plane(p + 2, rb0, F0);
+    stage_plane(p + 1, rb1, F1);
+    stage_plane(p + 1, rb2, F2);
+    stage_plane(p + 1, rrhs, E);
     cp_commit();
     cp_wait1();
     __syncthreads();
+    double* R = sr + pmod(p, 3) * QL;
     {
-      double* R = sr[mod3(p)];
-      const double* O0 = so[(p - 1) & 3];
-      const double* O1 = so[p & 3];
-      const double* O2 = so[(p + 1) & 3];
-      const int pa = acoord(E, L, 0, p);
-      for (int q = threadIdx.x; q < QJ * QK; q += NT) {
+      const double* O0 = rx.slot(p - 1);
+      const double* O1 = rx.slot(p);
+      const double* O2 = rx.slot(p + 1);
+      for (int q = threadIdx.x; q < QL; q += NT) {
         const int jj = q / QK, kk = q - jj * QK;
         R[q] = O1[(jj + 1) * RK + (kk + 1)];
       }
       __syncthreads();
+      const int pa = acoord(E, L, 0, p);
       if (pa >= 0) {
         for (int q = threadIdx.x; q < QJ * RED_PER_ROW; q += NT) {
           const int jj = q / RED_PER_ROW, m = q - jj * RED_PER_ROW;
           const int j = j0 - 1 + jj;
           const int kk = ((-p - j - (k0 - 1)) & 1) + 2 * m;
           const int k = k0 - 1 + kk;
-          int ca[3] = {pa, acoord(E, L, 1, j), acoord(E, L, 2, k)};
+          const int ca[3] = {pa, acoord(E, L, 1, j), acoord(E, L, 2, k)};
           if (ca[1] < 0 || ca[2] < 0) continue;
           const int o = (jj + 1) * RK + (kk + 1);
           UA7 s;
@@ -236,10 +389,10 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
           s.m[1] = O1[o - RK];
           s.p[2] = O1[o + 1];
           s.m[2] = O1[o - 1];
-          const int c = ca[0] * L.s0 + ca[1] * L.s1 + ca[2];
+          const SBeta<decltype(rb0), decltype(rb1), decltype(rb2)> ba{rb0, rb1, rb2, p, o};
           double dg;
-          const double lp = cell_row_core<3>(L, s, c, ca, dg);
-          const double res = __ldg(rhs + c) - lp;
+          const double lp = cell_row_t<3>(L, s, ba, ca, dg);
+          const double res = rrhs.slot(p)[o] - lp;
           R[jj * QK + kk] = s.c + omega * res / dg;
         }
       }
@@ -247,29 +400,30 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
     __syncthreads();
     const int pb = p - 1;
     if (pb >= i0 && pb <= i1) {
-      double* Rm = sr[mod3(pb)];
-      const double* Rlo = sr[mod3(pb - 1)];
-      const double* Rhi = sr[mod3(pb + 1)];
+      double* Rm = sr + pmod(pb, 3) * QL;
+      const double* Rlo = sr + pmod(pb - 1, 3) * QL;
+      const double* Rhi = sr + pmod(pb + 1, 3) * QL;
       for (int q = threadIdx.x; q < TJ * (TK / 2); q += NT) {
         const int jj = q / (TK / 2), m = q - jj * (TK / 2);
         const int j = j0 + jj;
         const int k = k0 + ((1 - pb - j - k0) & 1) + 2 * m;
         if (j >= E.e[1] || k >= E.e[2]) continue;
         const int ca[3] = {pb, j, k};
-        const int o = (jj + 1) * QK + (k - k0 + 1);
+        const int oq = (jj + 1) * QK + (k - k0 + 1);
         UA7 s;
-        s.c = Rm[o];
-        s.p[0] = Rhi[o];
-        s.m[0] = Rlo[o];
-        s.p[1] = Rm[o + QK];
-        s.m[1] = Rm[o - QK];
-        s.p[2] = Rm[o + 1];
-        s.m[2] = Rm[o - 1];
-        const int c = ca[0] * L.s0 + ca[1] * L.s1 + ca[2];
+        s.c = Rm[oq];
+        s.p[0] = Rhi[oq];
+        s.m[0] = Rlo[oq];
+        s.p[1] = Rm[oq + QK];
+        s.m[1] = Rm[oq - QK];
+        s.p[2] = Rm[oq + 1];
+        s.m[2] = Rm[oq - 1];
+        const int o = (jj + 2) * RK + (k - k0 + 2);
+        const SBeta<decltype(rb0), decltype(rb1), decltype(rb2)> ba{rb0, rb1, rb2, pb, o};
         double dg;
-        const double lp = cell_row_core<3>(L, s, c, ca, dg);
-        const double res = __ldg(rhs + c) - lp;
-        Rm[o] = s.c + omega * res / dg;
+        const double lp = cell_row_t<3>(L, s, ba, ca, dg);
+        const double res = rrhs.slot(pb)[o] - lp;
+        Rm[oq] = s.c + omega * res / dg;
       }
       __syncthreads();
       for (int q = threadIdx.x; q < TJ * TK; q += NT) {
@@ -281,14 +435,43 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
   }
 }
 
-inline dim3 sweep_grid(int e0, int e1, int e2, int& chunk) {
+inline dim3 sweep_grid(int e0, int e1, int e2, int ctas_per_sm, int& chunk) {
   const int gx = (e2 + TK - 1) / TK, gy = (e1 + TJ - 1) / TJ;
   const int cols = gx * gy;
-  int nch = std::max(1, std::min(e0 / 16, (148 * 4 + cols - 1) / cols));
-  if (nch < 1) nch = 1;
+  int nch = std::max(1, std::min(e0 / 16, (148 * ctas_per_sm + cols - 1) / cols));
   chunk = (e0 + nch - 1) / nch;
   nch = (e0 + chunk - 1) / chunk;
   return dim3(gx, gy, nch);
+}
+
+template <int FORM, int A, bool TH>
+size_t face_smem() {
+  constexpr int B1 = A == 0 ? 1 : 0;
+  constexpr int LA = A == 0 ? -1 : 0;
+  const int slots = Ring<0, 1>::NS + Ring<LA, B1 == 0 ? 1 : 0>::NS + 2 * Ring<LA, 0>::NS +
+                    Ring<0, B1 == 0 ? 1 : 0>::NS + Ring<0, 0>::NS * (TH ? 3 : 2);
+  return (size_t)(slots * PL + 3 * QL) * sizeof(double);
+}
+
+template <int FORM, int A, bool TH>
+void launch_face_t(cudaStream_t s, const LevelDev& L, CPtr3 u, double* unew, const double* rhsA, double omega) {
+  static bool configured = false;
+  const size_t sm = face_smem<FORM, A, TH>();
+  if (!configured) {
+    cudaFuncSetAttribute(k_face_sweep2<FORM, A, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  int e[3];
+  for (int a = 0; a < 3; ++a) e[a] = L.n[a] + ((a == A && L.bclo[a] != BC_PER) ? 1 : 0);
+  int chunk;
+  const dim3 g = sweep_grid(e[0], e[1], e[2], sm > 110 * 1024 ? 1 : 2, chunk);
+  k_face_sweep2<FORM, A, TH><<<g, NT, sm, s>>>(L, u, unew, rhsA, omega, chunk);
+}
+
+template <int FORM, int A>
+void launch_face_a(cudaStream_t s, const LevelDev& L, CPtr3 u, double* unew, const double* rhsA, double omega) {
+  if (L.theta > 0.0) launch_face_t<FORM, A, true>(s, L, u, unew, rhsA, omega);
+  else launch_face_t<FORM, A, false>(s, L, u, unew, rhsA, omega);
 }
 
 }  // namespace
@@ -303,27 +486,29 @@ bool sweep2_supported(const LevelDev& L, int dim, int form) {
 void launch_face_sweep2(cudaStream_t s, const LevelDev& L, int form, int A, CPtr3 u, double* unew,
                         const double* rhsA, double omega) {
   ++g_kernel_launches;
-  int e[3];
-  for (int a = 0; a < 3; ++a) e[a] = L.n[a] + ((a == A && L.bclo[a] != BC_PER) ? 1 : 0);
-  int chunk;
-  const dim3 g = sweep_grid(e[0], e[1], e[2], chunk);
   if (form == F_LAP) {
-    if (A == 0) k_face_sweep2<F_LAP, 0><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
-    else if (A == 1) k_face_sweep2<F_LAP, 1><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
-    else k_face_sweep2<F_LAP, 2><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
+    if (A == 0) launch_face_a<F_LAP, 0>(s, L, u, unew, rhsA, omega);
+    else if (A == 1) launch_face_a<F_LAP, 1>(s, L, u, unew, rhsA, omega);
+    else launch_face_a<F_LAP, 2>(s, L, u, unew, rhsA, omega);
   } else {
-    if (A == 0) k_face_sweep2<F_STRESS, 0><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
-    else if (A == 1) k_face_sweep2<F_STRESS, 1><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
-    else k_face_sweep2<F_STRESS, 2><<<g, NT, 0, s>>>(L, u, unew, rhsA, omega, chunk);
+    if (A == 0) launch_face_a<F_STRESS, 0>(s, L, u, unew, rhsA, omega);
+    else if (A == 1) launch_face_a<F_STRESS, 1>(s, L, u, unew, rhsA, omega);
+    else launch_face_a<F_STRESS, 2>(s, L, u, unew, rhsA, omega);
   }
 }
 
 void launch_cell_sweep2(cudaStream_t s, const LevelDev& L, const double* phi, double* pnew, const double* rhs,
                         double omega) {
   ++g_kernel_launches;
+  static bool configured = false;
+  const size_t sm = (size_t)((Ring<0, 1>::NS * 2 + Ring<0, 0>::NS * 3) * PL + 3 * QL) * sizeof(double);
+  if (!configured) {
+    cudaFuncSetAttribute(k_cell_sweep2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
   int chunk;
-  const dim3 g = sweep_grid(L.n[0], L.n[1], L.n[2], chunk);
-  k_cell_sweep2<3><<<g, NT, 0, s>>>(L, phi, pnew, rhs, omega, chunk);
+  const dim3 g = sweep_grid(L.n[0], L.n[1], L.n[2], 3, chunk);
+  k_cell_sweep2<<<g, NT, sm, s>>>(L, phi, pnew, rhs, omega, chunk);
 }
 
 }  // namespace sb
