@@ -67,17 +67,46 @@ __device__ __forceinline__ int acoord(const Ext& E, const LevelDev& L, int a, in
   return (x >= 0 && x < E.e[a]) ? x : -1;
 }
 
+// Per-CTA in-plane offset tables: tab[cls][t] = ja*s1 + ka of staged position
+// t (halo 2, wraps applied) or -1 outside the array.  cls bit 0: the array has
+// n1+1 entries along axis 1 (wall), bit 1: n2+1 along axis 2.  Plane-independent,
+// so staging a plane is a table lookup + cp.async per element.
+__device__ __forceinline__ void build_tabs(const LevelDev& L, int (*tab)[PL], int j0, int k0) {
+  for (int t = threadIdx.x; t < 4 * PL; t += NT) {
+    const int cls = t / PL, u = t - cls * PL;
+    const int jj = u / RK, kk = u - jj * RK;
+    int j = j0 - 2 + jj, k = k0 - 2 + kk;
+    const int e1 = L.n[1] + ((cls & 1) && L.bclo[1] != BC_PER ? 1 : 0);
+    const int e2 = L.n[2] + ((cls & 2) && L.bclo[2] != BC_PER ? 1 : 0);
+    bool ok = true;
+    if (L.bclo[1] == BC_PER) j = j < 0 ? j + L.n[1] : (j >= L.n[1] ? j - L.n[1] : j);
+    else ok = ok && j >= 0 && j < e1;
+    if (L.bclo[2] == BC_PER) k = k < 0 ? k + L.n[2] : (k >= L.n[2] ? k - L.n[2] : k);
+    else ok = ok && k >= 0 && k < e2;
+    tab[cls][u] = ok ? j * L.s1 + k : -1;
+  }
+}
+
 // stage plane q (halo 2) of x into a shared slot; outside the array -> 0
-__device__ __forceinline__ void stage(const LevelDev& L, const Ext& E, const double* x, double* slot, int q,
-                                     int j0, int k0) {
-  const int qa = acoord(E, L, 0, q);
+__device__ __forceinline__ void stage(const LevelDev& L, const Ext& E, const int* tab, const double* x,
+                                     double* slot, int q) {
+  int qa = q;
+  if (E.p[0]) qa = q < 0 ? q + L.n[0] : (q >= L.n[0] ? q - L.n[0] : q);
+  else if (q < 0 || q >= E.e[0]) qa = -1;
+  if (qa < 0) {
+    for (int t = threadIdx.x; t < PL; t += NT) slot[t] = 0.0;
+    return;
+  }
+  const double* xp = x + qa * L.s0;
   for (int t = threadIdx.x; t < PL; t += NT) {
-    const int jj = t / RK, kk = t - jj * RK;
-    const int ja = acoord(E, L, 1, j0 - 2 + jj), ka = acoord(E, L, 2, k0 - 2 + kk);
-    if (qa >= 0 && ja >= 0 && ka >= 0) cp_async8(slot + t, x + qa * L.s0 + ja * L.s1 + ka);
+    const int o = tab[t];
+    if (o >= 0) cp_async8(slot + t, xp + o);
     else slot[t] = 0.0;
   }
 }
+
+template <int AX>
+__host__ __device__ constexpr int cls_of_face() { return (AX == 1 ? 1 : 0) | (AX == 2 ? 2 : 0); }
 
 // A staged operand: ring of NS planes; at step p its window is planes
 // [p-1+LO, p+HI] and plane p+1+HI is in flight.
@@ -141,6 +170,7 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
   constexpr int B1 = A == 0 ? 1 : 0, B2 = A == 2 ? 1 : 2;
   constexpr int LA = A == 0 ? -1 : 0;
   extern __shared__ double smem[];
+  __shared__ int tab[4][PL];
   Ring<0, 1> rx;                            // u_A (old), red window [p-1, p+1]
   Ring<LA, B1 == 0 ? 1 : 0> rb1;            // u_B1
   Ring<LA, 0> rb2;                          // u_B2 (B2 is never axis 0)
@@ -191,29 +221,33 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
   const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, E.e[0]) - 1;
   auto unknown = [&](const int* ca) { return E.p[A] || (ca[A] != 0 && ca[A] != L.n[A]); };
 
-  auto stage_plane = [&](int q, auto& r, const Ext& Ex) { stage(L, Ex, r.src, r.slot(q), q, j0, k0); };
+  build_tabs(L, tab, j0, k0);
+  __syncthreads();
+  // table class per operand: which of axes 1/2 it is staggered along
+  constexpr int cA = cls_of_face<A>(), cB1 = cls_of_face<B1>(), cB2 = cls_of_face<B2>();
+  auto stage_plane = [&](int q, auto& r, const Ext& Ex, int cls) { stage(L, Ex, tab[cls], r.src, r.slot(q), q); };
   // prologue: window of step i0-1
-  for (int q = i0 - 2 + 0; q <= i0 - 1 + 1; ++q) stage_plane(q, rx, E);
-  for (int q = i0 - 2 + LA; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, rb1, EB1);
-  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rb2, EB2);
-  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rmu, EC);
-  for (int q = i0 - 2; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, re1, EE1);
-  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, re2, EE2);
-  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E);
+  for (int q = i0 - 2 + 0; q <= i0 - 1 + 1; ++q) stage_plane(q, rx, E, cA);
+  for (int q = i0 - 2 + LA; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, rb1, EB1, cB1);
+  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rb2, EB2, cB2);
+  for (int q = i0 - 2 + LA; q <= i0 - 1; ++q) stage_plane(q, rmu, EC, 0);
+  for (int q = i0 - 2; q <= i0 - 1 + (B1 == 0 ? 1 : 0); ++q) stage_plane(q, re1, EE1, cA | cB1);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, re2, EE2, cA | cB2);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E, cA);
   if (TH)
-    for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrho, E);
+    for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrho, E, cA);
   cp_commit();
 
   for (int p = i0 - 1; p <= i1 + 1; ++p) {
     // prefetch the newest plane of every window for step p+1
-    stage_plane(p + 2, rx, E);
-    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), rb1, EB1);
-    stage_plane(p + 1, rb2, EB2);
-    stage_plane(p + 1, rmu, EC);
-    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), re1, EE1);
-    stage_plane(p + 1, re2, EE2);
-    stage_plane(p + 1, rrhs, E);
-    if (TH) stage_plane(p + 1, rrho, E);
+    stage_plane(p + 2, rx, E, cA);
+    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), rb1, EB1, cB1);
+    stage_plane(p + 1, rb2, EB2, cB2);
+    stage_plane(p + 1, rmu, EC, 0);
+    stage_plane(p + 1 + (B1 == 0 ? 1 : 0), re1, EE1, cA | cB1);
+    stage_plane(p + 1, re2, EE2, cA | cB2);
+    stage_plane(p + 1, rrhs, E, cA);
+    if (TH) stage_plane(p + 1, rrho, E, cA);
     cp_commit();
     cp_wait1();
     __syncthreads();
@@ -315,6 +349,7 @@ __global__ void __launch_bounds__(NT)
 k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ pnew,
               const double* __restrict__ rhs, double omega, int chunk) {
   extern __shared__ double smem[];
+  __shared__ int tab[4][PL];
   Ring<0, 1> rx;    // phi (old)
   Ring<0, 1> rb0;   // beta_0 (reads plane +1)
   Ring<0, 0> rb1;   // beta_1
@@ -344,20 +379,22 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
   if (!E.p[2]) F2.e[2] += 1;
   const int k0 = blockIdx.x * TK, j0 = blockIdx.y * TJ;
   const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, E.e[0]) - 1;
-  auto stage_plane = [&](int q, auto& r, const Ext& Ex) { stage(L, Ex, r.src, r.slot(q), q, j0, k0); };
-  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rx, E);
-  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rb0, F0);
-  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb1, F1);
-  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb2, F2);
-  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E);
+  build_tabs(L, tab, j0, k0);
+  __syncthreads();
+  auto stage_plane = [&](int q, auto& r, const Ext& Ex, int cls) { stage(L, Ex, tab[cls], r.src, r.slot(q), q); };
+  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rx, E, 0);
+  for (int q = i0 - 2; q <= i0; ++q) stage_plane(q, rb0, F0, 0);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb1, F1, 1);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rb2, F2, 2);
+  for (int q = i0 - 2; q <= i0 - 1; ++q) stage_plane(q, rrhs, E, 0);
   cp_commit();
 
   for (int p = i0 - 1; p <= i1 + 1; ++p) {
-    stage_plane(p + 2, rx, E);
-    stage_plane(p + 2, rb0, F0);
-    stage_plane(p + 1, rb1, F1);
-    stage_plane(p + 1, rb2, F2);
-    stage_plane(p + 1, rrhs, E);
+    stage_plane(p + 2, rx, E, 0);
+    stage_plane(p + 2, rb0, F0, 0);
+    stage_plane(p + 1, rb1, F1, 1);
+    stage_plane(p + 1, rb2, F2, 2);
+    stage_plane(p + 1, rrhs, E, 0);
     cp_commit();
     cp_wait1();
     __syncthreads();
@@ -464,7 +501,7 @@ void launch_face_t(cudaStream_t s, const LevelDev& L, CPtr3 u, double* unew, con
   int e[3];
   for (int a = 0; a < 3; ++a) e[a] = L.n[a] + ((a == A && L.bclo[a] != BC_PER) ? 1 : 0);
   int chunk;
-  const dim3 g = sweep_grid(e[0], e[1], e[2], sm > 110 * 1024 ? 1 : 2, chunk);
+  const dim3 g = sweep_grid(e[0], e[1], e[2], sm > 100 * 1024 ? 1 : 2, chunk);
   k_face_sweep2<FORM, A, TH><<<g, NT, sm, s>>>(L, u, unew, rhsA, omega, chunk);
 }
 
