@@ -30,6 +30,9 @@ struct LevelDev {
 };
 
 __host__ __device__ __forceinline__ bool per(const LevelDev& L, int a) { return L.bclo[a] == BC_PER; }
+// PA: every axis of the level is periodic (compile-time) -> wall logic compiled out
+template <bool PA>
+__host__ __device__ __forceinline__ bool perq(const LevelDev& L, int a) { return PA || L.bclo[a] == BC_PER; }
 
 template <int AX>
 __device__ __forceinline__ int stride(const LevelDev& L) {
@@ -37,13 +40,13 @@ __device__ __forceinline__ int stride(const LevelDev& L) {
 }
 
 // index shift to the +1 / -1 neighbour along AX of coordinate c (periodic wrap)
-template <int AX>
+template <int AX, bool PA = false>
 __device__ __forceinline__ int dplus(const LevelDev& L, int c) {
-  return (L.bclo[AX] == BC_PER && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
+  return (perq<PA>(L, AX) && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
 }
-template <int AX>
+template <int AX, bool PA = false>
 __device__ __forceinline__ int dminus(const LevelDev& L, int c) {
-  return (L.bclo[AX] == BC_PER && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
+  return (perq<PA>(L, AX) && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
 }
 
 __device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + i); }
@@ -51,14 +54,14 @@ __device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + 
 __host__ __device__ constexpr int edge_of(int a, int b) { return 3 - a - b; }
 
 // (D u)(c) * h accumulated in axis order: ((d0 + d1) + d2)  (operators.py:182-188)
-template <int DIM>
+template <int DIM, bool PA = false>
 __device__ __forceinline__ double div_sum(const LevelDev& L, const double* const* u, int c,
                                           const int* ci) {
   double acc = 0.0;
   bool first = true;
 #pragma unroll
   for (int b = 3 - DIM; b < 3; ++b) {
-    int dp = (b == 0) ? dplus<0>(L, ci[0]) : (b == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+    int dp = (b == 0) ? dplus<0, PA>(L, ci[0]) : (b == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
     // on a wall axis the high face of cell c is c+1 (<= n), never wrapped
     double d = u[b][c + dp] - u[b][c];
     acc = first ? d : acc + d;
@@ -74,16 +77,16 @@ struct UA7 {
   double c, p[3], m[3];
 };
 
-template <int DIM, int A>
+template <int DIM, int A, bool PA = false>
 __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, int f, const int* ci) {
   UA7 s;
   s.c = ua[f];
 #pragma unroll
   for (int b = 3 - DIM; b < 3; ++b) {
-    const int dp = b == 0 ? dplus<0>(L, ci[0]) : (b == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
-    const int dm = b == 0 ? dminus<0>(L, ci[0]) : (b == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+    const int dp = b == 0 ? dplus<0, PA>(L, ci[0]) : (b == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
+    const int dm = b == 0 ? dminus<0, PA>(L, ci[0]) : (b == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
     // on a wall axis B != A the +/- neighbours are only read away from the wall
-    const bool wallB = b != A && L.bclo[b] != BC_PER;
+    const bool wallB = b != A && !perq<PA>(L, b);
     s.p[b] = (wallB && ci[b] == L.n[b] - 1) ? 0.0 : ua[f + dp];
     s.m[b] = (wallB && ci[b] == 0) ? 0.0 : ua[f + dm];
   }
@@ -95,7 +98,7 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // (f | f+e_B) (- e_A), rho_A and rhs at f, plus the u_A neighbourhood.
 // GAcc gathers from global memory with periodic wraps; the streaming sweep
 // kernels (sb_sweep.cu) provide a shared-memory accessor with the same API.
-template <int DIM, int A>
+template <int DIM, int A, bool PA = false>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
@@ -104,11 +107,11 @@ struct GAcc {
   int dmA;
   __device__ __forceinline__ GAcc(const LevelDev& L_, const double* const* u_, int f_, const int* ci_)
       : L(L_), u(u_), f(f_), ci(ci_) {
-    dmA = (A == 0) ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+    dmA = (A == 0) ? dminus<0, PA>(L, ci[0]) : (A == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
   }
   template <int B>
   __device__ __forceinline__ int eB() const {
-    return B == 0 ? dplus<0>(L, ci[0]) : (B == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
+    return B == 0 ? dplus<0, PA>(L, ci[0]) : (B == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
   }
   __device__ __forceinline__ double mu(bool lo) const { return ld(L.mu_c, lo ? f + dmA : f); }
   __device__ __forceinline__ double gam(bool lo) const { return ld(L.gam_c, lo ? f + dmA : f); }
@@ -122,10 +125,10 @@ struct GAcc {
   __device__ __forceinline__ double rho() const { return ld(L.rho_f[A], f); }
   // (D u) h at the cells c_hi = f / c_lo = f - e_A (stress+bulk form only)
   __device__ __forceinline__ double divh(bool lo) const {
-    if (!lo) return div_sum<DIM>(L, u, f, ci);
+    if (!lo) return div_sum<DIM, PA>(L, u, f, ci);
     int clo[3] = {ci[0], ci[1], ci[2]};
-    clo[A] = (per(L, A) && ci[A] == 0) ? L.n[A] - 1 : ci[A] - 1;
-    return div_sum<DIM>(L, u, f + dmA, clo);
+    clo[A] = (perq<PA>(L, A) && ci[A] == 0) ? L.n[A] - 1 : ci[A] - 1;
+    return div_sum<DIM, PA>(L, u, f + dmA, clo);
   }
 };
 
@@ -133,11 +136,11 @@ struct GAcc {
 // jj = cB, hi edge jj = cB+1) and the matching diagonal weight
 // (operators.py:267-300, 331-340; diag :424-434).  u_hi/u_lo are u_A on the
 // two sides of the edge along B.
-template <int FORM, int A, int B, class ACC>
+template <int FORM, int A, int B, bool PA, class ACC>
 __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int cB, bool hi_edge, double u_hi,
                                           double u_lo, double& flux, double& w) {
   const int nB = L.n[B];
-  const bool pB = per(L, B);
+  const bool pB = perq<PA>(L, B);
   const int jj = hi_edge ? cB + 1 : cB;
   const double mue = acc.template mue<B>(hi_edge);
   double tang;
@@ -158,7 +161,7 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int
   }
   ft = mue * ft;
   w = mue;
-  if (side >= 0) {
+  if (!PA && side >= 0) {
     const int kind = side == 0 ? L.bclo[B] : L.bchi[B];
     if (kind == BC_FREESLIP) {
       ft = 0.0;
@@ -173,7 +176,7 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int
 // (A u)_A at unknown face f (coords ci) from the u_A neighbourhood s and the
 // accessor, plus the smoother diagonal of that row.
 // operators.py:303-360 (row form multigrid.py:343-383), diag operators.py:408-439.
-template <int DIM, int FORM, int A, class ACC>
+template <int DIM, int FORM, int A, bool PA, class ACC>
 __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, const ACC& acc, const int* ci,
                                              double& diag) {
   const double uf = s.c, up = s.p[A], um = s.m[A];
@@ -200,14 +203,14 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
     double f_lo, f_hi, w_lo, w_hi;
     const int cB = ci[B];
     if (B == 0) {
-      tang_flux<FORM, A, 0>(L, acc, cB, false, uf, s.m[0], f_lo, w_lo);
-      tang_flux<FORM, A, 0>(L, acc, cB, true, s.p[0], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 0, PA>(L, acc, cB, false, uf, s.m[0], f_lo, w_lo);
+      tang_flux<FORM, A, 0, PA>(L, acc, cB, true, s.p[0], uf, f_hi, w_hi);
     } else if (B == 1) {
-      tang_flux<FORM, A, 1>(L, acc, cB, false, uf, s.m[1], f_lo, w_lo);
-      tang_flux<FORM, A, 1>(L, acc, cB, true, s.p[1], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 1, PA>(L, acc, cB, false, uf, s.m[1], f_lo, w_lo);
+      tang_flux<FORM, A, 1, PA>(L, acc, cB, true, s.p[1], uf, f_hi, w_hi);
     } else {
-      tang_flux<FORM, A, 2>(L, acc, cB, false, uf, s.m[2], f_lo, w_lo);
-      tang_flux<FORM, A, 2>(L, acc, cB, true, s.p[2], uf, f_hi, w_hi);
+      tang_flux<FORM, A, 2, PA>(L, acc, cB, false, uf, s.m[2], f_lo, w_lo);
+      tang_flux<FORM, A, 2, PA>(L, acc, cB, true, s.p[2], uf, f_hi, w_hi);
     }
     res = res + (f_hi - f_lo) * L.inv_h;
     dg = dg + (w_lo + w_hi) * L.inv_h2;
@@ -217,20 +220,21 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA = false>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
-  return face_row_t<DIM, FORM, A>(L, s, GAcc<DIM, A>(L, u, f, ci), ci, diag);
+  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA>(L, u, f, ci), ci, diag);
 }
 
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA = false>
 __device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, int f, const int* ci,
                                            double& diag) {
-  return face_row_core<DIM, FORM, A>(L, gather_ua<DIM, A>(L, u[A], f, ci), u, f, ci, diag);
+  return face_row_core<DIM, FORM, A, PA>(L, gather_ua<DIM, A, PA>(L, u[A], f, ci), u, f, ci, diag);
 }
 
 // beta = 1/rho_face accessor for the cell row: beta_a at the low face (c) or
 // the high face (c + e_a, wrapped) of cell c.
+template <bool PA = false>
 struct GBeta {
   const LevelDev& L;
   int c;
@@ -238,13 +242,13 @@ struct GBeta {
   __device__ __forceinline__ GBeta(const LevelDev& L_, int c_, const int* ci_) : L(L_), c(c_), ci(ci_) {}
   template <int AX>
   __device__ __forceinline__ double beta(bool hi) const {
-    return ld(L.beta_f[AX], hi ? c + dplus<AX>(L, ci[AX]) : c);
+    return ld(L.beta_f[AX], hi ? c + dplus<AX, PA>(L, ci[AX]) : c);
   }
 };
 
 // (L_rho phi)(c) and its diagonal from the 7-point phi neighbourhood s
 // (operators.py:206-215, 396-405).
-template <int DIM, class BA>
+template <int DIM, bool PA, class BA>
 __device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, const BA& ba, const int* ci,
                                              double& diag) {
   const double pc = s.c;
@@ -253,7 +257,7 @@ __device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, co
 #pragma unroll
   for (int a = 3 - DIM; a < 3; ++a) {
     const int n = L.n[a];
-    const bool p = per(L, a);
+    const bool p = perq<PA>(L, a);
     double b_lo, b_hi;
     if (a == 0) {
       b_lo = ba.template beta<0>(false);
@@ -277,31 +281,31 @@ __device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, co
   return acc * L.inv_h;
 }
 
-template <int DIM>
+template <int DIM, bool PA = false>
 __device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s, int c, const int* ci,
                                                 double& diag) {
-  return cell_row_t<DIM>(L, s, GBeta(L, c, ci), ci, diag);
+  return cell_row_t<DIM, PA>(L, s, GBeta<PA>(L, c, ci), ci, diag);
 }
 
-template <int DIM>
+template <int DIM, bool PA = false>
 __device__ __forceinline__ UA7 gather_cell(const LevelDev& L, const double* phi, int c, const int* ci) {
   UA7 s;
   s.c = phi[c];
 #pragma unroll
   for (int a = 3 - DIM; a < 3; ++a) {
-    const int dp = a == 0 ? dplus<0>(L, ci[0]) : (a == 1 ? dplus<1>(L, ci[1]) : dplus<2>(L, ci[2]));
-    const int dm = a == 0 ? dminus<0>(L, ci[0]) : (a == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
-    const bool wall = L.bclo[a] != BC_PER;
+    const int dp = a == 0 ? dplus<0, PA>(L, ci[0]) : (a == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
+    const int dm = a == 0 ? dminus<0, PA>(L, ci[0]) : (a == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
+    const bool wall = !perq<PA>(L, a);
     s.p[a] = (wall && ci[a] == L.n[a] - 1) ? 0.0 : phi[c + dp];
     s.m[a] = (wall && ci[a] == 0) ? 0.0 : phi[c + dm];
   }
   return s;
 }
 
-template <int DIM>
+template <int DIM, bool PA = false>
 __device__ __forceinline__ double cell_row(const LevelDev& L, const double* phi, int c, const int* ci,
                                            double& diag) {
-  return cell_row_core<DIM>(L, gather_cell<DIM>(L, phi, c, ci), c, ci, diag);
+  return cell_row_core<DIM, PA>(L, gather_cell<DIM, PA>(L, phi, c, ci), c, ci, diag);
 }
 
 }  // namespace sb

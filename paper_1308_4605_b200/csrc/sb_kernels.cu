@@ -100,7 +100,7 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 // same-colour faces couple through the wrap): phase 0 stores the new values in
 // tmp, phase 1 copies them in -- exactly the reference's compute-all-then-
 // update-masked order.
-template <int DIM, int FORM, int A, int PHASE>
+template <int DIM, int FORM, int A, int PHASE, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -121,7 +121,7 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
     }
     const double* uc[3] = {u.p[0], u.p[1], u.p[2]};
     double dg;
-    const double au = face_row<DIM, FORM, A>(L, uc, f, ci, dg);
+    const double au = face_row<DIM, FORM, A, PA>(L, uc, f, ci, dg);
     const double res = __ldg(rhs + f) - au;
     const double nv = uc[A][f] + omega * (res / dg);
     if (PHASE == 2) tmp[f] = nv;
@@ -129,7 +129,7 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
   }
 }
 
-template <int DIM, int PHASE>
+template <int DIM, int PHASE, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -148,7 +148,7 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
       return;
     }
     double dg;
-    const double lp = cell_row<DIM>(L, phi, c, ci, dg);
+    const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
     const double res = __ldg(rhs + c) - lp;
     const double nv = phi[c] + omega * res / dg;
     if (PHASE == 2) tmp[c] = nv;
@@ -160,18 +160,18 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
 // residual -> restriction (multigrid.py:195-233, 177-182, 403-406)
 // ---------------------------------------------------------------------------
 
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA>
 __device__ __forceinline__ double face_resid_at(const LevelDev& L, const double* const* u,
                                                 const double* rhs, const int* ci) {
   const int f = lin(L, ci);
   double dg;
-  const double au = face_row<DIM, FORM, A>(L, u, f, ci, dg);
+  const double au = face_row<DIM, FORM, A, PA>(L, u, f, ci, dg);
   return __ldg(rhs + f) - au;
 }
 
 // Tangential 2^(d-1) mean of fine residuals at fine normal index fa, coarse
 // tangential indices in C (mean along B1 first, then B2: multigrid.py:112-119).
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA>
 __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* const* u, const double* rhs,
                                               const int* C, int fa) {
   using O = Others<DIM, A>;
@@ -186,23 +186,23 @@ __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* 
       q0[O::B2] += t2;
       q1[O::B2] += t2;
       q1[O::B1] += 1;
-      const double m0 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q0);
-      const double m1 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q1);
+      const double m0 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q0);
+      const double m1 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q1);
       p[t2] = 0.5 * (m0 + m1);
     }
     return 0.5 * (p[0] + p[1]);
   }
   int q1[3] = {fi[0], fi[1], fi[2]};
   q1[O::B1] += 1;
-  const double m0 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, fi);
-  const double m1 = face_resid_at<DIM, FORM, A>(Lf, u, rhs, q1);
+  const double m0 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, fi);
+  const double m1 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q1);
   return 0.5 * (m0 + m1);
 }
 
 // Fused residual -> restriction, each fine residual evaluated once.
 // A == 2 (contiguous axis): lanes run along coarse K; t(2K-1) is the previous
 // lane's t(2K+1) (warp shuffle), lane 0 evaluates it itself.
-template <int DIM, int FORM>
+template <int DIM, int FORM, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
             Box cb) {
@@ -213,21 +213,21 @@ k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   C[0] = cb.lo[0] + (int)blockIdx.z;
   const bool ok = C[2] <= cb.hi[2] && C[1] <= cb.hi[1];
   int Cs[3] = {C[0], ok ? C[1] : cb.lo[1], ok ? C[2] : cb.lo[2]};
-  const double t0 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, 2 * Cs[A]);
-  const double t1 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, 2 * Cs[A] + 1);
+  const double t0 = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, Cs, 2 * Cs[A]);
+  const double t1 = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, Cs, 2 * Cs[A] + 1);
   double tm = __shfl_up_sync(0xffffffffu, t1, 1);
   const int lane = threadIdx.x & 31;
   if (lane == 0 || Cs[A] == cb.lo[A]) {
     int fa = 2 * Cs[A] - 1;
     if (fa < 0) fa += Lf.n[A];
-    tm = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, Cs, fa);
+    tm = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, Cs, fa);
   }
   if (ok) coarse[lin(Lc, C)] = (0.25 * tm + 0.5 * t0) + 0.25 * t1;
 }
 
 // A in {0, 1}: lanes along coarse axis 2 (coalesced), each thread marches a
 // chunk of coarse indices along A, carrying t(2C+1) into the next t(2C-1).
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
             Box cb, int chunk) {
@@ -246,27 +246,27 @@ k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   C[A] = a0;
   int fa = 2 * a0 - 1;
   if (fa < 0) fa += Lf.n[A];
-  double tm = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, fa);
+  double tm = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, fa);
 #pragma unroll 1
   for (int c = a0; c <= a1; ++c) {
     C[A] = c;
-    const double t0 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, 2 * c);
-    const double t1 = tmean_resid<DIM, FORM, A>(Lf, u.p, rhs, C, 2 * c + 1);
+    const double t0 = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, 2 * c);
+    const double t1 = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, 2 * c + 1);
     coarse[lin(Lc, C)] = (0.25 * tm + 0.5 * t0) + 0.25 * t1;
     tm = t1;
   }
 }
 
-template <int DIM>
+template <int DIM, bool PA>
 __device__ __forceinline__ double cell_resid_at(const LevelDev& L, const double* phi,
                                                 const double* rhs, const int* ci) {
   const int c = lin(L, ci);
   double dg;
-  const double lp = cell_row<DIM>(L, phi, c, ci, dg);
+  const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
   return __ldg(rhs + c) - lp;
 }
 
-template <int DIM>
+template <int DIM, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict__ rhs,
           double* __restrict__ coarse, Box cb, unsigned total) {
@@ -283,7 +283,7 @@ k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict_
         for (int j = 0; j < 2; ++j) {
           int a0[3] = {2 * C[0], 2 * C[1] + j, 2 * C[2] + k};
           int a1[3] = {2 * C[0] + 1, 2 * C[1] + j, 2 * C[2] + k};
-          q[j] = 0.5 * (cell_resid_at<3>(Lf, phi, rhs, a0) + cell_resid_at<3>(Lf, phi, rhs, a1));
+          q[j] = 0.5 * (cell_resid_at<3, PA>(Lf, phi, rhs, a0) + cell_resid_at<3, PA>(Lf, phi, rhs, a1));
         }
         s[k] = 0.5 * (q[0] + q[1]);
       }
@@ -294,7 +294,7 @@ k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict_
       for (int k = 0; k < 2; ++k) {
         int a0[3] = {0, 2 * C[1], 2 * C[2] + k};
         int a1[3] = {0, 2 * C[1] + 1, 2 * C[2] + k};
-        q[k] = 0.5 * (cell_resid_at<2>(Lf, phi, rhs, a0) + cell_resid_at<2>(Lf, phi, rhs, a1));
+        q[k] = 0.5 * (cell_resid_at<2, PA>(Lf, phi, rhs, a0) + cell_resid_at<2, PA>(Lf, phi, rhs, a1));
       }
       out = 0.5 * (q[0] + q[1]);
     }
@@ -405,7 +405,7 @@ __device__ __forceinline__ double grad_at(const LevelDev& L, const double* q, in
   return (__ldg(q + f) - __ldg(q + f + dm)) * L.inv_h;
 }
 
-template <int DIM, int FORM, int A>
+template <int DIM, int FORM, int A, bool PA>
 __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u, const double* p,
                                        double* out, const int* ci) {
   if (!in_face(L, A, ci)) return;
@@ -415,23 +415,23 @@ __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u
     return;
   }
   double dg;
-  const double au = face_row<DIM, FORM, A>(L, u, f, ci, dg);
+  const double au = face_row<DIM, FORM, A, PA>(L, u, f, ci, dg);
   out[f] = au + grad_at<A>(L, p, f, ci);
 }
 
-template <int DIM, int FORM>
+template <int DIM, int FORM, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_apply_M(LevelDev L, CPtr3 u, const double* __restrict__ p, Ptr3 out_u, double* __restrict__ out_p,
           Box b, unsigned total) {
   {
     int ci[3];
     if (!box_point(b, ci)) return;
-    if (DIM == 3) m_face<3, FORM, 0>(L, u.p, p, out_u.p[0], ci);
-    m_face<DIM, FORM, 1>(L, u.p, p, out_u.p[1], ci);
-    m_face<DIM, FORM, 2>(L, u.p, p, out_u.p[2], ci);
+    if (DIM == 3) m_face<3, FORM, 0, PA>(L, u.p, p, out_u.p[0], ci);
+    m_face<DIM, FORM, 1, PA>(L, u.p, p, out_u.p[1], ci);
+    m_face<DIM, FORM, 2, PA>(L, u.p, p, out_u.p[2], ci);
     if (in_cell(L, ci)) {
       const int c = lin(L, ci);
-      out_p[c] = -(div_sum<DIM>(L, u.p, c, ci) * L.inv_h);
+      out_p[c] = -(div_sum<DIM, PA>(L, u.p, c, ci) * L.inv_h);
     }
   }
 }
@@ -1075,6 +1075,10 @@ int reduce_blocks() { return kRedBlocks; }
     default: { constexpr int FM = F_BULK; __VA_ARGS__; } break;         \
   }
 
+static bool all_periodic(const LevelDev& L) {
+  return L.bclo[0] == BC_PER && L.bclo[1] == BC_PER && L.bclo[2] == BC_PER;
+}
+
 static bool odd_periodic(const LevelDev& L, int dim) {
   for (int a = 3 - dim; a < 3; ++a)
     if (L.bclo[a] == BC_PER && (L.n[a] & 1)) return true;
@@ -1091,11 +1095,12 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
   const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    k_face_colour<DIM, FM, A, 0><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    if (all_periodic(L)) k_face_colour<DIM, FM, A, 0, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    else k_face_colour<DIM, FM, A, 0, false><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
   } else {
     ++g_kernel_launches;
-    k_face_colour<DIM, FM, A, 2><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
-    k_face_colour<DIM, FM, A, 1><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
+    k_face_colour<DIM, FM, A, 2, false><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
+    k_face_colour<DIM, FM, A, 1, false><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -1142,11 +1147,12 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
   const L3 c3 = cfg3(L.n[0], L.n[1], (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    k_cell_colour<DIM, 0><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
+    if (all_periodic(L)) k_cell_colour<DIM, 0, true><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
+    else k_cell_colour<DIM, 0, false><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
   } else {
     ++g_kernel_launches;
-    k_cell_colour<DIM, 2><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
-    k_cell_colour<DIM, 1><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
+    k_cell_colour<DIM, 2, false><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
+    k_cell_colour<DIM, 1, false><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -1177,7 +1183,8 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
       b = dim3(32, kThreads / 32, 1);
       g = dim3((cb.hi[2] - cb.lo[2] + 32) / 32, (cb.hi[1] - cb.lo[1] + b.y) / b.y, cb.hi[0] - cb.lo[0] + 1);
     }
-    k_face_rr_c<DIM, FM><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
+    if (all_periodic(Lf)) k_face_rr_c<DIM, FM, true><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
+    else k_face_rr_c<DIM, FM, false><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
   } else {
     constexpr int T = (A == 0) ? 1 : 0;
     const int e2 = cb.hi[2] - cb.lo[2] + 1;
@@ -1191,7 +1198,8 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
     const int chunk = (eA + nchunk - 1) / nchunk;
     nchunk = (eA + chunk - 1) / chunk;
     dim3 g(c3.g.x, c3.g.y, nchunk);
-    k_face_rr_m<DIM, FM, A><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
+    if (all_periodic(Lf)) k_face_rr_m<DIM, FM, A, true><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
+    else k_face_rr_m<DIM, FM, A, false><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
   }
 }
 
@@ -1215,8 +1223,14 @@ void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
   ++g_kernel_launches;
   Box cb = cell_box(Lc);
   const unsigned total = box_count(cb);
-  if (dim == 3) k_cell_rr<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
-  else k_cell_rr<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+  const bool pa = all_periodic(Lf);
+  if (dim == 3) {
+    if (pa) k_cell_rr<3, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+    else k_cell_rr<3, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+  } else {
+    if (pa) k_cell_rr<2, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+    else k_cell_rr<2, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+  }
 }
 
 void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
@@ -1259,8 +1273,13 @@ void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 
   Box b = full_box(L);
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
-    if (dim == 3) k_apply_M<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-    else k_apply_M<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    if (all_periodic(L)) {
+      if (dim == 3) k_apply_M<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+      else k_apply_M<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    } else {
+      if (dim == 3) k_apply_M<3, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+      else k_apply_M<2, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    }
   });
 }
 

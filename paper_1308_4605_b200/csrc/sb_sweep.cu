@@ -283,7 +283,7 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
           const SAcc<A, decltype(rb1), decltype(rb2), decltype(rmu), decltype(re1), decltype(re2)> acc{
               rb1, rb2, rmu, re1, re2, rrho.slot(p), p, o};
           double dg;
-          const double au = face_row_t<3, FORM, A>(L, s, acc, ca, dg);
+          const double au = face_row_t<3, FORM, A, false>(L, s, acc, ca, dg);
           const double res = rrhs.slot(p)[o] - au;
           R[jj * QK + kk] = s.c + omega * (res / dg);
         }
@@ -316,7 +316,7 @@ k_face_sweep2(LevelDev L, CPtr3 u, double* __restrict__ unew, const double* __re
         const SAcc<A, decltype(rb1), decltype(rb2), decltype(rmu), decltype(re1), decltype(re2)> acc{
             rb1, rb2, rmu, re1, re2, rrho.slot(pb), pb, o};
         double dg;
-        const double au = face_row_t<3, FORM, A>(L, s, acc, ca, dg);
+        const double au = face_row_t<3, FORM, A, false>(L, s, acc, ca, dg);
         const double res = rrhs.slot(pb)[o] - au;
         Rm[oq] = s.c + omega * (res / dg);
       }
@@ -428,7 +428,7 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
           s.m[2] = O1[o - 1];
           const SBeta<decltype(rb0), decltype(rb1), decltype(rb2)> ba{rb0, rb1, rb2, p, o};
           double dg;
-          const double lp = cell_row_t<3>(L, s, ba, ca, dg);
+          const double lp = cell_row_t<3, false>(L, s, ba, ca, dg);
           const double res = rrhs.slot(p)[o] - lp;
           R[jj * QK + kk] = s.c + omega * res / dg;
         }
@@ -458,7 +458,7 @@ k_cell_sweep2(LevelDev L, const double* __restrict__ phi, double* __restrict__ p
         const int o = (jj + 2) * RK + (k - k0 + 2);
         const SBeta<decltype(rb0), decltype(rb1), decltype(rb2)> ba{rb0, rb1, rb2, pb, o};
         double dg;
-        const double lp = cell_row_t<3>(L, s, ba, ca, dg);
+        const double lp = cell_row_t<3, false>(L, s, ba, ca, dg);
         const double res = rrhs.slot(pb)[o] - lp;
         Rm[oq] = s.c + omega * res / dg;
       }
