@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include "sb_kernels.h"
 
 namespace sb {
@@ -967,12 +968,77 @@ k_dcgs_b_stash(const double* __restrict__ Q, long long vstride, int nv, const do
   }
 }
 
+// pass B, L2-resident variant: a bounded grid (2 CTAs/SM) so the tile of the
+// basis read by the update loop is still in L2 (126 MB) when the dot loop
+// re-reads it; the update loop is unrolled for memory-level parallelism.
+constexpr int kL2Blocks = kSMs * 2;
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_b_l2(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
+            const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[kMaxVec + 1][kThreads / 32];
+  __shared__ double ds[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (nv + 1) * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) ds[i] = d[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += step) {
+    const bool ok = e < n2;
+    double2 wv = ok ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    int i = 0;
+    for (; i + 8 <= nv; i += 8) {
+      double2 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        a[u] = ok ? __ldg(reinterpret_cast<const double2*>(Q + (i + u) * vstride) + e) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        wv.x -= ds[i + u] * a[u].x;
+        wv.y -= ds[i + u] * a[u].y;
+      }
+    }
+    for (; i < nv; ++i) {
+      const double2 a = ok ? __ldg(reinterpret_cast<const double2*>(Q + i * vstride) + e) : make_double2(0.0, 0.0);
+      wv.x -= ds[i] * a.x;
+      wv.y -= ds[i] * a.y;
+    }
+    if (ok) o2[e] = wv;
+    i = 0;
+    for (; i + 8 <= nv; i += 8) {
+      double2 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        a[u] = ok ? __ldg(reinterpret_cast<const double2*>(Q + (i + u) * vstride) + e) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double sdot = warp_sum(a[u].x * wv.x + a[u].y * wv.y);
+        if (lane == 0) acc[i + u][warp] += sdot;
+      }
+    }
+    for (; i < nv; ++i) {
+      const double2 a = ok ? __ldg(reinterpret_cast<const double2*>(Q + i * vstride) + e) : make_double2(0.0, 0.0);
+      const double sdot = warp_sum(a.x * wv.x + a.y * wv.y);
+      if (lane == 0) acc[i][warp] += sdot;
+    }
+    const double nn = warp_sum(wv.x * wv.x + wv.y * wv.y);
+    if (lane == 0) acc[nv][warp] += nn;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= nv; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // out[i] = sum_b partials[i*kRedBlocks + b], fixed-order tree (deterministic)
-__global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out) {
+__global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out, int nblocks) {
   __shared__ double s[kThreads];
   const int i = blockIdx.x;
   double v = 0.0;
-  for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += partials[i * kRedBlocks + b];
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += partials[i * kRedBlocks + b];
   s[threadIdx.x] = v;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
@@ -1065,6 +1131,7 @@ k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __r
 // ===========================================================================
 
 long long g_kernel_launches = 0;
+static int g_red_blocks_used = kRedBlocks;  // partial slots written by the last reduction
 
 int reduce_blocks() { return kRedBlocks; }
 
@@ -1426,21 +1493,33 @@ void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const do
 void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
                    double* out, long long n, double* partials) {
   ++g_kernel_launches;
-  const size_t stash = (size_t)nv * kStashThreads * sizeof(double2);
-  if (stash <= 160 * 1024) {
-    static size_t configured = 0;
-    if (stash > configured) {
+  static const int variant = [] {
+    const char* e = std::getenv("SB_DCGS_B");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (variant == 1) {
+    const size_t stash = (size_t)nv * kStashThreads * sizeof(double2);
+    static bool configured = false;
+    if (!configured) {
       cudaFuncSetAttribute(k_dcgs_b_stash, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      configured = 160 * 1024;
+      configured = true;
     }
-    k_dcgs_b_stash<<<kRedBlocks, kStashThreads, stash, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
-  } else {
-    k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+    if (stash <= 160 * 1024) {
+      k_dcgs_b_stash<<<kRedBlocks, kStashThreads, stash, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+      return;
+    }
   }
+  if (variant == 2) {
+    k_dcgs_b_l2<<<kL2Blocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+    g_red_blocks_used = kL2Blocks;
+    return;
+  }
+  k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {
-  k_finalize<<<nv, kThreads, 0, s>>>(partials, out);
+  k_finalize<<<nv, kThreads, 0, s>>>(partials, out, g_red_blocks_used);
+  g_red_blocks_used = kRedBlocks;
 }
 
 void launch_sum_partial(cudaStream_t s, const double* x, long long n, double* partials) {
