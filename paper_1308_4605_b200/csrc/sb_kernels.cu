@@ -1033,6 +1033,112 @@ k_dcgs_b_l2(const double* __restrict__ Q, long long vstride, int nv, const doubl
   }
 }
 
+// Gram variant, pass A: like k_dcgs_a, plus the dots Q_l . s_k (l < k) and
+// s_k . s_k of the provisional vector, from which the host extends the Gram
+// matrix of the basis.  Partial slots: [0..k] Q.w with the finished q_k,
+// [k+1..2k] Q_l . s_k, [2k+1] s_k . s_k.
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_a_g(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+           const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nslot = 2 * k + 2;
+  for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    const double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    const double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    const double2 sa = ok0 ? s2[e] : make_double2(0.0, 0.0);
+    const double2 sb = ok1 ? s2[e1] : make_double2(0.0, 0.0);
+    double2 q0 = sa, q1 = sb;
+    for (int i = 0; i < k; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double ci = cs[i];
+      q0.x -= ci * a.x;
+      q0.y -= ci * a.y;
+      q1.x -= ci * b.x;
+      q1.y -= ci * b.y;
+      const double dw = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
+      const double dsv = warp_sum((a.x * sa.x + a.y * sa.y) + (b.x * sb.x + b.y * sb.y));
+      if (lane == 0) {
+        acc[i][warp] += dw;
+        acc[k + 1 + i][warp] += dsv;
+      }
+    }
+    if (k > 0) {
+      q0.x *= inv_gamma;
+      q0.y *= inv_gamma;
+      q1.x *= inv_gamma;
+      q1.y *= inv_gamma;
+      if (ok0) s2[e] = q0;
+      if (ok1) s2[e1] = q1;
+    }
+    const double dq = warp_sum((q0.x * w0.x + q0.y * w0.y) + (q1.x * wv1.x + q1.y * wv1.y));
+    const double ss = warp_sum((sa.x * sa.x + sa.y * sa.y) + (sb.x * sb.x + sb.y * sb.y));
+    if (lane == 0) {
+      acc[k][warp] += dq;
+      acc[2 * k + 1][warp] += ss;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
+// Gram variant, pass B: w' = w - sum_i d_i Q_i written to `out`, ||w'||^2 only
+// (one streaming read of the basis).
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
+           const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[kThreads / 32];
+  __shared__ double ds[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kThreads / 32) acc[threadIdx.x] = 0.0;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) ds[i] = d[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    for (int i = 0; i < nv; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double di = ds[i];
+      w0.x -= di * a.x;
+      w0.y -= di * a.y;
+      wv1.x -= di * b.x;
+      wv1.y -= di * b.y;
+    }
+    if (ok0) o2[e] = w0;
+    if (ok1) o2[e1] = wv1;
+    const double nn = warp_sum((w0.x * w0.x + w0.y * w0.y) + (wv1.x * wv1.x + wv1.y * wv1.y));
+    if (lane == 0) acc[warp] += nn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[kk];
+    partials[blockIdx.x] = s;
+  }
+}
+
 // out[i] = sum_b partials[i*kRedBlocks + b], fixed-order tree (deterministic)
 __global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out, int nblocks) {
   __shared__ double s[kThreads];
@@ -1515,6 +1621,18 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
     return;
   }
   k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+}
+
+void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
+                     const double* w, long long n, double* partials) {
+  ++g_kernel_launches;
+  k_dcgs_a_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+}
+
+void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
+                     double* out, long long n, double* partials) {
+  ++g_kernel_launches;
+  k_dcgs_b_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {

@@ -76,6 +76,11 @@ void launch_multi_dot(cudaStream_t s, const double* V, long long vstride, int nv
 void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* h,
                        double* w, long long n, double* partials, int mode);  // mode 0: dots, 1: norm
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out);
+// Gram-matrix variant of the delayed-reorthogonalisation passes
+void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
+                     const double* w, long long n, double* partials);
+void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
+                     double* out, long long n, double* partials);
 // delayed-reorthogonalisation Arnoldi passes (see sb_solver.cu gmres())
 void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                    const double* w, long long n, double* partials);

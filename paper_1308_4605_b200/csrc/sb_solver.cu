@@ -458,14 +458,15 @@ void mg_cell(sb_ctx* c, int ncyc, const double* rhs, double* out, const sb_smoot
 
 // ---- reductions ----------------------------------------------------------------
 
+// small device/host scratch: [h1: 3*kMaxVec][h2: kMaxVec][misc 64][y kMaxVec]
 double* dh1(sb_ctx* c) { return c->dsmall; }
-double* dh2(sb_ctx* c) { return c->dsmall + kMaxVec; }
-double* dmisc(sb_ctx* c) { return c->dsmall + 2 * kMaxVec; }
-double* dy(sb_ctx* c) { return c->dsmall + 2 * kMaxVec + 64; }
+double* dh2(sb_ctx* c) { return c->dsmall + 3 * kMaxVec; }
+double* dmisc(sb_ctx* c) { return c->dsmall + 4 * kMaxVec; }
+double* dy(sb_ctx* c) { return c->dsmall + 4 * kMaxVec + 64; }
 double* hh1(sb_ctx* c) { return c->hsmall; }
-double* hh2(sb_ctx* c) { return c->hsmall + kMaxVec; }
-double* hmisc(sb_ctx* c) { return c->hsmall + 2 * kMaxVec; }
-double* hy(sb_ctx* c) { return c->hsmall + 2 * kMaxVec + 64; }
+double* hh2(sb_ctx* c) { return c->hsmall + 3 * kMaxVec; }
+double* hmisc(sb_ctx* c) { return c->hsmall + 4 * kMaxVec; }
+double* hy(sb_ctx* c) { return c->hsmall + 4 * kMaxVec + 64; }
 
 // device sum of a full block into dmisc[slot]
 void block_sum(sb_ctx* c, const double* x, long long n, int slot) {
@@ -779,6 +780,11 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     const char* e = std::getenv("SB_ORTHO");
     return e && std::strcmp(e, "cgs2") == 0;
   }();
+  static const bool gram = [] {
+    const char* e = std::getenv("SB_ORTHO");
+    return e && std::strcmp(e, "gram") == 0;
+  }();
+  std::vector<double> G((m + 1) * (m + 1), 0.0);
   double gam = 1.0;
   int k = 0;
   bool first = true;
@@ -792,6 +798,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     if (beta == 0.0) return finish(SB_STATUS_CONVERGED);
     std::fill(H.begin(), H.end(), 0.0);
     std::fill(Horig.begin(), Horig.end(), 0.0);
+    std::fill(G.begin(), G.end(), 0.0);
     gam = 1.0;  // q_0 = r / beta is final: no pending correction
     std::fill(cs.begin(), cs.end(), 0.0);
     std::fill(sn.begin(), sn.end(), 0.0);
@@ -816,7 +823,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         launch_finalize(c->st, c->dpart, nv, dh2(c));
         launch_update_dot(c->st, V, vl, nv, dh2(c), c->vw, vl, c->dpart, 1);
         launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
-        CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
         sync(c);
         for (int i = 0; i <= j; ++i) H[i * m + j] = hh1(c)[i] + hh2(c)[i];
         hn = std::sqrt(hmisc(c)[1]);
@@ -829,17 +836,49 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         //  H[:j+1, j] = (d - Horig cpend + c')/gam_j,
         //  H[j+1, j]  = sqrt(||w'||^2 - ||c'||^2)/gam_j, and slot j+1 becomes
         //  s_{j+1} = w' with cpend = c', gam_{j+1} = sqrt(||w'||^2 - ||c'||^2).
+        // gram: c' = d - G d from the Gram matrix G = Q^T Q, maintained from the
+        // extra dots of pass A, so pass B streams the basis once (no re-read).
         for (int i = 0; i < j; ++i) hy(c)[i] = cpend[i];
         if (j > 0) CK(cudaMemcpyAsync(dh2(c), hy(c), j * 8, cudaMemcpyHostToDevice, c->st));
-        launch_dcgs_a(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
-        launch_finalize(c->st, c->dpart, j + 1, dh1(c));
-        launch_dcgs_b(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
-        launch_finalize(c->st, c->dpart, j + 2, dh2(c));
-        CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
-        sync(c);
-        double cc = 0.0;
+        double cc = 0.0, ww;
+        if (gram) {
+          launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
+          launch_finalize(c->st, c->dpart, 2 * j + 2, dh1(c));
+          launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
+          launch_finalize(c->st, c->dpart, 1, dh2(c) + kMaxVec - 1);
+          CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
+          sync(c);
+          const double* dd = hh1(c);
+          const double* sd = hh1(c) + j + 1;  // Q_l . s_j
+          const double ss = hh1(c)[2 * j + 1];
+          // extend G with the finished q_j = (s_j - Q_j cpend)/gam
+          double cgc = 0.0, csd = 0.0;
+          for (int l = 0; l < j; ++l) {
+            double gcl = 0.0;
+            for (int t = 0; t < j; ++t) gcl += G[l * (m + 1) + t] * cpend[t];
+            const double gjl = (sd[l] - gcl) / gam;
+            G[j * (m + 1) + l] = gjl;
+            G[l * (m + 1) + j] = gjl;
+            cgc += cpend[l] * gcl;
+            csd += cpend[l] * sd[l];
+          }
+          G[j * (m + 1) + j] = j == 0 ? ss : (ss - 2.0 * csd + cgc) / (gam * gam);
+          for (int i = 0; i <= j; ++i) {
+            double gd = 0.0;
+            for (int t = 0; t <= j; ++t) gd += G[i * (m + 1) + t] * dd[t];
+            hh2(c)[i] = dd[i] - gd;  // c'
+          }
+          ww = hh2(c)[kMaxVec - 1];
+        } else {
+          launch_dcgs_a(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
+          launch_finalize(c->st, c->dpart, j + 1, dh1(c));
+          launch_dcgs_b(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
+          launch_finalize(c->st, c->dpart, j + 2, dh2(c));
+          CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
+          sync(c);
+          ww = hh2(c)[j + 1];
+        }
         for (int i = 0; i <= j; ++i) cc += hh2(c)[i] * hh2(c)[i];
-        const double ww = hh2(c)[j + 1];
         const double g2 = std::max(ww - cc, 0.0);
         const double gnext = std::sqrt(g2);
         for (int i = 0; i <= j; ++i) {
@@ -977,9 +1016,9 @@ sb_ctx* sb_create(int dim, const int* cells, double h, const int* bc, int viscou
     CK(cudaMalloc(&fl, 16));
     c->allocs.push_back(fl);
     c->dflags = fl;
-    c->dpart = dalloc(c, (long long)kMaxVec * reduce_blocks());
-    c->dsmall = dalloc(c, 4 * kMaxVec);
-    CK(cudaMallocHost(&c->hsmall, 4 * kMaxVec * 8));
+    c->dpart = dalloc(c, (long long)(2 * kMaxVec + 2) * reduce_blocks());
+    c->dsmall = dalloc(c, 8 * kMaxVec);
+    CK(cudaMallocHost(&c->hsmall, 8 * kMaxVec * 8));
     c->launches_base = g_kernel_launches;
     sync(c);
     return SB_OK;
