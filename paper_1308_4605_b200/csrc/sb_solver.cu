@@ -780,9 +780,10 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     const char* e = std::getenv("SB_ORTHO");
     return e && std::strcmp(e, "cgs2") == 0;
   }();
+  // default: Gram variant; SB_ORTHO=dcgs re-reads the basis for c', =cgs2 three passes
   static const bool gram = [] {
     const char* e = std::getenv("SB_ORTHO");
-    return e && std::strcmp(e, "gram") == 0;
+    return !(e && (std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
   }();
   std::vector<double> G((m + 1) * (m + 1), 0.0);
   double gam = 1.0;
