@@ -200,6 +200,25 @@ __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* 
   return 0.5 * (m0 + m1);
 }
 
+// Small levels: one thread per coarse face, all 3 (or 2D: 3) normal offsets
+// evaluated by that thread (fine residuals on odd normal planes computed twice;
+// parallelism matters more than redundancy below ~32^3).
+template <int DIM, int FORM, int A, bool PA>
+__global__ void __launch_bounds__(kThreads)
+k_face_rr_s(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
+            Box cb, unsigned total) {
+  int C[3];
+  if (!box_point(cb, C)) return;
+  double tv[3];
+#pragma unroll 1
+  for (int o = -1; o <= 1; ++o) {
+    int fa = 2 * C[A] + o;
+    if (fa < 0) fa += Lf.n[A];
+    tv[o + 1] = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, fa);
+  }
+  coarse[lin(Lc, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
+}
+
 // Fused residual -> restriction, each fine residual evaluated once.
 // A == 2 (contiguous axis): lanes run along coarse K; t(2K-1) is the previous
 // lane's t(2K+1) (warp shuffle), lane 0 evaluates it itself.
@@ -1349,6 +1368,12 @@ template <int DIM, int FM, int A>
 static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CPtr3 u, const double* rhs,
                       double* coarse) {
   Box cb = face_box(Lc, DIM, A);
+  const unsigned ncoarse = box_count(cb);
+  if (ncoarse < 32768u) {  // small level: thread per coarse face
+    if (all_periodic(Lf)) k_face_rr_s<DIM, FM, A, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, ncoarse);
+    else k_face_rr_s<DIM, FM, A, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, ncoarse);
+    return;
+  }
   if (A == 2) {
     const L3 c3 = cfg3(cb.hi[0] - cb.lo[0] + 1, cb.hi[1] - cb.lo[1] + 1, cb.hi[2] - cb.lo[2] + 1);
     dim3 b = c3.b, g = c3.g;
