@@ -194,6 +194,33 @@ long long sb_device_bytes(sb_ctx* ctx);
  * CUDA events recorded there bracket the solve */
 int sb_set_stream(sb_ctx* ctx, void* stream);
 
+/* ---- slab-decomposed multi-GPU solve ----------
+ * The global 3D grid is cut along axis 0 (must be periodic) into
+ * nranks x nslab slabs; a process owns nslab consecutive slabs.  nranks > 1:
+ * one slab per process, one GPU per process, NCCL halo exchange / allreduce /
+ * allgather (communicator from sb_nccl_unique_id on rank 0, broadcast by the
+ * caller).  nranks == 1 with nslab > 1 runs the same decomposition on one GPU.
+ * Array arguments hold THIS RANK's planes [rank*n0r, (rank+1)*n0r) of the
+ * reference layouts (n0r = N0 / nranks).  Replaces the same seams as
+ * sb_set_coefficients / sb_apply_M / sb_precond_apply / sb_gmres_solve
+ * (operators.py:107, :363; precond.py:111; krylov.py:164). */
+typedef struct sb_dist sb_dist;
+int sb_nccl_id_bytes(void);
+int sb_nccl_unique_id(unsigned char* out);
+sb_dist* sb_dist_create(const int* cells, double h, const int* bc, int viscous_form, int nranks, int rank,
+                        int nslab, const unsigned char* nccl_id);
+void sb_dist_destroy(sb_dist* dist);
+/* out[4] = {distributed levels, agglomerated levels, planes per slab, slabs in this process} */
+int sb_dist_info(sb_dist* dist, int* out);
+int sb_dist_set_coefficients(sb_dist* dist, double theta, const double* const* rho_face, const double* mu_cell,
+                             const double* const* mu_edge, const double* gamma_cell);
+int sb_dist_apply_M(sb_dist* dist, const double* const* u, const double* p, double* const* out_u, double* out_p);
+int sb_dist_precond_apply(sb_dist* dist, const sb_precond* pc, const sb_smoother* sm, const double* const* r_u,
+                          const double* r_p, double* const* x_u, double* x_p);
+int sb_dist_gmres_solve(sb_dist* dist, const sb_precond* pc, const sb_gmres* gc, const sb_smoother* sm,
+                        const double* const* b_u, const double* b_p, double* const* x_u, double* x_p,
+                        sb_history_row* rows, int max_rows, int* n_rows, int* status, long long* scalar_vcycles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,8 @@ enum { BC_PER = 0, BC_NOSLIP = 1, BC_FREESLIP = 2 };
 enum { F_LAP = 0, F_STRESS = 1, F_BULK = 2 };
 
 struct LevelDev {
-  int n[3];          // cells per internal axis
+  int n[3];          // cells per internal axis (axis 0: this slab's planes when distributed)
+  int dist0;         // axis 0 is slab-distributed: neighbours come from 2 ghost planes, no wrap
   int bclo[3], bchi[3];
   int s0, s1;        // strides of axes 0 and 1 (axis 2 is contiguous); boxes < 2^31 points
   double h, inv_h, inv_h2, theta;
@@ -40,13 +41,18 @@ __device__ __forceinline__ int stride(const LevelDev& L) {
 }
 
 // index shift to the +1 / -1 neighbour along AX of coordinate c (periodic wrap)
+// periodic wrap along AX, except along a slab-distributed axis 0 (ghosts)
+template <int AX, bool PA = false>
+__device__ __forceinline__ bool wraps(const LevelDev& L) {
+  return perq<PA>(L, AX) && !(AX == 0 && L.dist0);
+}
 template <int AX, bool PA = false>
 __device__ __forceinline__ int dplus(const LevelDev& L, int c) {
-  return (perq<PA>(L, AX) && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
+  return (wraps<AX, PA>(L) && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
 }
 template <int AX, bool PA = false>
 __device__ __forceinline__ int dminus(const LevelDev& L, int c) {
-  return (perq<PA>(L, AX) && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
+  return (wraps<AX, PA>(L) && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
 }
 
 __device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + i); }
@@ -127,7 +133,7 @@ struct GAcc {
   __device__ __forceinline__ double divh(bool lo) const {
     if (!lo) return div_sum<DIM, PA>(L, u, f, ci);
     int clo[3] = {ci[0], ci[1], ci[2]};
-    clo[A] = (perq<PA>(L, A) && ci[A] == 0) ? L.n[A] - 1 : ci[A] - 1;
+    clo[A] = (perq<PA>(L, A) && ci[A] == 0 && !(A == 0 && L.dist0)) ? L.n[A] - 1 : ci[A] - 1;
     return div_sum<DIM, PA>(L, u, f + dmA, clo);
   }
 };

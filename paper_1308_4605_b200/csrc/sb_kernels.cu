@@ -213,7 +213,7 @@ k_face_rr_s(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
 #pragma unroll 1
   for (int o = -1; o <= 1; ++o) {
     int fa = 2 * C[A] + o;
-    if (fa < 0) fa += Lf.n[A];
+    if (fa < 0 && !(A == 0 && Lf.dist0)) fa += Lf.n[A];
     tv[o + 1] = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, fa);
   }
   coarse[lin(Lc, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
@@ -239,7 +239,7 @@ k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   const int lane = threadIdx.x & 31;
   if (lane == 0 || Cs[A] == cb.lo[A]) {
     int fa = 2 * Cs[A] - 1;
-    if (fa < 0) fa += Lf.n[A];
+    if (fa < 0 && !(A == 0 && Lf.dist0)) fa += Lf.n[A];
     tm = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, Cs, fa);
   }
   if (ok) coarse[lin(Lc, C)] = (0.25 * tm + 0.5 * t0) + 0.25 * t1;
@@ -265,7 +265,7 @@ k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   const int a1 = min(a0 + chunk - 1, cb.hi[A]);
   C[A] = a0;
   int fa = 2 * a0 - 1;
-  if (fa < 0) fa += Lf.n[A];
+  if (fa < 0 && !(A == 0 && Lf.dist0)) fa += Lf.n[A];
   double tm = tmean_resid<DIM, FORM, A, PA>(Lf, u.p, rhs, C, fa);
 #pragma unroll 1
   for (int c = a0; c <= a1; ++c) {
@@ -330,7 +330,9 @@ __device__ __forceinline__ void tang_pair(const LevelDev& Lc, int ax, int fine_i
   J = fine_i >> 1;
   nb = (fine_i & 1) ? J + 1 : J - 1;
   const int n = Lc.n[ax];
-  if (Lc.bclo[ax] == BC_PER) {
+  if (ax == 0 && Lc.dist0) {
+    // ghost planes hold the neighbouring slabs' values
+  } else if (Lc.bclo[ax] == BC_PER) {
     if (nb < 0) nb += n;
     if (nb >= n) nb -= n;
   } else {
@@ -378,7 +380,7 @@ k_face_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* _
       v = T(I);
     } else {
       int I2 = I + 1;
-      if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A]) I2 = 0;
+      if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A] && !(A == 0 && Lc.dist0)) I2 = 0;
       v = 0.5 * (T(I) + T(I2));
     }
     const int f = lin(Lf, F);
@@ -731,6 +733,8 @@ __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double 
     x[i] = x[i] - m;
   }
 }
+
+__global__ void k_add_scalar(double* y, const double* x) { *y += *x; }
 
 __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, Box b, unsigned total) {
   {
@@ -1596,6 +1600,11 @@ void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, 
   ++g_kernel_launches;
   const unsigned total = box_count(b);
   k_box_sub_mean<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, sum, inv_count, b, total);
+}
+
+void launch_axpy_scalar(cudaStream_t s, double* y, const double* x) {
+  ++g_kernel_launches;
+  k_add_scalar<<<1, 1, 0, s>>>(y, x);
 }
 
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x) {

@@ -68,6 +68,7 @@ void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double
 void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, const double* sum,
                            double inv_count);  // x -= sum*inv_count
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x);  // y += x
+void launch_axpy_scalar(cudaStream_t s, double* y, const double* x);  // *y += *x (one thread)
 
 // flat-vector kernels (GMRES; whole padded box, pads are zero)
 int reduce_blocks();

@@ -968,6 +968,52 @@ int guard(F&& f) {
   }
 }
 
+
+// Coarsen the level-0 coefficients (already on the device) down the hierarchy,
+// derive 1/rho_face, run the zero-diagonal / positive-density checks and the
+// velocity null space (multigrid.py:92-169, :70-89; operators.py:368-388).
+void build_from_level0(sb_ctx* c) {
+    for (size_t l = 0; l + 1 < c->lv.size(); ++l) {
+      Level& F = c->lv[l];
+      Level& C = c->lv[l + 1];
+      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.mu_c, C.mu_c);
+      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.gam_c, C.gam_c);
+      for (int A = c->off; A < 3; ++A) launch_coarsen_face(c->st, F.d, C.d, c->dim, A, F.rho_f[A], C.rho_f[A]);
+      if (c->dim == 3) {
+        for (int e = 0; e < 3; ++e) launch_coarsen_edge(c->st, F.d, C.d, 3, e, F.mu_e[e], C.mu_e[e]);
+      } else {
+        launch_coarsen_edge(c->st, F.d, C.d, 2, 0, F.mu_e[0], C.mu_e[0]);
+      }
+    }
+    CK(cudaMemsetAsync(c->dflags, 0, 16, c->st));
+    int hf[4] = {0, 0, 0, 0};
+    for (size_t l = 0; l < c->lv.size(); ++l) {
+      Level& L = c->lv[l];
+      for (int A = c->off; A < 3; ++A) launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2);
+    }
+    for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
+    CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    c->flag_face = hf[0] & 1;
+    c->flag_cell = (hf[0] >> 1) & 1;
+    c->flag_rho = hf[2] & 1;
+    // operators.py:368-388 velocity_null_components
+    c->null_comps.clear();
+    if (c->theta == 0.0) {
+      for (int A = c->off; A < 3; ++A) {
+        if (c->bc[A][0] != BC_PER) continue;
+        bool ok = true;
+        for (int B = c->off; B < 3; ++B) {
+          if (B == A) continue;
+          const bool pb = c->bc[B][0] == BC_PER;
+          const bool fs = c->bc[B][0] == BC_FREESLIP && c->bc[B][1] == BC_FREESLIP;
+          if (!(pb || fs)) ok = false;
+        }
+        if (ok) c->null_comps.push_back(A);
+      }
+    }
+}
+
 }  // namespace
 
 // ====================================================================================
@@ -1062,45 +1108,7 @@ int sb_set_coefficients(sb_ctx* c, double theta, const double* const* rho_face, 
     } else {
       copy_in(c, L0, 10, mu_edge[0], L0.mu_e[0]);
     }
-    for (size_t l = 0; l + 1 < c->lv.size(); ++l) {
-      Level& F = c->lv[l];
-      Level& C = c->lv[l + 1];
-      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.mu_c, C.mu_c);
-      launch_coarsen_cellmean(c->st, F.d, C.d, c->dim, F.gam_c, C.gam_c);
-      for (int A = c->off; A < 3; ++A) launch_coarsen_face(c->st, F.d, C.d, c->dim, A, F.rho_f[A], C.rho_f[A]);
-      if (c->dim == 3) {
-        for (int e = 0; e < 3; ++e) launch_coarsen_edge(c->st, F.d, C.d, 3, e, F.mu_e[e], C.mu_e[e]);
-      } else {
-        launch_coarsen_edge(c->st, F.d, C.d, 2, 0, F.mu_e[0], C.mu_e[0]);
-      }
-    }
-    CK(cudaMemsetAsync(c->dflags, 0, 16, c->st));
-    int hf[4] = {0, 0, 0, 0};
-    for (size_t l = 0; l < c->lv.size(); ++l) {
-      Level& L = c->lv[l];
-      for (int A = c->off; A < 3; ++A) launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2);
-    }
-    for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
-    CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    c->flag_face = hf[0] & 1;
-    c->flag_cell = (hf[0] >> 1) & 1;
-    c->flag_rho = hf[2] & 1;
-    // operators.py:368-388 velocity_null_components
-    c->null_comps.clear();
-    if (theta == 0.0) {
-      for (int A = c->off; A < 3; ++A) {
-        if (c->bc[A][0] != BC_PER) continue;
-        bool ok = true;
-        for (int B = c->off; B < 3; ++B) {
-          if (B == A) continue;
-          const bool pb = c->bc[B][0] == BC_PER;
-          const bool fs = c->bc[B][0] == BC_FREESLIP && c->bc[B][1] == BC_FREESLIP;
-          if (!(pb || fs)) ok = false;
-        }
-        if (ok) c->null_comps.push_back(A);
-      }
-    }
+    build_from_level0(c);
     c->have_coef = true;
     return SB_OK;
   });
@@ -1371,3 +1379,6 @@ int sb_set_stream(sb_ctx* c, void* stream) {
 }
 
 }  // extern "C"
+
+// slab-decomposed multi-GPU path (shares this translation unit)
+#include "sb_dist.inc"

@@ -514,7 +514,7 @@ void launch_face_a(cudaStream_t s, const LevelDev& L, CPtr3 u, double* unew, con
 }  // namespace
 
 bool sweep2_supported(const LevelDev& L, int dim, int form) {
-  if (dim != 3 || form == F_BULK) return false;
+  if (dim != 3 || form == F_BULK || L.dist0) return false;
   for (int a = 0; a < 3; ++a)
     if (L.n[a] < 8 || (L.bclo[a] == BC_PER && (L.n[a] & 1))) return false;
   return true;
