@@ -210,6 +210,8 @@ int sb_nccl_unique_id(unsigned char* out);
 sb_dist* sb_dist_create(const int* cells, double h, const int* bc, int viscous_form, int nranks, int rank,
                         int nslab, const unsigned char* nccl_id);
 void sb_dist_destroy(sb_dist* dist);
+/* the CUDA stream the distributed context launches on (cudaStream_t) */
+void* sb_dist_stream(sb_dist* dist);
 /* out[4] = {distributed levels, agglomerated levels, planes per slab, slabs in this process} */
 int sb_dist_info(sb_dist* dist, int* out);
 int sb_dist_set_coefficients(sb_dist* dist, double theta, const double* const* rho_face, const double* mu_cell,

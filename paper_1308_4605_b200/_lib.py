@@ -27,7 +27,7 @@ EXPORTS = (
     "sb_num_levels", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
-    "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info",
+    "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
     "sb_dist_set_coefficients", "sb_dist_apply_M", "sb_dist_precond_apply", "sb_dist_gmres_solve",
 )
 
@@ -94,6 +94,7 @@ _SIGS = {
     "sb_dist_create": (_P, [C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int,
                             C.c_int, C.c_char_p]),
     "sb_dist_destroy": (None, [_P]),
+    "sb_dist_stream": (_P, [_P]),
     "sb_dist_info": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "sb_dist_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
     "sb_dist_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),

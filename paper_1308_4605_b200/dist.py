@@ -80,13 +80,21 @@ class DistSolver:
         self.h = h
         self.scalar_vcycles = 0
 
+    def stream_ptr(self) -> int:
+        return int(self.lib.sb_dist_stream(self.h) or 0)
+
     def info(self) -> dict:
         out = (C.c_int * 4)()
         self.lib.sb_dist_info(self.h, out)
         return {"distributed_levels": out[0], "agglomerated_levels": out[1], "planes_per_slab": out[2],
                 "slabs": out[3]}
 
+    #: arrays passed in already hold only this rank's planes (bench: slab-local generation)
+    local_inputs = False
+
     def _mine(self, x):
+        if self.local_inputs:
+            return _f64(x)
         return _f64(rank_planes(np.asarray(x), self.nranks, self.rank))
 
     def set_coefficients(self, coeff):

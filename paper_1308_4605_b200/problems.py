@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .grid import NO_SLIP, PERIODIC, CellField, FaceField, GridSpec, StokesVector
+from .grid import NO_SLIP, PERIODIC, CellField, FaceField, GridSpec, NodeEdgeField, StokesVector
 from .operators import STRESS, make_coefficients, rescale
 
 
@@ -200,3 +200,77 @@ def make_case(name: str, n: int | tuple | None = None, seed: int = 1308) -> Case
 def prepare(case: Case):
     """Apply ``rescale`` as the reference CLI does; returns (coeff', rhs', spec)."""
     return rescale(case.coeff, case.rhs)
+
+
+def c5_cells(n_gpus: int):
+    """C5 weak scaling at h = 1/512: 256^3 per GPU (1 GPU 256^3,
+    2 GPUs 512x256x256, 4 GPUs 512x512x256, 8 GPUs 512^3)."""
+    return {1: (256, 256, 256), 2: (512, 256, 256), 4: (512, 512, 256), 8: (512, 512, 512)}.get(
+        n_gpus, (256 * n_gpus, 256, 256))
+
+
+def make_c5_slab(cells, nranks: int, rank: int, seed: int = 1308, reduce=None):
+    """This rank's axis-0 planes of the C5 recipe on the global box `cells`
+    (h = 1/512), generated without materialising the global fields.
+
+    The log-viscosity Fourier field is evaluated on the rank's planes plus one
+    plane each side (for the face / edge averages); its global min/max comes
+    from `reduce(local_min, local_max) -> (gmin, gmax)` (torch.distributed in
+    the bench).  Forces and divergence source draw from per-rank Philox streams
+    and get their global means removed through `reduce` as well
+    (`reduce(sum, count)`).  Returns (grid, coeff, rhs) with rank-local arrays;
+    coefficient/rhs arrays hold exactly the rank's planes."""
+    from .grid import FaceField
+    grid = GridSpec(tuple(cells), 1.0 / 512, _bc("ppp"))
+    n0 = cells[0] // nranks
+    lo = rank * n0
+    s_coef = streams(seed)[0]
+    # modes: identical on every rank (same stream)
+    modes = []
+    for _ in range(8):
+        while True:
+            k = s_coef.integers(-4, 5, size=3)
+            if np.any(k != 0):
+                break
+        modes.append((k, s_coef.uniform(0.0, 2.0 * np.pi)))
+    L = grid.lengths
+    xs = [(np.arange(n) + 0.5) * grid.h for n in cells]
+    x0 = (np.arange(lo - 1, lo + n0 + 1) + 0.5) * grid.h  # one extra plane each side (periodic field)
+    F = np.zeros((n0 + 2, cells[1], cells[2]))
+    for k, phi in modes:
+        arg = phi + (2 * np.pi * k[0] / L[0]) * x0[:, None, None] + \
+            (2 * np.pi * k[1] / L[1]) * xs[1][None, :, None] + (2 * np.pi * k[2] / L[2]) * xs[2][None, None, :]
+        F += np.cos(arg)
+    fmin, fmax = reduce("minmax", float(F[1:-1].min()), float(F[1:-1].max()))
+    mu_ext = 10.0 ** (3.0 * (F - fmin) / (fmax - fmin))
+    mu = mu_ext[1:-1]
+    # face / edge averages along axis 0 use the neighbour plane below (periodic)
+    rho_f = [np.ones((n0, cells[1], cells[2])) for _ in range(3)]
+    from .operators import _stagger_mean, CoefficientSet
+    mu0 = 0.5 * (mu_ext[1:-1] + mu_ext[:-2])          # staggered along axis 0
+    e01 = _stagger_mean(mu0, 1, True)                   # edges (0,1)
+    e02 = _stagger_mean(mu0, 2, True)                   # edges (0,2)
+    e12 = _stagger_mean(_stagger_mean(mu, 1, True), 2, True)
+    local = GridSpec((n0, cells[1], cells[2]), grid.h, grid.bc)
+    coeff = CoefficientSet.__new__(CoefficientSet)
+    coeff.theta = 0.0
+    coeff.rho_cell = CellField(local, np.ones((n0, cells[1], cells[2])))
+    coeff.rho_face = FaceField(local, tuple(rho_f))
+    coeff.mu_cell = CellField(local, mu)
+    coeff.mu_node_edge = NodeEdgeField(local, {(0, 1): e01, (0, 2): e02, (1, 2): e12})
+    coeff.gamma_cell = CellField.zeros(local)
+    coeff.viscous_form = STRESS
+    gens = [np.random.Generator(np.random.Philox(s)) for s in np.random.SeedSequence([seed, rank]).spawn(4)]
+    f = [gens[1].standard_normal((n0, cells[1], cells[2])) for _ in range(3)]
+    gsrc = gens[2].standard_normal((n0, cells[1], cells[2]))
+    cnt = float(np.prod(cells))
+    for a in range(3):
+        f[a] -= reduce("sum", float(f[a].sum()), 0.0)[0] / cnt
+    gsrc -= reduce("sum", float(gsrc.sum()), 0.0)[0] / cnt
+    # rescale (operators.py:532-550): c = h / max(mu) over the GLOBAL field
+    mmax = reduce("minmax", float(mu.min()), float(mu.max()))[1]
+    c = grid.h / mmax
+    coeff.mu_cell = CellField(local, c * mu)
+    coeff.mu_node_edge = NodeEdgeField(local, {k: c * v for k, v in coeff.mu_node_edge.arrays.items()})
+    rhs = StokesVector(FaceField(local, tuple(c * x for x in f)), CellField(local, -gsrc))
+    return grid, coeff, rhs, c
