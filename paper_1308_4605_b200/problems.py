@@ -274,3 +274,93 @@ def make_c5_slab(cells, nranks: int, rank: int, seed: int = 1308, reduce=None):
     coeff.mu_node_edge = NodeEdgeField(local, {k: c * v for k, v in coeff.mu_node_edge.arrays.items()})
     rhs = StokesVector(FaceField(local, tuple(c * x for x in f)), CellField(local, -gsrc))
     return grid, coeff, rhs, c
+
+
+# ---------------------------------------------------------------------------
+# the paper's bubble problem (reference problems.py:36-135, 170-199), used by
+# the acceptance criteria (tests/test_gpu_acceptance.py)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class BubbleSpec:
+    """Smoothed sphere/disk: (r+1)/2 + (r-1)/2 tanh(d/eps) + noise_amp * U(0,1)."""
+
+    r_mu: float = 100.0
+    r_rho: float = 100.0
+    epsilon: float | None = None
+    radius: float | None = None
+    noise_amp: float = 0.1
+    seed: int = 0
+    positive_outside: bool = True
+
+    def __post_init__(self):
+        if self.r_mu < 1 or self.r_rho < 1:
+            raise ValueError("contrast ratios must be >= 1")
+        if self.epsilon is not None and not self.epsilon > 0:
+            raise ValueError("smoothing width must be positive")
+
+
+def bubble_profile(grid, r, spec, noise):
+    xs = grid.cell_centers()
+    centre = [0.5 * L for L in grid.lengths]
+    radius = spec.radius if spec.radius is not None else 0.25 * max(grid.lengths)
+    eps = spec.epsilon if spec.epsilon is not None else grid.h
+    d = np.sqrt(sum((x - c) ** 2 for x, c in zip(xs, centre))) - radius
+    if not spec.positive_outside:
+        d = -d
+    f = 0.5 * (r + 1.0) + 0.5 * (r - 1.0) * np.tanh(d / eps)
+    if noise is not None:
+        f = f + spec.noise_amp * noise
+    return f
+
+
+def bubble_coefficients(grid, spec, theta=0.0, viscous_form=STRESS, mu0=1.0, rho0=1.0, gamma0=0.0):
+    g_mu, g_rho = streams(spec.seed, 2)
+    n_mu = g_mu.random(grid.cells) if spec.noise_amp else None
+    n_rho = g_rho.random(grid.cells) if spec.noise_amp else None
+    mu = CellField(grid, mu0 * bubble_profile(grid, spec.r_mu, spec, n_mu))
+    rho = CellField(grid, rho0 * bubble_profile(grid, spec.r_rho, spec, n_rho))
+    gam = CellField.full(grid, gamma0) if gamma0 else CellField.zeros(grid)
+    return make_coefficients(grid, theta, rho, mu, gam, viscous_form)
+
+
+def bubble_density(grid, spec, rho0=1.0):
+    _, g_rho = streams(spec.seed, 2)
+    noise = g_rho.random(grid.cells) if spec.noise_amp else None
+    return CellField(grid, rho0 * bubble_profile(grid, spec.r_rho, spec, noise))
+
+
+def inviscid_coefficients(grid, rho_cell, theta=1.0):
+    from .operators import CoefficientSet, average_cell_to_faces, average_cell_to_node_edge
+    zero = CellField.zeros(grid)
+    return CoefficientSet(theta=theta, rho_cell=rho_cell, rho_face=average_cell_to_faces(rho_cell),
+                          mu_cell=zero, mu_node_edge=average_cell_to_node_edge(zero),
+                          gamma_cell=CellField.zeros(grid), viscous_form=STRESS)
+
+
+def project_nulls(x, coeff):
+    from .operators import velocity_null_components
+    out = x.copy()
+    out.p.data -= out.p.data.mean()
+    for a in velocity_null_components(x.grid, coeff):
+        v = out.u.interior(a)
+        v -= v.mean()
+    return out
+
+
+def make_rhs(grid, coeff, seed=0):
+    """Random consistent rhs = M x_exact with x_exact drawn in the unknown space
+    (M applied on the device)."""
+    from .grid import norm2
+    from .operators import apply_M
+    for gen in streams(seed, 4):
+        x = StokesVector.zeros(grid)
+        for a in range(grid.dim):
+            v = x.u.interior(a)
+            v[...] = gen.standard_normal(v.shape)
+        x.p.data[...] = gen.standard_normal(grid.cells)
+        x = project_nulls(x, coeff)
+        if norm2(x) > 1e-8 * math.sqrt(grid.n_unknowns()):
+            return apply_M(x, coeff), x
+    raise RuntimeError("could not draw a nondegenerate solution")
