@@ -1120,6 +1120,81 @@ k_dcgs_a_g(double* __restrict__ Q, long long vstride, int k, const double* __res
   }
 }
 
+// Same as k_dcgs_a_g, register-chunked: every thread owns CH double2 of each
+// vector per step, so the two warp reductions per basis vector are amortised
+// over 2*CH elements (instead of 4) and CH independent loads are in flight.
+template <int CH>
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nslot = 2 * k + 2;
+  for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long span = (long long)blockDim.x * CH;
+  for (long long base = blockIdx.x * span; base < n2; base += (long long)gridDim.x * span) {
+    double2 wv[CH], sv[CH], q[CH];
+    bool ok[CH];
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      const long long e = base + t * blockDim.x + threadIdx.x;
+      ok[t] = e < n2;
+      wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
+      q[t] = sv[t];
+    }
+    for (int i = 0; i < k; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      double2 a[CH];
+#pragma unroll
+      for (int t = 0; t < CH; ++t) a[t] = ok[t] ? __ldg(v2 + base + t * blockDim.x + threadIdx.x) : make_double2(0.0, 0.0);
+      const double ci = cs[i];
+      double dw = 0.0, dsv = 0.0;
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        q[t].x -= ci * a[t].x;
+        q[t].y -= ci * a[t].y;
+        dw += a[t].x * wv[t].x + a[t].y * wv[t].y;
+        dsv += a[t].x * sv[t].x + a[t].y * sv[t].y;
+      }
+      dw = warp_sum(dw);
+      dsv = warp_sum(dsv);
+      if (lane == 0) {
+        acc[i][warp] += dw;
+        acc[k + 1 + i][warp] += dsv;
+      }
+    }
+    double dq = 0.0, ss = 0.0;
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      if (k > 0) {
+        q[t].x *= inv_gamma;
+        q[t].y *= inv_gamma;
+        if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+      }
+      dq += q[t].x * wv[t].x + q[t].y * wv[t].y;
+      ss += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+    }
+    dq = warp_sum(dq);
+    ss = warp_sum(ss);
+    if (lane == 0) {
+      acc[k][warp] += dq;
+      acc[2 * k + 1][warp] += ss;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // Gram variant, pass B: w' = w - sum_i d_i Q_i written to `out`, ||w'||^2 only
 // (one streaming read of the basis).
 __global__ void __launch_bounds__(kThreads)
@@ -1660,7 +1735,12 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                      const double* w, long long n, double* partials) {
   ++g_kernel_launches;
-  k_dcgs_a_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+  static const bool chunked = [] {
+    const char* e = std::getenv("SB_DCGS_A");
+    return !(e && e[0] == '0');
+  }();
+  if (chunked) k_dcgs_a_g2<4><<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+  else k_dcgs_a_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
