@@ -194,6 +194,10 @@ long long sb_device_bytes(sb_ctx* ctx);
  * CUDA events recorded there bracket the solve */
 int sb_set_stream(sb_ctx* ctx, void* stream);
 
+/* page-locked host buffers (the Python API recycles them for returned arrays) */
+void* sb_host_alloc(long long bytes);
+void sb_host_free(void* ptr);
+
 /* ---- slab-decomposed multi-GPU solve ----------
  * The global 3D grid is cut along axis 0 (must be periodic) into
  * nranks x nslab slabs; a process owns nslab consecutive slabs.  nranks > 1:

@@ -29,6 +29,7 @@ EXPORTS = (
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
     "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
     "sb_dist_set_coefficients", "sb_dist_apply_M", "sb_dist_precond_apply", "sb_dist_gmres_solve",
+    "sb_host_alloc", "sb_host_free",
 )
 
 
@@ -95,6 +96,8 @@ _SIGS = {
                             C.c_int, C.c_char_p]),
     "sb_dist_destroy": (None, [_P]),
     "sb_dist_stream": (_P, [_P]),
+    "sb_host_alloc": (_P, [C.c_longlong]),
+    "sb_host_free": (None, [_P]),
     "sb_dist_info": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "sb_dist_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
     "sb_dist_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),
@@ -156,3 +159,36 @@ def ptr(a) -> int:
 def parr(arrs):
     vals = [C.c_void_p(ptr(a) if a is not None else 0) for a in arrs]
     return (C.c_void_p * max(len(vals), 1))(*vals)
+
+
+class PinnedPool:
+    """Recycled page-locked host buffers for arrays the API returns.
+
+    D2H copies into fresh pageable NumPy pages run at a fraction of PCIe speed
+    (first-touch faults + staging); a returned array is a view of a pinned
+    buffer that goes back to the pool when the array is garbage-collected.
+    """
+
+    def __init__(self):
+        self.free = {}
+
+    def array(self, shape):
+        import weakref
+        n = int(np.prod(shape)) * 8
+        lst = self.free.get(n)
+        p = lst.pop() if lst else None
+        if p is None:
+            p = load().sb_host_alloc(max(n, 8))
+            if not p:
+                return np.zeros(shape)
+        buf = (C.c_double * max(int(np.prod(shape)), 1)).from_address(p)
+        arr = np.frombuffer(buf, dtype=np.float64, count=int(np.prod(shape))).reshape(shape)
+        # every element is overwritten by the device->host copy of the result
+        weakref.finalize(buf, self._give_back, n, p)
+        return arr
+
+    def _give_back(self, n, p):
+        self.free.setdefault(n, []).append(p)
+
+
+pinned = PinnedPool()

@@ -1368,6 +1368,19 @@ void sb_set_graphs(sb_ctx* c, int enabled) {
 
 long long sb_device_bytes(sb_ctx* c) { return c->bytes; }
 
+void* sb_host_alloc(long long bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) {
+    g_err = "cudaMallocHost failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void sb_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int sb_set_stream(sb_ctx* c, void* stream) {
   return guard([&]() -> int {
     sync(c);

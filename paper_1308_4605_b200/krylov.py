@@ -127,8 +127,8 @@ def gmres_solve(rhs, coeff, pcfg: PrecondConfig, gcfg: GmresConfig,
     """
     g = as_grid(rhs.u.grid)
     P = _device_precond(coeff, pcfg, smoother, precond)
-    xu = [np.zeros(g.face_shape(a)) for a in range(g.dim)]
-    xp = np.zeros(g.cells)
+    xu = [_lib.pinned.array(g.face_shape(a)) for a in range(g.dim)]
+    xp = _lib.pinned.array(g.cells)
     hist = solve_raw(P, gcfg, [_f64(c) for c in rhs.u.components], _f64(rhs.p.data), xu, xp)
     return StokesVector(FaceField(g, tuple(xu)), CellField(g, xp)), hist
 
