@@ -134,8 +134,26 @@ int sb_set_coefficients(sb_ctx* ctx, double theta, const double* const* rho_face
 int sb_apply_M(sb_ctx* ctx, const double* const* u, const double* p,
                double* const* out_u, double* out_p);
 
-/* operators.py:348-360 apply_A on a face field. */
+/* operators.py:348-360 apply_A on a face field.  Like the reference, the
+ * wall-normal boundary faces of u (and of sb_apply_M's u) are read as given:
+ * a boundary lift there enters the interior rows. */
 int sb_apply_A(sb_ctx* ctx, const double* const* u, double* const* out_u);
+
+/* operators.py:348-360 apply_A(u, coeff, bvals) with BoundaryValues
+ * (operators.py:224-264): tangential[(axis*2 + side)*3 + comp] is the C-order
+ * plane tangential_values(axis, side, comp) (comp's face array with `axis`
+ * dropped; reference axis/comp numbering), NULL = zero.  The normal values
+ * are the boundary faces of u (boundary_lift, operators.py:471). */
+int sb_apply_A_affine(sb_ctx* ctx, const double* const* u, const double* const* tangential,
+                      double* const* out_u);
+
+/* operators.py:484-512 homogenize(bvals, coeff, rhs): out = (rhs.u - A(u_b; bvals),
+ * rhs.p + div u_b), u_b = boundary_lift.  normal[axis*2 + side] is the plane
+ * normal_values(axis, side) (cells with `axis` dropped), NULL = zero;
+ * tangential as sb_apply_A_affine.  SB_EINVAL "incompatible boundary data: ..."
+ * when the net boundary flux does not match the divergence source (:505). */
+int sb_homogenize(sb_ctx* ctx, const double* const* normal, const double* const* tangential,
+                  const double* const* rhs_u, const double* rhs_p, double* const* out_u, double* out_p);
 
 /* operators.py:206-215 apply_Lrho on a cell field. */
 int sb_apply_Lrho(sb_ctx* ctx, const double* p, double* out_p);

@@ -227,8 +227,9 @@ def lrho(geo, coef, p):
     return div(geo, [g[a] / coef.rho_face[a] for a in range(geo.dim)])
 
 
-def _wall_tangent_grad(geo, ua, b):
-    """d u_a / d x_b at (a,b)-staggered points, homogeneous walls (operators.py:267-291)."""
+def _wall_tangent_grad(geo, ua, b, lo=0.0, hi=0.0):
+    """d u_a / d x_b at (a,b)-staggered points (operators.py:267-291); lo/hi are
+    the prescribed tangential wall velocities (BoundaryValues.tangential_values)."""
     if geo.per(b):
         return (ua - np.roll(ua, 1, axis=b)) / geo.h
     shp = list(ua.shape)
@@ -236,13 +237,14 @@ def _wall_tangent_grad(geo, ua, b):
     t = np.zeros(shp)
     nd = ua.ndim
     t[_ax(nd, b, slice(1, -1))] = np.diff(ua, axis=b) / geo.h
-    t[_ax(nd, b, 0)] = 2.0 * (ua[_ax(nd, b, 0)] - 0.0) / geo.h
-    t[_ax(nd, b, -1)] = 2.0 * (0.0 - ua[_ax(nd, b, -1)]) / geo.h
+    t[_ax(nd, b, 0)] = 2.0 * (ua[_ax(nd, b, 0)] - lo) / geo.h
+    t[_ax(nd, b, -1)] = 2.0 * (hi - ua[_ax(nd, b, -1)]) / geo.h
     return t
 
 
-def visc_row(geo, coef, u, a):
-    """Row a of L_mu u (operators.py:303-345; the smoother's copy multigrid.py:343-383)."""
+def visc_row(geo, coef, u, a, tang=None):
+    """Row a of L_mu u (operators.py:303-345; the smoother's copy multigrid.py:343-383).
+    tang: {(axis, side, comp): plane} tangential wall velocities (operators.py:224-264)."""
     h = geo.h
     mu = coef.mu_cell
     ncoef = mu if coef.form == LAPLACIAN else 2.0 * mu
@@ -254,7 +256,11 @@ def visc_row(geo, coef, u, a):
     for b in range(geo.dim):
         if b == a:
             continue
-        ft = _wall_tangent_grad(geo, ua, b)
+        lo = hi = 0.0
+        if tang is not None and not geo.per(b):
+            lo = tang.get((b, 0, a), 0.0)
+            hi = tang.get((b, 1, a), 0.0)
+        ft = _wall_tangent_grad(geo, ua, b, lo, hi)
         if coef.form != LAPLACIAN:
             ft = ft + here_minus_down(u[b], a, geo.per(a)) / h
         ft = coef.edge(a, b) * ft
@@ -267,16 +273,17 @@ def visc_row(geo, coef, u, a):
     return row
 
 
-def a_row(geo, coef, u, a):
+def a_row(geo, coef, u, a, tang=None):
     """Row a of A = theta rho - L_mu, wall rows zeroed (operators.py:348-360)."""
-    out = coef.theta * coef.rho_face[a] * u[a] - visc_row(geo, coef, u, a)
+    out = coef.theta * coef.rho_face[a] * u[a] - visc_row(geo, coef, u, a, tang)
     if not geo.per(a):
         zero_ends(out, a)
     return out
 
 
-def apply_A(geo, coef, u):
-    return [a_row(geo, coef, u, a) for a in range(geo.dim)]
+def apply_A(geo, coef, u, tang=None):
+    """operators.py:348-360; tang given = apply_A(u, coeff, bvals)."""
+    return [a_row(geo, coef, u, a, tang) for a in range(geo.dim)]
 
 
 def apply_M(geo, coef, u, p):
@@ -284,6 +291,34 @@ def apply_M(geo, coef, u, p):
     au = apply_A(geo, coef, u)
     gp = grad(geo, p)
     return [au[a] + gp[a] for a in range(geo.dim)], -div(geo, u)
+
+
+def boundary_lift(geo, normal):
+    """operators.py:471-481: face field holding the prescribed normal wall
+    velocities {(axis, side): plane} on the boundary faces, zero elsewhere."""
+    u = [np.zeros(geo.fshape(a)) for a in range(geo.dim)]
+    for a in range(geo.dim):
+        if geo.per(a):
+            continue
+        u[a][_ax(geo.dim, a, 0)] = normal.get((a, 0), 0.0)
+        u[a][_ax(geo.dim, a, -1)] = normal.get((a, 1), 0.0)
+    return u
+
+
+def homogenize(geo, coef, normal, tang, ru, rp):
+    """operators.py:484-512: subtract the affine wall contribution from the rhs.
+    Raises ValueError('incompatible boundary data ...') on a flux mismatch."""
+    ub = boundary_lift(geo, normal)
+    hd = geo.h ** geo.dim
+    dv = div(geo, ub)
+    flux = float(dv.sum()) * hd
+    src = -float(rp.sum()) * hd
+    scale = max(1.0, float(np.abs(dv).sum()) * hd, float(np.abs(rp).sum()) * hd)
+    if abs(flux - src) > 1e-10 * scale:
+        raise ValueError(f"incompatible boundary data: net boundary flux {flux:g} "
+                         f"!= divergence-source integral {src:g}")
+    cu = apply_A(geo, coef, ub, tang)
+    return [ru[a] - cu[a] for a in range(geo.dim)], rp - (-dv)
 
 
 # ---------------------------------------------------------------------------

@@ -23,7 +23,7 @@ STATUS = {0: "converged", 1: "breakdown", 2: "maxiter"}
 #: every symbol declared in include/stokesb200.h (checked by the CPU tests)
 EXPORTS = (
     "sb_create", "sb_destroy", "sb_last_error", "sb_set_coefficients", "sb_apply_M",
-    "sb_apply_A", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
+    "sb_apply_A", "sb_apply_A_affine", "sb_homogenize", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
     "sb_num_levels", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
@@ -71,6 +71,8 @@ _SIGS = {
     "sb_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
     "sb_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),
     "sb_apply_A": (C.c_int, [_P, _PP, _PP]),
+    "sb_apply_A_affine": (C.c_int, [_P, _PP, _PP, _PP]),
+    "sb_homogenize": (C.c_int, [_P, _PP, _PP, _PP, _P, _PP, _P]),
     "sb_apply_Lrho": (C.c_int, [_P, _P, _P]),
     "sb_mg_solve": (C.c_int, [_P, C.c_int, C.POINTER(Smoother), C.c_int, _PP, _PP]),
     "sb_precond_apply": (C.c_int, [_P, C.POINTER(Precond), C.POINTER(Smoother), _PP, _P, _PP, _P,

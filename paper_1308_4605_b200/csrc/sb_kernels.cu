@@ -723,6 +723,58 @@ __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned tota
   }
 }
 
+// Inhomogeneous tangential wall velocity (operators.py:267-291 with BoundaryValues):
+// the one-sided wall gradient 2(u - lo)/h (low wall) / 2(hi - u)/h (high wall)
+// differs from the homogeneous one by -/+ 2 v/h, times mu_e at the wall edge,
+// so row A of the face adjacent to wall (B, side) moves by -2 mu_e v / h^2.
+// Free-slip walls zero the flux (no contribution); wall-normal boundary rows
+// of A stay zero.  plane: C-order over the face extents of A with B dropped.
+__global__ void k_wall_tangent(LevelDev L, int A, int B, int side, const double* __restrict__ plane,
+                               double* out, Box b, int e1, int e2) {
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  if (L.bclo[A] != BC_PER && (ci[A] == 0 || ci[A] == L.n[A])) return;
+  int q[3] = {ci[0], ci[1], ci[2]};
+  q[B] = 0;
+  const double v = plane[((long long)q[0] * e1 + q[1]) * e2 + q[2]];
+  const int f = lin(L, ci);
+  const int st = B == 0 ? L.s0 : (B == 1 ? L.s1 : 1);
+  const double mue = L.mu_e[edge_of(A, B)][side ? f + st : f];
+  out[f] = out[f] - (mue * (2.0 * v * L.inv_h)) * L.inv_h;
+}
+
+// block partials of sum(x) and sum(|x|) (homogenize's flux compatibility check)
+__global__ void __launch_bounds__(kThreads)
+k_sum_abs_partial(const double* __restrict__ x, long long n, double* __restrict__ partials, int stride) {
+  __shared__ double acc[2][kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = 0.0, va = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double t = __ldg(x + e);
+    v += t;
+    va += fabs(t);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_down_sync(0xffffffffu, v, o);
+    va += __shfl_down_sync(0xffffffffu, va, o);
+  }
+  if (lane == 0) {
+    acc[0][warp] = v;
+    acc[1][warp] = va;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0, sa = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) {
+      s += acc[0][k];
+      sa += acc[1][k];
+    }
+    partials[blockIdx.x] = s;
+    partials[stride + blockIdx.x] = sa;
+  }
+}
+
 __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double inv_count, Box b,
                                unsigned total) {
   const double m = sum[0] * inv_count;
@@ -1675,6 +1727,28 @@ void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, 
   ++g_kernel_launches;
   const unsigned total = box_count(b);
   k_box_sub_mean<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, sum, inv_count, b, total);
+}
+
+void launch_wall_tangent(cudaStream_t s, const LevelDev& L, int A, int B, int side, const double* plane,
+                         double* out) {
+  ++g_kernel_launches;
+  Box b;
+  int ext[3];
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = 0;
+    b.hi[a] = L.n[a] - 1 + ((a == A && L.bclo[A] != BC_PER) ? 1 : 0);
+    ext[a] = b.hi[a] + 1;
+  }
+  b.lo[B] = b.hi[B] = side ? L.n[B] - 1 : 0;
+  ext[B] = 1;
+  const unsigned total = box_count(b);
+  (void)total;
+  k_wall_tangent<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, B, side, plane, out, b, ext[1], ext[2]);
+}
+
+void launch_sum_abs_partial(cudaStream_t s, const double* x, long long n, double* partials) {
+  ++g_kernel_launches;
+  k_sum_abs_partial<<<kRedBlocks, kThreads, 0, s>>>(x, n, partials, kRedBlocks);
 }
 
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x) {

@@ -69,6 +69,10 @@ void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, 
                            double inv_count);  // x -= sum*inv_count
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x);  // y += x
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x);  // *y += *x (one thread)
+// inhomogeneous walls (operators.py:267-291, 484-512)
+void launch_wall_tangent(cudaStream_t s, const LevelDev& L, int A, int B, int side, const double* plane,
+                         double* out);  // out_A -= 2 mu_e v / h^2 on the rows next to wall (B, side)
+void launch_sum_abs_partial(cudaStream_t s, const double* x, long long n, double* partials);  // sum, sum|x|
 
 // flat-vector kernels (GMRES; whole padded box, pads are zero)
 int reduce_blocks();

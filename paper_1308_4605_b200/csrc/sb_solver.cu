@@ -8,7 +8,9 @@
 // fused multi-vector kernels (CGS2) with one host sync per iteration for the
 // Hessenberg column.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -89,6 +91,7 @@ struct sb_ctx {
   int basis_cap = 0;
   double *sc0 = nullptr, *sc1 = nullptr, *scR = nullptr, *scC = nullptr;
   double *sf0[3]{}, *sf1[3]{}, *sfR[3]{}, *sfC[3]{};
+  double* splane = nullptr;   // staging for one wall plane of BoundaryValues
   bool scratch = false, scratch_mg = false;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -235,6 +238,45 @@ void zero_wall_faces(sb_ctx* c, const Level& L, int A, double* x) {
   launch_box_fill(c->st, L.d, b, x, 0.0);
   b.lo[A] = b.hi[A] = L.d.n[A];
   launch_box_fill(c->st, L.d, b, x, 0.0);
+}
+
+// one plane (index j along axis B) of an array kind, from a C-order plane
+// holding the kind's extents with axis B dropped (BoundaryValues layouts)
+void copy_plane_in(sb_ctx* c, const Level& L, int kind, int B, int j, const double* src, double* dst) {
+  int ext[3];
+  extents(c, L, kind, ext);
+  ext[B] = 1;
+  const long long st = B == 0 ? (long long)L.d.s0 : (B == 1 ? (long long)L.d.s1 : 1LL);
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)ext[2] * 8, (size_t)ext[2], (size_t)ext[1]);
+  p.dstPtr = make_cudaPitchedPtr((void*)(dst + j * st), (size_t)L.P[2] * 8, (size_t)L.P[2], (size_t)L.P[1]);
+  p.extent = make_cudaExtent((size_t)ext[2] * 8, (size_t)ext[1], (size_t)ext[0]);
+  p.kind = cudaMemcpyDefault;
+  CK(cudaMemcpy3DAsync(&p, c->st));
+}
+
+// tangential wall velocities of BoundaryValues (operators.py:267-291):
+// tangential[(axis*2 + side)*3 + comp] in reference axes, NULL = zero
+void wall_tangent(sb_ctx* c, const double* const* tangential, double* const* out) {
+  const Level& L = c->lv[0];
+  if (!c->splane) c->splane = dalloc(c, L.block);
+  for (int rb = 0; rb < c->dim; ++rb) {
+    const int B = rb + c->off;
+    for (int side = 0; side < 2; ++side) {
+      if (c->bc[B][side] != BC_NOSLIP) continue;  // periodic: none; free slip: flux zeroed
+      for (int ra = 0; ra < c->dim; ++ra) {
+        const double* src = ra == rb ? nullptr : tangential[(rb * 2 + side) * 3 + ra];
+        if (!src) continue;
+        const int A = ra + c->off;
+        int ext[3];
+        extents(c, L, A, ext);
+        ext[B] = 1;
+        CK(cudaMemcpyAsync(c->splane, src, (size_t)ext[0] * ext[1] * ext[2] * 8, cudaMemcpyDefault, c->st));
+        launch_wall_tangent(c->st, L.d, A, B, side, c->splane, out[A]);
+      }
+    }
+  }
 }
 
 void sync(sb_ctx* c) {
@@ -669,12 +711,14 @@ void apply_M_vec(sb_ctx* c, const double* x, double* out) {
 }
 
 // upload a host/device vector in the reference layout into a level-0 vector
-void vec_in(sb_ctx* c, const double* const* u, const double* p, double* v) {
+// keep_walls: read the wall-normal boundary faces as given (operators.apply_M);
+// otherwise zero them (vectors of the packed unknown space, grid.py:373)
+void vec_in(sb_ctx* c, const double* const* u, const double* p, double* v, bool keep_walls = false) {
   const Level& L = c->lv[0];
   for (int r = 0; r < c->dim; ++r) {
     const int A = r + c->off;
     copy_in(c, L, A, u[r], vcomp(c, v, A));
-    zero_wall_faces(c, L, A, vcomp(c, v, A));
+    if (!keep_walls) zero_wall_faces(c, L, A, vcomp(c, v, A));
   }
   copy_in(c, L, -1, p, vpres(c, v));
 }
@@ -1092,7 +1136,10 @@ int sb_set_coefficients(sb_ctx* c, double theta, const double* const* rho_face, 
                         const double* const* mu_edge, const double* gamma_cell) {
   return guard([&]() -> int {
     if (!(theta >= 0)) throw ArgErr(SB_EINVAL, "theta must be >= 0");
-    drop_graph(c);
+    // the captured P^-1 graph holds buffer pointers and theta (kernel
+    // parameters, null-space components); new coefficient VALUES in the same
+    // buffers replay correctly, so only a theta change invalidates it
+    if (!c->have_coef || theta != c->theta) drop_graph(c);
     c->theta = theta;
     for (auto& L : c->lv) L.d.theta = theta;
     Level& L0 = c->lv[0];
@@ -1118,7 +1165,7 @@ int sb_apply_M(sb_ctx* c, const double* const* u, const double* p, double* const
   return guard([&]() -> int {
     check_ready(c);
     ensure_vectors(c);
-    vec_in(c, u, p, c->vt);
+    vec_in(c, u, p, c->vt, true);
     apply_M_vec(c, c->vt, c->vMv);
     vec_out(c, c->vMv, out_u, out_p);
     sync(c);
@@ -1126,20 +1173,79 @@ int sb_apply_M(sb_ctx* c, const double* const* u, const double* p, double* const
   });
 }
 
-int sb_apply_A(sb_ctx* c, const double* const* u, double* const* out_u) {
+int sb_apply_A_affine(sb_ctx* c, const double* const* u, const double* const* tangential,
+                      double* const* out_u) {
   return guard([&]() -> int {
     check_ready(c);
     ensure_scratch(c);
     const Level& L = c->lv[0];
-    for (int r = 0; r < c->dim; ++r) {
-      const int A = r + c->off;
-      copy_in(c, L, A, u[r], c->sf0[A]);
-      zero_wall_faces(c, L, A, c->sf0[A]);
-    }
+    // wall-normal boundary faces are read as given (the boundary lift), as
+    // the reference's apply_A does
+    for (int r = 0; r < c->dim; ++r) copy_in(c, L, r + c->off, u[r], c->sf0[r + c->off]);
     CPtr3 x{{c->sf0[0], c->sf0[1], c->sf0[2]}}, none{{nullptr, nullptr, nullptr}};
     Ptr3 o{{c->sf1[0], c->sf1[1], c->sf1[2]}};
     launch_face_residual(c->st, L.d, c->dim, c->form, x, none, nullptr, o);
+    if (tangential) wall_tangent(c, tangential, c->sf1);
     for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, c->sf1[r + c->off], out_u[r]);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_apply_A(sb_ctx* c, const double* const* u, double* const* out_u) {
+  return sb_apply_A_affine(c, u, nullptr, out_u);
+}
+
+// operators.py:484-512 homogenize
+int sb_homogenize(sb_ctx* c, const double* const* normal, const double* const* tangential,
+                  const double* const* rhs_u, const double* rhs_p, double* const* out_u, double* out_p) {
+  return guard([&]() -> int {
+    check_ready(c);
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    // u_b = boundary_lift(bvals) (operators.py:471-481)
+    for (int r = 0; r < c->dim; ++r) {
+      const int A = r + c->off;
+      CK(cudaMemsetAsync(c->sf0[A], 0, L.block * 8, c->st));
+      if (c->bc[A][0] == BC_PER || !normal) continue;
+      for (int side = 0; side < 2; ++side)
+        if (normal[2 * r + side]) copy_plane_in(c, L, A, A, side ? L.d.n[A] : 0, normal[2 * r + side], c->sf0[A]);
+    }
+    CK(cudaMemsetAsync(c->sc0, 0, L.block * 8, c->st));
+    {
+      CPtr3 ub{{c->sf0[0], c->sf0[1], c->sf0[2]}};
+      Ptr3 o{{c->sf1[0], c->sf1[1], c->sf1[2]}};
+      launch_apply_M(c->st, L.d, c->dim, c->form, ub, c->sc0, o, c->sc1);  // A u_b, -div(u_b)
+    }
+    if (tangential) wall_tangent(c, tangential, c->sf1);
+    // compatibility of the boundary flux with the divergence source (:495-509)
+    copy_in(c, L, -1, rhs_p, c->sc0);
+    const int rb = reduce_blocks();
+    launch_sum_abs_partial(c->st, c->sc1, L.block, c->dpart);
+    launch_sum_abs_partial(c->st, c->sc0, L.block, c->dpart + 2 * rb);
+    launch_finalize(c->st, c->dpart, 4, dmisc(c));
+    CK(cudaMemcpyAsync(hmisc(c), dmisc(c), 4 * 8, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const double* hs = hmisc(c);
+    const double hd = std::pow(c->h, (double)c->dim);
+    const double flux = -hs[0] * hd;         // sum(div u_b) h^d
+    const double source = -hs[2] * hd;
+    const double scale = std::max(1.0, std::max(hs[1] * hd, hs[3] * hd));
+    if (std::fabs(flux - source) > 1e-10 * scale) {
+      char msg[160];
+      std::snprintf(msg, sizeof msg, "incompatible boundary data: net boundary flux %g != divergence-source integral %g",
+                    flux, source);
+      throw ArgErr(SB_EINVAL, msg);
+    }
+    // (rhs.u - A u_b, rhs.p - (-div u_b)) over the full arrays
+    for (int r = 0; r < c->dim; ++r) {
+      const int A = r + c->off;
+      copy_in(c, L, A, rhs_u[r], c->sf0[A]);
+      launch_sub(c->st, c->sf0[A], c->sf1[A], c->sf0[A], L.block);
+      copy_out(c, L, A, c->sf0[A], out_u[r]);
+    }
+    launch_sub(c->st, c->sc0, c->sc1, c->sc0, L.block);
+    copy_out(c, L, -1, c->sc0, out_p);
     sync(c);
     return SB_OK;
   });

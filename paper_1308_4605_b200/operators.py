@@ -9,7 +9,9 @@ Mirrors the hot-path surface of the reference's ``stokesmg.operators``
   (:81-125), ``RescaleSpec`` / ``rescale`` (:515-550) and
   ``velocity_null_components`` (:368-388);
 * the operators themselves run on the B200 through the C ABI:
-  ``apply_M`` (:363), ``apply_A`` (:348), ``apply_Lrho`` (:206).
+  ``apply_M`` (:363), ``apply_A`` (:348, with ``BoundaryValues`` :224),
+  ``apply_Lrho`` (:206) and ``homogenize`` (:484);
+* ``BoundaryValues`` / ``boundary_lift`` (:224-264, :471): host containers.
 
 Inputs/outputs are the reference's field types (this package's mirror or the
 reference's own objects, duck-typed).
@@ -263,15 +265,113 @@ def apply_M(x, coeff, ctx: DeviceContext | None = None) -> StokesVector:
     return StokesVector(FaceField(g, tuple(ou)), CellField(g, op))
 
 
+def _tangential_ptrs(bvals, g):
+    """BoundaryValues.tangential -> the 18 plane pointers of sb_apply_A_affine
+    (index (axis*2 + side)*3 + comp); shapes checked as the reference does."""
+    keep, ptrs = [], [None] * 18
+    for (axis, side, comp) in sorted(bvals.tangential):
+        v = _f64(bvals.tangential_values(axis, side, comp))
+        keep.append(v)
+        ptrs[(axis * 2 + side) * 3 + comp] = v
+    return keep, _lib.parr(ptrs)
+
+
 def apply_A(u, coeff, bvals=None, ctx: DeviceContext | None = None) -> FaceField:
-    """Velocity operator theta rho u - L_mu u on the device (operators.py:348-360)."""
-    if bvals is not None:
-        raise NotImplementedError("inhomogeneous walls (homogenize) are outside the device path")
+    """Velocity operator theta rho u - L_mu u on the device (operators.py:348-360).
+
+    Wall-normal boundary faces of ``u`` are read as given (a boundary lift);
+    ``bvals`` adds the prescribed tangential wall velocities (operators.py:267-291)."""
     g = as_grid(u.grid)
     ctx = ctx or _ctx_for(coeff, g)
     ou = _out_face(g)
-    _lib.check(ctx.lib.sb_apply_A(ctx.h, _lib.parr([_f64(c) for c in u.components]), _lib.parr(ou)))
+    uu = _lib.parr([_f64(c) for c in u.components])
+    if bvals is None:
+        _lib.check(ctx.lib.sb_apply_A(ctx.h, uu, _lib.parr(ou)))
+    else:
+        keep, tp = _tangential_ptrs(bvals, g)
+        _lib.check(ctx.lib.sb_apply_A_affine(ctx.h, uu, tp, _lib.parr(ou)))
     return FaceField(g, tuple(ou))
+
+
+# ---------------------------------------------------------------------------
+# inhomogeneous walls (operators.py:224-264, 471-512)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class BoundaryValues:
+    """Prescribed wall velocities (operators.py:224-264).
+
+    ``normal[(axis, side)]``: the normal component on that wall's boundary
+    faces (the component array with its own axis dropped).
+    ``tangential[(axis, side, comp)]``: the ``comp`` velocity on the wall plane
+    of ``(axis, side)`` (the ``comp`` array with ``axis`` dropped).  Missing
+    entries are zero; ``side`` is 0 (low) or 1 (high)."""
+
+    grid: GridSpec
+    normal: dict
+    tangential: dict
+
+    @classmethod
+    def zeros(cls, grid) -> "BoundaryValues":
+        return cls(grid, {}, {})
+
+    def normal_values(self, axis: int, side: int) -> np.ndarray:
+        shape = tuple(n for a, n in enumerate(self.grid.cells) if a != axis)
+        vals = self.normal.get((axis, side))
+        if vals is None:
+            return np.zeros(shape)
+        vals = np.asarray(vals, dtype=np.float64)
+        if vals.shape != shape:
+            raise ValueError(f"normal values for axis {axis} must have shape {shape}")
+        return vals
+
+    def tangential_values(self, axis: int, side: int, comp: int) -> np.ndarray:
+        shape = tuple(n for a, n in enumerate(self.grid.face_shape(comp)) if a != axis)
+        vals = self.tangential.get((axis, side, comp))
+        if vals is None:
+            return np.zeros(shape)
+        vals = np.asarray(vals, dtype=np.float64)
+        if vals.shape != shape:
+            raise ValueError(f"tangential values for (axis {axis}, comp {comp}) must have shape {shape}")
+        return vals
+
+
+def boundary_lift(bvals) -> FaceField:
+    """FaceField holding the prescribed normal values on the boundary faces
+    (operators.py:471-481; array assembly, no arithmetic)."""
+    g = as_grid(bvals.grid)
+    u = FaceField.zeros(g)
+    for a in range(g.dim):
+        if g.periodic(a):
+            continue
+        arr = u.components[a]
+        lo = [slice(None)] * g.dim
+        hi = [slice(None)] * g.dim
+        lo[a], hi[a] = 0, -1
+        arr[tuple(lo)] = bvals.normal_values(a, 0)
+        arr[tuple(hi)] = bvals.normal_values(a, 1)
+    return u
+
+
+def homogenize(bvals, coeff, rhs, ctx: DeviceContext | None = None) -> StokesVector:
+    """Subtract the affine boundary contribution from the right-hand side on the
+    device (operators.py:484-512): (rhs.u - A(u_b; bvals), rhs.p + div u_b).
+    Raises ValueError ('incompatible boundary data ...') when the net boundary
+    flux does not match the divergence source carried in ``rhs.p``."""
+    g = as_grid(rhs.u.grid)
+    ctx = ctx or _ctx_for(coeff, g)
+    keep_n, nptr = [], [None] * 6
+    for (axis, side) in sorted(bvals.normal):
+        v = _f64(bvals.normal_values(axis, side))
+        keep_n.append(v)
+        nptr[axis * 2 + side] = v
+    keep_t, tp = _tangential_ptrs(bvals, g)
+    ou, op = _out_face(g), np.zeros(g.cells)
+    _lib.check(ctx.lib.sb_homogenize(ctx.h, _lib.parr(nptr), tp,
+                                     _lib.parr([_f64(c) for c in rhs.u.components]),
+                                     _lib.ptr(_f64(rhs.p.data)), _lib.parr(ou), _lib.ptr(op)))
+    return StokesVector(FaceField(g, tuple(ou)), CellField(g, op))
 
 
 def apply_Lrho(p, coeff, ctx: DeviceContext | None = None) -> CellField:

@@ -108,3 +108,11 @@ def gpu_available():
 def lib():
     from paper_1308_4605_b200 import _lib
     return _lib.load()
+
+
+def golden_bvals(e):
+    """(normal {(axis, side): plane}, tangential {(axis, side, comp): plane}) of an affine case."""
+    n = e["name"]
+    normal = {(int(k[0]), int(k[1])): arr(n, f"bn{k}") for k in e["normal"]}
+    tang = {(int(k[0]), int(k[1]), int(k[2])): arr(n, f"bt{k}") for k in e["tangential"]}
+    return normal, tang

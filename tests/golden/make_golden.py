@@ -194,6 +194,58 @@ def gen_vcycles():
             meta(name, "vcycle", g, bc, theta, form, levels=len(hier), vcycles=counts)
 
 
+def gen_affine():
+    """Inhomogeneous walls: apply_A(u, coeff, bvals), boundary_lift, homogenize
+    (operators.py:224-264, 348-360, 471-512) on every wall-bounded operator grid."""
+    rng = np.random.default_rng(4605)
+    for gi, (cells, bc, h) in enumerate(OPER_GRIDS):
+        g = grid(cells, bc, h)
+        if all(g.periodic(a) for a in range(g.dim)):
+            continue
+        for form in ("laplacian", "stress", "stress_bulk"):
+            name = f"af{gi}_{form}"
+            c = rand_coeff(g, rng, 0.7, form)
+            normal, tang = {}, {}
+            for a in range(g.dim):
+                if g.periodic(a):
+                    continue
+                for side in (0, 1):
+                    normal[(a, side)] = rng.standard_normal(
+                        tuple(n for ax, n in enumerate(g.cells) if ax != a))
+                    put(name, f"bn{a}{side}", normal[(a, side)])
+                    for comp in range(g.dim):
+                        if comp == a:
+                            continue
+                        tang[(a, side, comp)] = rng.standard_normal(
+                            tuple(n for ax, n in enumerate(g.face_shape(comp)) if ax != a))
+                        put(name, f"bt{a}{side}{comp}", tang[(a, side, comp)])
+            bv = OP.BoundaryValues(g, normal, tang)
+            u = OP.boundary_lift(bv)
+            put_face(name, "lift", OP.boundary_lift(bv))
+            for a in range(g.dim):
+                u.interior(a)[...] = rng.standard_normal(u.interior(a).shape)
+            put_coeff(name, c)
+            put_face(name, "u", u)
+            put_face(name, "Au", OP.apply_A(u, c, bv))
+            put_face(name, "A0", OP.apply_A(u, c))
+            m = OP.apply_M(G.StokesVector(u, G.CellField(g, np.zeros(g.cells))), c)
+            put_face(name, "Mu", m.u)
+            put(name, "Mp", m.p.data)
+            rhs = G.StokesVector(rand_face(g, rng), rand_cell(g, rng))
+            for a in range(g.dim):  # boundary faces of the rhs carry data too
+                rhs.u.components[a][...] = rng.standard_normal(rhs.u.components[a].shape)
+            rhs.p.data -= rhs.p.data.mean()
+            net = float(OP.div(OP.boundary_lift(bv)).data.sum())
+            rhs.p.data -= net / rhs.p.data.size  # compatible divergence source
+            put_face(name, "ru", rhs.u)
+            put(name, "rp", rhs.p.data)
+            hom = OP.homogenize(bv, c, rhs)
+            put_face(name, "hu", hom.u)
+            put(name, "hp", hom.p.data)
+            meta(name, "affine", g, bc, 0.7, form, normal=sorted(f"{a}{s}" for a, s in normal),
+                 tangential=sorted(f"{a}{s}{k}" for a, s, k in tang))
+
+
 def gen_gmres():
     """Full solves of the BASELINE recipes at reduced size (reference API only)."""
     sys.path.insert(0, str(OUT.parent.parent))
@@ -235,6 +287,7 @@ def main():
     gen_operators()
     gen_vcycles()
     gen_gmres()
+    gen_affine()
     np.savez_compressed(OUT / "golden.npz", **store)
     (OUT / "golden.json").write_text(json.dumps(index, indent=1))
     print(len(index), "cases,", len(store), "arrays ->", OUT / "golden.npz")

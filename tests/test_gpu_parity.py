@@ -158,6 +158,39 @@ def test_gmres_vs_golden(e):
     assert np.allclose(rows[:k, 3], h[:k, 3], rtol=1e-5, atol=1e-12 * h[0, 3])  # r_true
 
 
+def test_graph_reused_across_coefficient_sets():
+    """A pooled context keeps its captured P^-1 graph when new coefficients with
+    the same theta arrive (sb_set_coefficients); the replay must see the new
+    values: solve a perturbed set first, then the golden set on the same context."""
+    from paper_1308_4605_b200.grid import CellField, FaceField, StokesVector, pack_stokes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.operators import DeviceContext
+    from paper_1308_4605_b200.precond import PrecondConfig, PrecondKind, Preconditioner
+    e = [x for x in cases("gmres") if x["name"] == "gm_C5_16_P1"][0]
+    g = pkg_grid(e)
+    c = pkg_coeff(e, grid=g)
+    n = e["name"]
+    rhs = StokesVector(FaceField(g, tuple(face(n, "bu", g.dim))), CellField(g, arr(n, "bp")))
+    pert = pkg_coeff(e, grid=g)
+    pert.mu_cell.data[...] *= 1.7
+    for k in pert.mu_node_edge.arrays:
+        pert.mu_node_edge.arrays[k] = pert.mu_node_edge.arrays[k] * 1.7
+    gcfg = GmresConfig(restart=e["restart"], track_true_residual=False)
+    pc = PrecondConfig(kind=PrecondKind(e["precond"]))
+    P1 = Preconditioner(pert, pc)
+    h0 = P1.ctx.h
+    x0, _ = gmres_solve(rhs, pert, pc, gcfg, precond=P1)
+    del P1  # back to the pool
+    P2 = Preconditioner(c, pc)
+    assert P2.ctx.h == h0  # same context, same captured graph
+    x, hist = gmres_solve(rhs, c, pc, gcfg, precond=P2)
+    assert abs(hist.iterations - e["iterations"]) <= 1
+    ref = StokesVector(FaceField(g, tuple(face(n, "xu", g.dim))), CellField(g, arr(n, "xp")))
+    xr, xg = pack_stokes(ref), pack_stokes(x)
+    assert np.linalg.norm(xg - xr) <= 1e-8 * np.linalg.norm(xr)
+    assert np.linalg.norm(pack_stokes(x0) - xr) > 1e-3 * np.linalg.norm(xr)
+
+
 @pytest.mark.parametrize("name,n,kind", [("C2", 256, "P1"), ("C2", 256, "P2"), ("C3", 32, "P1"),
                                          ("C4", 32, "P1"), ("C5", 32, "P2")])
 def test_gmres_vs_oracle_baseline_recipes(name, n, kind):

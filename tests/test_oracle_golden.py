@@ -149,3 +149,39 @@ def test_paper_transfer_examples():
     c2[0][2, 2] = 4.0
     c2[0][3, 2] = 8.0
     assert O.prolong_face(gc, c2)[0][5, 4] == pytest.approx(4.5)
+
+
+@pytest.mark.parametrize("e", cases("affine"), ids=lambda e: e["name"])
+def test_inhomogeneous_walls(e):
+    """apply_A with BoundaryValues, boundary_lift and homogenize (operators.py:224-264,
+    348-360, 471-512) against the reference on every wall-bounded grid and form."""
+    from conftest import golden_bvals
+    geo, c = oracle_geo(e), oracle_coef(e)
+    d, n = geo.dim, e["name"]
+    normal, tang = golden_bvals(e)
+    lift = O.boundary_lift(geo, normal)
+    for a in range(d):
+        assert np.array_equal(lift[a], arr(n, f"lift{a}"))
+    u = face(n, "u", d)
+    au, a0 = O.apply_A(geo, c, u, tang), O.apply_A(geo, c, u)
+    mu, mp = O.apply_M(geo, c, u, np.zeros(geo.cells))
+    for a in range(d):
+        assert relerr(au[a], arr(n, f"Au{a}")) <= TOL
+        assert relerr(a0[a], arr(n, f"A0{a}")) <= TOL
+        assert relerr(mu[a], arr(n, f"Mu{a}")) <= TOL
+    assert relerr(mp, arr(n, "Mp")) <= TOL
+    hu, hp = O.homogenize(geo, c, normal, tang, face(n, "ru", d), arr(n, "rp"))
+    for a in range(d):
+        assert relerr(hu[a], arr(n, f"hu{a}")) <= TOL
+    assert relerr(hp, arr(n, "hp")) <= TOL
+
+
+def test_homogenize_incompatible_rejected():
+    """operators.py:505-509 (reference test_operators.py:486-492): net inflow with a zero
+    divergence source is rejected."""
+    geo = O.Geo((8, 8), 1 / 8, (("no_slip",) * 2,) * 2)
+    rng = np.random.default_rng(2)
+    c = O.make_coef(geo, 0.0, 0.5 + rng.random((8, 8)), 0.5 + rng.random((8, 8)))
+    z = [np.zeros(geo.fshape(a)) for a in range(2)]
+    with pytest.raises(ValueError, match="incompatible"):
+        O.homogenize(geo, c, {(0, 0): np.full(8, 1.0)}, {}, z, np.zeros((8, 8)))
