@@ -202,9 +202,17 @@ void extents(const sb_ctx* c, const Level& L, int kind, int* ext) {
   }
 }
 
+// a reference array whose rows fill the box exactly (no pads along axes 1, 2)
+// moves as one linear copy; otherwise a pitched 3D copy
+bool dense_rows(const Level& L, const int* ext) { return ext[2] == L.P[2] && ext[1] == L.P[1]; }
+
 void copy_in(sb_ctx* c, const Level& L, int kind, const double* src, double* dst) {
   int ext[3];
   extents(c, L, kind, ext);
+  if (dense_rows(L, ext)) {
+    CK(cudaMemcpyAsync(dst, src, (size_t)ext[0] * ext[1] * ext[2] * 8, cudaMemcpyDefault, c->st));
+    return;
+  }
   cudaMemcpy3DParms p;
   std::memset(&p, 0, sizeof(p));
   p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)ext[2] * 8, (size_t)ext[2], (size_t)ext[1]);
@@ -217,6 +225,10 @@ void copy_in(sb_ctx* c, const Level& L, int kind, const double* src, double* dst
 void copy_out(sb_ctx* c, const Level& L, int kind, const double* src, double* dst) {
   int ext[3];
   extents(c, L, kind, ext);
+  if (dense_rows(L, ext)) {
+    CK(cudaMemcpyAsync(dst, src, (size_t)ext[0] * ext[1] * ext[2] * 8, cudaMemcpyDefault, c->st));
+    return;
+  }
   cudaMemcpy3DParms p;
   std::memset(&p, 0, sizeof(p));
   p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)L.P[2] * 8, (size_t)L.P[2], (size_t)L.P[1]);

@@ -34,14 +34,27 @@ hc.gamma_cell = CellField(g, pinned(cs.gamma_cell.data))
 hr = StokesVector(FaceField(g, tuple(pinned(c) for c in rs.u.components)), CellField(g, pinned(rs.p.data)))
 gcfg = GmresConfig(restart=50, max_iters=500, rtol=1e-9, track_true_residual=False)
 pc = PrecondConfig(kind=P1)
+from paper_1308_4605_b200 import _lib  # noqa: E402
+a = pinned(np.ones(g.cells))
+d = torch.empty(g.cells, dtype=torch.float64, device="cuda")
+for _ in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.copy_(torch.from_numpy(a), non_blocking=True)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    torch.from_numpy(a).copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+print(f"PCIe: H2D {a.nbytes / (t1 - t0) / 1e9:.1f} GB/s, D2H {a.nbytes / (t2 - t1) / 1e9:.1f} GB/s (pinned, 134 MB)")
 for rep in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     P = Preconditioner(hc, pc)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    xu = [np.zeros(g.face_shape(a)) for a in range(3)]
-    xp = np.zeros(g.cells)
+    xu = [_lib.pinned.array(g.face_shape(a)) for a in range(3)]
+    xp = _lib.pinned.array(g.cells)
     t2 = time.perf_counter()
     h = solve_raw(P, gcfg, [c for c in hr.u.components], hr.p.data, xu, xp)
     torch.cuda.synchronize()
