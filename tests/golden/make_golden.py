@@ -283,11 +283,48 @@ def gen_gmres():
              restart=case.restart, status=hist.status, iterations=hist.iterations, c=spec.c)
 
 
+DRIVER_CONFIGS = [
+    {"problem": {"kind": "bubble", "dim": 2, "cells": 32, "bc": "no_slip", "seed": 3},
+     "solver": {"gmres": {"restart": 10, "rtol": 1e-9}},
+     "sweep": {"solver.precond.kind": ["P1", "P2", "P3"], "problem.beta": ["inf", 0.5, 0]}},
+    {"problem": {"kind": "constant", "dim": 3, "cells": 8, "bc": "periodic", "mu0": 2.0,
+                 "beta": "inf", "seed": 5},
+     "solver": {"precond": {"kind": "P1"}, "gmres": {"restart": 20, "rtol": 1e-10}},
+     "sweep": {"solver.precond.velocity_cycles": [1, 2]}},
+    {"problem": {"kind": "bubble", "dim": 2, "cells": [32, 16], "bc": ["periodic", "free_slip"],
+                 "viscous_form": "stress_bulk", "gamma0": 0.5, "beta": 1.0, "seed": 11,
+                 "bubble": {"r_mu": 10.0, "r_rho": 5.0}},
+     "solver": {"gmres": {"restart": 30, "max_iters": 100, "track_true_residual": False}},
+     "sweep": {"solver.precond.kind": ["P4", "P5"], "solver.precond.schur_sign": ["minus", "plus"]}},
+]
+
+
+def gen_driver():
+    """The reference's own batch driver (cli.py cmd_run) on small configs: the
+    manifest rows and history CSVs the device driver must reproduce."""
+    import tempfile
+    from stokesmg import cli
+    for k, cfg in enumerate(DRIVER_CONFIGS):
+        with tempfile.TemporaryDirectory() as out:
+            rc = cli.cmd_run(json.loads(json.dumps(cfg)), out, 1, None)
+            man = json.loads((pathlib.Path(out) / "manifest.json").read_text())
+            rows = []
+            for r in man["runs"]:
+                text = (pathlib.Path(out) / r["file"]).read_text().splitlines()
+                assert text[0] == cli.CSV_HEADER
+                put(f"drv{k}", f"run{r['index']}", np.array([[float(v) for v in ln.split(",")] for ln in text[1:]]))
+                rows.append({key: r[key] for key in ("index", "file", "sweep_point", "seed", "status",
+                                                     "iterations", "scalar_vcycles")})
+        index.append(dict(name=f"drv{k}", kind="driver", config=cfg, exit_code=rc, runs=rows,
+                          manifest_keys=sorted(man), row_keys=sorted(man["runs"][0])))
+
+
 def main():
     gen_operators()
     gen_vcycles()
     gen_gmres()
     gen_affine()
+    gen_driver()
     np.savez_compressed(OUT / "golden.npz", **store)
     (OUT / "golden.json").write_text(json.dumps(index, indent=1))
     print(len(index), "cases,", len(store), "arrays ->", OUT / "golden.npz")
