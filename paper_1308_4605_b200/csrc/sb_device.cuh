@@ -83,18 +83,24 @@ struct UA7 {
   double c, p[3], m[3];
 };
 
-template <int DIM, int A, bool PA = false>
+// CG: load through L2 only (ld.global.cg).  The wavefront sweep kernels
+// (sb_wave.cu) read iterate values that other SMs wrote earlier in the same
+// launch; L1 is not coherent across SMs, so those loads bypass it.
+template <bool CG>
+__device__ __forceinline__ double ldu(const double* p, int i) { return CG ? __ldcg(p + i) : p[i]; }
+
+template <int DIM, int A, bool PA = false, bool CG = false>
 __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, int f, const int* ci) {
   UA7 s;
-  s.c = ua[f];
+  s.c = ldu<CG>(ua, f);
 #pragma unroll
   for (int b = 3 - DIM; b < 3; ++b) {
     const int dp = b == 0 ? dplus<0, PA>(L, ci[0]) : (b == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
     const int dm = b == 0 ? dminus<0, PA>(L, ci[0]) : (b == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
     // on a wall axis B != A the +/- neighbours are only read away from the wall
     const bool wallB = b != A && !perq<PA>(L, b);
-    s.p[b] = (wallB && ci[b] == L.n[b] - 1) ? 0.0 : ua[f + dp];
-    s.m[b] = (wallB && ci[b] == 0) ? 0.0 : ua[f + dm];
+    s.p[b] = (wallB && ci[b] == L.n[b] - 1) ? 0.0 : ldu<CG>(ua, f + dp);
+    s.m[b] = (wallB && ci[b] == 0) ? 0.0 : ldu<CG>(ua, f + dm);
   }
   return s;
 }
@@ -104,7 +110,10 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // (f | f+e_B) (- e_A), rho_A and rhs at f, plus the u_A neighbourhood.
 // GAcc gathers from global memory with periodic wraps; the streaming sweep
 // kernels (sb_sweep.cu) provide a shared-memory accessor with the same API.
-template <int DIM, int A, bool PA = false>
+// NC: the u_B operands go through the read-only (non-coherent) path.  The
+// single-CTA coarse-level kernel updates u inside the launch and reads it
+// back after __syncthreads, so it instantiates NC = false (plain loads).
+template <int DIM, int A, bool PA = false, bool NC = true>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
@@ -126,7 +135,7 @@ struct GAcc {
   template <int B>
   __device__ __forceinline__ double ub(bool hi, bool lowA) const {
     const int e = hi ? f + eB<B>() : f;
-    return ld(u[B], lowA ? e + dmA : e);
+    return NC ? ld(u[B], lowA ? e + dmA : e) : u[B][lowA ? e + dmA : e];
   }
   __device__ __forceinline__ double rho() const { return ld(L.rho_f[A], f); }
   // (D u) h at the cells c_hi = f / c_lo = f - e_A (stress+bulk form only)
@@ -226,16 +235,16 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A, bool PA = false>
+template <int DIM, int FORM, int A, bool PA = false, bool NC = true>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
-  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA>(L, u, f, ci), ci, diag);
+  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC>(L, u, f, ci), ci, diag);
 }
 
-template <int DIM, int FORM, int A, bool PA = false>
+template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool CG = false>
 __device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, int f, const int* ci,
                                            double& diag) {
-  return face_row_core<DIM, FORM, A, PA>(L, gather_ua<DIM, A, PA>(L, u[A], f, ci), u, f, ci, diag);
+  return face_row_core<DIM, FORM, A, PA, NC>(L, gather_ua<DIM, A, PA, CG>(L, u[A], f, ci), u, f, ci, diag);
 }
 
 // beta = 1/rho_face accessor for the cell row: beta_a at the low face (c) or
@@ -293,25 +302,25 @@ __device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s,
   return cell_row_t<DIM, PA>(L, s, GBeta<PA>(L, c, ci), ci, diag);
 }
 
-template <int DIM, bool PA = false>
+template <int DIM, bool PA = false, bool CG = false>
 __device__ __forceinline__ UA7 gather_cell(const LevelDev& L, const double* phi, int c, const int* ci) {
   UA7 s;
-  s.c = phi[c];
+  s.c = ldu<CG>(phi, c);
 #pragma unroll
   for (int a = 3 - DIM; a < 3; ++a) {
     const int dp = a == 0 ? dplus<0, PA>(L, ci[0]) : (a == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
     const int dm = a == 0 ? dminus<0, PA>(L, ci[0]) : (a == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
     const bool wall = !perq<PA>(L, a);
-    s.p[a] = (wall && ci[a] == L.n[a] - 1) ? 0.0 : phi[c + dp];
-    s.m[a] = (wall && ci[a] == 0) ? 0.0 : phi[c + dm];
+    s.p[a] = (wall && ci[a] == L.n[a] - 1) ? 0.0 : ldu<CG>(phi, c + dp);
+    s.m[a] = (wall && ci[a] == 0) ? 0.0 : ldu<CG>(phi, c + dm);
   }
   return s;
 }
 
-template <int DIM, bool PA = false>
+template <int DIM, bool PA = false, bool CG = false>
 __device__ __forceinline__ double cell_row(const LevelDev& L, const double* phi, int c, const int* ci,
                                            double& diag) {
-  return cell_row_core<DIM, PA>(L, gather_cell<DIM, PA>(L, phi, c, ci), c, ci, diag);
+  return cell_row_core<DIM, PA>(L, gather_cell<DIM, PA, CG>(L, phi, c, ci), c, ci, diag);
 }
 
 }  // namespace sb

@@ -62,7 +62,7 @@ __device__ __forceinline__ int lin(const LevelDev& L, const int* ci) {
 }
 
 // unknown faces of component A (wall axis A: 1..n_A-1)
-inline Box face_box(const LevelDev& L, int dim, int A) {
+__host__ __device__ inline Box face_box(const LevelDev& L, int dim, int A) {
   Box b;
   for (int a = 0; a < 3; ++a) {
     b.lo[a] = 0;
@@ -75,7 +75,7 @@ inline Box face_box(const LevelDev& L, int dim, int A) {
   (void)dim;
   return b;
 }
-inline Box cell_box(const LevelDev& L) {
+__host__ __device__ inline Box cell_box(const LevelDev& L) {
   Box b;
   for (int a = 0; a < 3; ++a) {
     b.lo[a] = 0;
@@ -161,18 +161,18 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
 // residual -> restriction (multigrid.py:195-233, 177-182, 403-406)
 // ---------------------------------------------------------------------------
 
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, bool PA, bool NC = true>
 __device__ __forceinline__ double face_resid_at(const LevelDev& L, const double* const* u,
                                                 const double* rhs, const int* ci) {
   const int f = lin(L, ci);
   double dg;
-  const double au = face_row<DIM, FORM, A, PA>(L, u, f, ci, dg);
-  return __ldg(rhs + f) - au;
+  const double au = face_row<DIM, FORM, A, PA, NC>(L, u, f, ci, dg);
+  return (NC ? __ldg(rhs + f) : rhs[f]) - au;
 }
 
 // Tangential 2^(d-1) mean of fine residuals at fine normal index fa, coarse
 // tangential indices in C (mean along B1 first, then B2: multigrid.py:112-119).
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, bool PA, bool NC = true>
 __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* const* u, const double* rhs,
                                               const int* C, int fa) {
   using O = Others<DIM, A>;
@@ -187,16 +187,16 @@ __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* 
       q0[O::B2] += t2;
       q1[O::B2] += t2;
       q1[O::B1] += 1;
-      const double m0 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q0);
-      const double m1 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q1);
+      const double m0 = face_resid_at<DIM, FORM, A, PA, NC>(Lf, u, rhs, q0);
+      const double m1 = face_resid_at<DIM, FORM, A, PA, NC>(Lf, u, rhs, q1);
       p[t2] = 0.5 * (m0 + m1);
     }
     return 0.5 * (p[0] + p[1]);
   }
   int q1[3] = {fi[0], fi[1], fi[2]};
   q1[O::B1] += 1;
-  const double m0 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, fi);
-  const double m1 = face_resid_at<DIM, FORM, A, PA>(Lf, u, rhs, q1);
+  const double m0 = face_resid_at<DIM, FORM, A, PA, NC>(Lf, u, rhs, fi);
+  const double m1 = face_resid_at<DIM, FORM, A, PA, NC>(Lf, u, rhs, q1);
   return 0.5 * (m0 + m1);
 }
 
@@ -277,49 +277,51 @@ k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   }
 }
 
-template <int DIM, bool PA>
+template <int DIM, bool PA, bool NC = true>
 __device__ __forceinline__ double cell_resid_at(const LevelDev& L, const double* phi,
                                                 const double* rhs, const int* ci) {
   const int c = lin(L, ci);
   double dg;
   const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
-  return __ldg(rhs + c) - lp;
+  return (NC ? __ldg(rhs + c) : rhs[c]) - lp;
+}
+
+// mean of the 2^d fine residuals of coarse cell C (multigrid.py:177-182)
+template <int DIM, bool PA, bool NC = true>
+__device__ __forceinline__ double cell_rr_at(const LevelDev& Lf, const double* phi, const double* rhs,
+                                             const int* C) {
+  if (DIM == 3) {
+    double s[2];
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      double q[2];
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        int a0[3] = {2 * C[0], 2 * C[1] + j, 2 * C[2] + k};
+        int a1[3] = {2 * C[0] + 1, 2 * C[1] + j, 2 * C[2] + k};
+        q[j] = 0.5 * (cell_resid_at<3, PA, NC>(Lf, phi, rhs, a0) + cell_resid_at<3, PA, NC>(Lf, phi, rhs, a1));
+      }
+      s[k] = 0.5 * (q[0] + q[1]);
+    }
+    return 0.5 * (s[0] + s[1]);
+  }
+  double q[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    int a0[3] = {0, 2 * C[1], 2 * C[2] + k};
+    int a1[3] = {0, 2 * C[1] + 1, 2 * C[2] + k};
+    q[k] = 0.5 * (cell_resid_at<2, PA, NC>(Lf, phi, rhs, a0) + cell_resid_at<2, PA, NC>(Lf, phi, rhs, a1));
+  }
+  return 0.5 * (q[0] + q[1]);
 }
 
 template <int DIM, bool PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict__ rhs,
           double* __restrict__ coarse, Box cb, unsigned total) {
-  {
-    int C[3];
-    if (!box_point(cb, C)) return;
-    double out;
-    if (DIM == 3) {
-      double s[2];
-#pragma unroll 1
-      for (int k = 0; k < 2; ++k) {
-        double q[2];
-#pragma unroll 1
-        for (int j = 0; j < 2; ++j) {
-          int a0[3] = {2 * C[0], 2 * C[1] + j, 2 * C[2] + k};
-          int a1[3] = {2 * C[0] + 1, 2 * C[1] + j, 2 * C[2] + k};
-          q[j] = 0.5 * (cell_resid_at<3, PA>(Lf, phi, rhs, a0) + cell_resid_at<3, PA>(Lf, phi, rhs, a1));
-        }
-        s[k] = 0.5 * (q[0] + q[1]);
-      }
-      out = 0.5 * (s[0] + s[1]);
-    } else {
-      double q[2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int a0[3] = {0, 2 * C[1], 2 * C[2] + k};
-        int a1[3] = {0, 2 * C[1] + 1, 2 * C[2] + k};
-        q[k] = 0.5 * (cell_resid_at<2, PA>(Lf, phi, rhs, a0) + cell_resid_at<2, PA>(Lf, phi, rhs, a1));
-      }
-      out = 0.5 * (q[0] + q[1]);
-    }
-    coarse[lin(Lc, C)] = out;
-  }
+  int C[3];
+  if (!box_point(cb, C)) return;
+  coarse[lin(Lc, C)] = cell_rr_at<DIM, PA>(Lf, phi, rhs, C);
 }
 
 // ---------------------------------------------------------------------------
@@ -340,65 +342,78 @@ __device__ __forceinline__ void tang_pair(const LevelDev& Lc, int ax, int fine_i
   }
 }
 
+template <bool NC>
+__device__ __forceinline__ double ldc(const double* p, int i) { return NC ? __ldg(p + i) : p[i]; }
+
+// fine face F of component A += bilinear prolongation of the coarse field
+// (multigrid.py:236-295): tangential (3/4, 1/4) weights, normal midpoint mean
+template <int DIM, int A, bool NC = true>
+__device__ __forceinline__ void face_pa_at(const LevelDev& Lf, const LevelDev& Lc, const double* coarse,
+                                           double* fine, const int* F) {
+  using O = Others<DIM, A>;
+  int J1, n1, J2 = 0, n2 = 0;
+  tang_pair(Lc, O::B1, F[O::B1], J1, n1);
+  if (DIM == 3) tang_pair(Lc, O::B2, F[O::B2], J2, n2);
+  auto T = [&](int I) -> double {
+    int c[3] = {0, 0, 0};
+    c[A] = I;
+    if (DIM == 3) {
+      c[O::B1] = J1; c[O::B2] = J2;
+      const double x00 = ldc<NC>(coarse, lin(Lc, c));
+      c[O::B1] = n1;
+      const double x10 = ldc<NC>(coarse, lin(Lc, c));
+      c[O::B1] = J1; c[O::B2] = n2;
+      const double x01 = ldc<NC>(coarse, lin(Lc, c));
+      c[O::B1] = n1;
+      const double x11 = ldc<NC>(coarse, lin(Lc, c));
+      const double ta = 0.75 * x00 + 0.25 * x10;
+      const double tb = 0.75 * x01 + 0.25 * x11;
+      return 0.75 * ta + 0.25 * tb;
+    } else {
+      c[O::B1] = J1;
+      const double x0 = ldc<NC>(coarse, lin(Lc, c));
+      c[O::B1] = n1;
+      const double x1 = ldc<NC>(coarse, lin(Lc, c));
+      return 0.75 * x0 + 0.25 * x1;
+    }
+  };
+  const int I = F[A] >> 1;
+  double v;
+  if ((F[A] & 1) == 0) {
+    v = T(I);
+  } else {
+    int I2 = I + 1;
+    if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A] && !(A == 0 && Lc.dist0)) I2 = 0;
+    v = 0.5 * (T(I) + T(I2));
+  }
+  const int f = lin(Lf, F);
+  fine[f] = fine[f] + v;
+}
+
 template <int DIM, int A>
 __global__ void __launch_bounds__(kThreads)
 k_face_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
           Box fb, unsigned total) {
-  using O = Others<DIM, A>;
-  {
-    int F[3];
-    if (!box_point(fb, F)) return;
-    int J1, n1, J2 = 0, n2 = 0;
-    tang_pair(Lc, O::B1, F[O::B1], J1, n1);
-    if (DIM == 3) tang_pair(Lc, O::B2, F[O::B2], J2, n2);
-    auto T = [&](int I) -> double {
-      int c[3] = {0, 0, 0};
-      c[A] = I;
-      if (DIM == 3) {
-        c[O::B1] = J1; c[O::B2] = J2;
-        const double x00 = __ldg(coarse + lin(Lc, c));
-        c[O::B1] = n1;
-        const double x10 = __ldg(coarse + lin(Lc, c));
-        c[O::B1] = J1; c[O::B2] = n2;
-        const double x01 = __ldg(coarse + lin(Lc, c));
-        c[O::B1] = n1;
-        const double x11 = __ldg(coarse + lin(Lc, c));
-        const double ta = 0.75 * x00 + 0.25 * x10;
-        const double tb = 0.75 * x01 + 0.25 * x11;
-        return 0.75 * ta + 0.25 * tb;
-      } else {
-        c[O::B1] = J1;
-        const double x0 = __ldg(coarse + lin(Lc, c));
-        c[O::B1] = n1;
-        const double x1 = __ldg(coarse + lin(Lc, c));
-        return 0.75 * x0 + 0.25 * x1;
-      }
-    };
-    const int I = F[A] >> 1;
-    double v;
-    if ((F[A] & 1) == 0) {
-      v = T(I);
-    } else {
-      int I2 = I + 1;
-      if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A] && !(A == 0 && Lc.dist0)) I2 = 0;
-      v = 0.5 * (T(I) + T(I2));
-    }
-    const int f = lin(Lf, F);
-    fine[f] = fine[f] + v;
-  }
+  int F[3];
+  if (!box_point(fb, F)) return;
+  face_pa_at<DIM, A>(Lf, Lc, coarse, fine, F);
+}
+
+template <int DIM, bool NC = true>
+__device__ __forceinline__ void cell_pa_at(const LevelDev& Lf, const LevelDev& Lc, const double* coarse,
+                                           double* fine, const int* F) {
+  int C[3] = {DIM == 3 ? F[0] >> 1 : 0, F[1] >> 1, F[2] >> 1};
+  const int f = lin(Lf, F);
+  fine[f] = fine[f] + ldc<NC>(coarse, lin(Lc, C));
 }
 
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
           Box fb, unsigned total) {
-  {
-    int F[3];
-    if (!box_point(fb, F)) return;
-    int C[3] = {DIM == 3 ? F[0] >> 1 : 0, F[1] >> 1, F[2] >> 1};
-    const int f = lin(Lf, F);
-    fine[f] = fine[f] + __ldg(coarse + lin(Lc, C));
-  }
+  int F[3];
+  if (!box_point(fb, F)) return;
+  cell_pa_at<DIM>(Lf, Lc, coarse, fine, F);
 }
 
 // ---------------------------------------------------------------------------
@@ -1380,6 +1395,221 @@ k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// coarse-level tail of a V-cycle in ONE CTA (multigrid.py:391-439 below the
+// chain's top level).  Levels of <= 16^3 cells are launch-latency bound: each
+// colour pass / transfer is 1-2 us of work behind 3-5 us of launch and drain.
+// Here every pass is a block-strided loop followed by __syncthreads, the
+// iterate and right-hand sides are re-read with plain (coherent) loads, and
+// the operation order is the multi-kernel V-cycle's, so results are
+// identical to it.
+// ---------------------------------------------------------------------------
+
+constexpr int kCoarseThreads = 512;
+
+__device__ __forceinline__ void cz_fill(double* x, long long n) {
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
+}
+
+// one colour pass of component A on chain level C (k_face_colour's mapping)
+template <int DIM, int FORM, int A, bool PA>
+__device__ void cf_colour(const CoarseLv& C, double omega, int parity) {
+  const LevelDev& L = C.d;
+  const Box b = face_box(L, DIM, A);
+  const int off = (L.bclo[A] == BC_PER) ? 0 : 1;
+  const int e1 = b.hi[1] - b.lo[1] + 1;
+  const int half2 = (b.hi[2] - b.lo[2] + 2) / 2;
+  const int total = (b.hi[0] - b.lo[0] + 1) * e1 * half2;
+  double* const* x = C.x;
+  const double* uc[3] = {x[0], x[1], x[2]};
+  const double* rhs = C.rhs[A];
+  for (int phase = 0; phase < (C.two_phase ? 2 : 1); ++phase) {
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int tt = t % half2, r = t / half2;
+      int ci[3];
+      ci[1] = b.lo[1] + r % e1;
+      ci[0] = b.lo[0] + r / e1;
+      ci[2] = b.lo[2] + ((parity + off - ci[0] - ci[1] - b.lo[2]) & 1) + 2 * tt;
+      if (ci[2] > b.hi[2]) continue;
+      const int f = lin(L, ci);
+      if (phase == 1) {
+        x[A][f] = C.tmp[f];
+        continue;
+      }
+      double dg;
+      const double au = face_row<DIM, FORM, A, PA, false>(L, uc, f, ci, dg);
+      const double nv = uc[A][f] + omega * ((rhs[f] - au) / dg);
+      if (C.two_phase) C.tmp[f] = nv;
+      else x[A][f] = nv;
+    }
+    __syncthreads();
+  }
+}
+
+template <int DIM, int FORM, int A, bool PA>
+__device__ void cf_rr(const CoarseLv& F, const CoarseLv& Cc) {
+  const Box cb = face_box(Cc.d, DIM, A);
+  const int e1 = cb.hi[1] - cb.lo[1] + 1, e2 = cb.hi[2] - cb.lo[2] + 1;
+  const int total = (cb.hi[0] - cb.lo[0] + 1) * e1 * e2;
+  const double* u[3] = {F.x[0], F.x[1], F.x[2]};
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    int C[3];
+    C[2] = cb.lo[2] + t % e2;
+    C[1] = cb.lo[1] + (t / e2) % e1;
+    C[0] = cb.lo[0] + t / (e1 * e2);
+    double tv[3];
+#pragma unroll 1
+    for (int o = -1; o <= 1; ++o) {
+      int fa = 2 * C[A] + o;
+      if (fa < 0) fa += F.d.n[A];
+      tv[o + 1] = tmean_resid<DIM, FORM, A, PA, false>(F.d, u, F.rhs[A], C, fa);
+    }
+    Cc.rhs[A][lin(Cc.d, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
+  }
+}
+
+template <int DIM, int A>
+__device__ void cf_pa(const CoarseLv& Cc, const CoarseLv& F) {
+  const Box fb = face_box(F.d, DIM, A);
+  const int e1 = fb.hi[1] - fb.lo[1] + 1, e2 = fb.hi[2] - fb.lo[2] + 1;
+  const int total = (fb.hi[0] - fb.lo[0] + 1) * e1 * e2;
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    int X[3];
+    X[2] = fb.lo[2] + t % e2;
+    X[1] = fb.lo[1] + (t / e2) % e1;
+    X[0] = fb.lo[0] + t / (e1 * e2);
+    face_pa_at<DIM, A, false>(F.d, Cc.d, Cc.x[A], F.x[A], X);
+  }
+}
+
+template <int DIM, int FORM, bool PA>
+__device__ void cf_smooth(const CoarseLv& C, double omega, int sweeps) {
+  for (int s = 0; s < sweeps; ++s) {
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) {
+      if (DIM == 3) cf_colour<3, FORM, 0, PA>(C, omega, p);
+    }
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) cf_colour<DIM, FORM, 1, PA>(C, omega, p);
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) cf_colour<DIM, FORM, 2, PA>(C, omega, p);
+  }
+}
+
+template <int DIM, int FORM, bool PA>
+__global__ void __launch_bounds__(kCoarseThreads, 1)
+k_coarse_face(const CoarseChain* __restrict__ gch, int sweeps_down, int sweeps_up, int bottom, double omega) {
+  __shared__ CoarseChain ch;
+  {
+    const int* src = reinterpret_cast<const int*>(gch);
+    int* dst = reinterpret_cast<int*>(&ch);
+    for (int i = threadIdx.x; i < (int)(sizeof(CoarseChain) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int nl = ch.nl;
+  for (int l = 0; l < nl; ++l) {
+    const CoarseLv& C = ch.lv[l];
+    for (int A = 3 - DIM; A < 3; ++A) cz_fill(C.x[A], C.block);
+    __syncthreads();
+    if (l == nl - 1) {
+      cf_smooth<DIM, FORM, PA>(C, omega, bottom);
+    } else {
+      cf_smooth<DIM, FORM, PA>(C, omega, sweeps_down);
+      if (DIM == 3) cf_rr<3, FORM, 0, PA>(C, ch.lv[l + 1]);
+      cf_rr<DIM, FORM, 1, PA>(C, ch.lv[l + 1]);
+      cf_rr<DIM, FORM, 2, PA>(C, ch.lv[l + 1]);
+      __syncthreads();
+    }
+  }
+  for (int l = nl - 2; l >= 0; --l) {
+    const CoarseLv& C = ch.lv[l];
+    if (DIM == 3) cf_pa<3, 0>(ch.lv[l + 1], C);
+    cf_pa<DIM, 1>(ch.lv[l + 1], C);
+    cf_pa<DIM, 2>(ch.lv[l + 1], C);
+    __syncthreads();
+    cf_smooth<DIM, FORM, PA>(C, omega, sweeps_up);
+  }
+}
+
+template <int DIM, bool PA>
+__device__ void cc_smooth(const CoarseLv& C, double omega, int sweeps) {
+  const LevelDev& L = C.d;
+  const int e1 = L.n[1];
+  const int half2 = (L.n[2] + 1) / 2;
+  const int total = L.n[0] * e1 * half2;
+  double* phi = C.x[0];
+  const double* rhs = C.rhs[0];
+  for (int s = 0; s < sweeps; ++s) {
+#pragma unroll 1
+    for (int parity = 0; parity < 2; ++parity) {
+      for (int phase = 0; phase < (C.two_phase ? 2 : 1); ++phase) {
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+          const int tt = t % half2, r = t / half2;
+          int ci[3];
+          ci[1] = r % e1;
+          ci[0] = r / e1;
+          ci[2] = ((parity - ci[0] - ci[1]) & 1) + 2 * tt;
+          if (ci[2] >= L.n[2]) continue;
+          const int c = lin(L, ci);
+          if (phase == 1) {
+            phi[c] = C.tmp[c];
+            continue;
+          }
+          double dg;
+          const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
+          const double nv = phi[c] + omega * (rhs[c] - lp) / dg;
+          if (C.two_phase) C.tmp[c] = nv;
+          else phi[c] = nv;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <int DIM, bool PA>
+__global__ void __launch_bounds__(kCoarseThreads, 1)
+k_coarse_cell(const CoarseChain* __restrict__ gch, int sweeps_down, int sweeps_up, int bottom, double omega) {
+  __shared__ CoarseChain ch;
+  {
+    const int* src = reinterpret_cast<const int*>(gch);
+    int* dst = reinterpret_cast<int*>(&ch);
+    for (int i = threadIdx.x; i < (int)(sizeof(CoarseChain) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int nl = ch.nl;
+  for (int l = 0; l < nl; ++l) {
+    const CoarseLv& C = ch.lv[l];
+    cz_fill(C.x[0], C.block);
+    __syncthreads();
+    if (l == nl - 1) {
+      cc_smooth<DIM, PA>(C, omega, bottom);
+    } else {
+      cc_smooth<DIM, PA>(C, omega, sweeps_down);
+      const CoarseLv& Cc = ch.lv[l + 1];
+      const int e1 = Cc.d.n[1], e2 = Cc.d.n[2];
+      const int total = Cc.d.n[0] * e1 * e2;
+      for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        int K[3] = {t / (e1 * e2), (t / e2) % e1, t % e2};
+        Cc.rhs[0][lin(Cc.d, K)] = cell_rr_at<DIM, PA, false>(C.d, C.x[0], C.rhs[0], K);
+      }
+      __syncthreads();
+    }
+  }
+  for (int l = nl - 2; l >= 0; --l) {
+    const CoarseLv& C = ch.lv[l];
+    const CoarseLv& Cc = ch.lv[l + 1];
+    const int e1 = C.d.n[1], e2 = C.d.n[2];
+    const int total = C.d.n[0] * e1 * e2;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      int F[3] = {t / (e1 * e2), (t / e2) % e1, t % e2};
+      cell_pa_at<DIM, false>(C.d, Cc.d, Cc.x[0], C.x[0], F);
+    }
+    __syncthreads();
+    cc_smooth<DIM, PA>(C, omega, sweeps_up);
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1584,6 +1814,32 @@ void launch_cell_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   const unsigned total = box_count(fb);
   if (dim == 3) k_cell_pa<3><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
   else k_cell_pa<2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
+}
+
+void launch_coarse_face(cudaStream_t s, int dim, int form, bool pa, const CoarseChain* dchain,
+                        int sweeps_down, int sweeps_up, int bottom, double omega) {
+  ++g_kernel_launches;
+  SB_DISPATCH_FORM(form, {
+    if (dim == 3) {
+      if (pa) k_coarse_face<3, FM, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+      else k_coarse_face<3, FM, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    } else {
+      if (pa) k_coarse_face<2, FM, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+      else k_coarse_face<2, FM, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    }
+  });
+}
+
+void launch_coarse_cell(cudaStream_t s, int dim, bool pa, const CoarseChain* dchain, int sweeps_down,
+                        int sweeps_up, int bottom, double omega) {
+  ++g_kernel_launches;
+  if (dim == 3) {
+    if (pa) k_coarse_cell<3, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    else k_coarse_cell<3, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+  } else {
+    if (pa) k_coarse_cell<2, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    else k_coarse_cell<2, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+  }
 }
 
 // padded box covering every array of the level

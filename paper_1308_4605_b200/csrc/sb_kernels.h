@@ -1,6 +1,7 @@
 // sb_kernels.h -- host-side launchers for the sm_100a kernels (sb_kernels.cu).
 #pragma once
 #include <cuda_runtime.h>
+#include <vector>
 #include "sb_device.cuh"
 
 namespace sb {
@@ -10,6 +11,25 @@ struct CPtr3 { const double* p[3]; };
 
 // Sub-box of a level: lo/hi inclusive per internal axis.
 struct Box { int lo[3], hi[3]; };
+
+// The coarse-level tail of a V-cycle (levels of <= kCoarseCells cells) run by
+// one CTA: level 0 of the chain receives its right-hand side from the fine
+// levels' residual->restriction and returns its correction in x.
+constexpr int kCoarseMaxLevels = 10;
+constexpr long long kCoarseCells = 4096;
+struct CoarseLv {
+  LevelDev d;
+  double* x[3];      // iterate (face components; cell uses x[0])
+  double* rhs[3];
+  double* tmp;       // two-phase scratch (odd periodic extents)
+  long long block;   // elements per array of the level
+  int two_phase;
+  int pad_;
+};
+struct CoarseChain {
+  int nl, pad_[3];
+  CoarseLv lv[kCoarseMaxLevels];
+};
 
 // colour passes (multigrid.py:318-340)
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
@@ -29,6 +49,13 @@ void launch_face_sweep2(cudaStream_t s, const LevelDev& L, int form, int A, CPtr
                         const double* rhsA, double omega);
 void launch_cell_sweep2(cudaStream_t s, const LevelDev& L, const double* phi, double* pnew, const double* rhs,
                         double omega);
+// wavefront red-black sweeps, one launch per component (sb_wave.cu)
+bool wave_supported(const LevelDev& L, int dim, int form);
+std::vector<int> wave_steps(int np, bool per0, int lookahead);  // step order, 2*plane + colour
+void launch_face_wave(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u, const double* rhsA,
+                      double omega, const int* steps, int nsteps, int* ctr);
+void launch_cell_wave(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double omega,
+                      const int* steps, int nsteps, int* ctr);
 // fused residual -> restriction (multigrid.py:403-406 + :177-233)
 void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
                                 int form, int A, CPtr3 u, const double* rhsA, double* coarseA);
@@ -39,6 +66,11 @@ void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
                              const double* coarseA, double* fineA);
 void launch_cell_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
                              const double* coarse, double* fine);
+// one-CTA coarse tail (sb_kernels.cu k_coarse_face / k_coarse_cell); dchain in device memory
+void launch_coarse_face(cudaStream_t s, int dim, int form, bool all_periodic, const CoarseChain* dchain,
+                        int sweeps_down, int sweeps_up, int bottom, double omega);
+void launch_coarse_cell(cudaStream_t s, int dim, bool all_periodic, const CoarseChain* dchain,
+                        int sweeps_down, int sweeps_up, int bottom, double omega);
 // full-level operators
 void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 u, const double* p,
                     Ptr3 out_u, double* out_p);

@@ -55,6 +55,10 @@ struct Level {
   double *mu_c = nullptr, *gam_c = nullptr, *mu_e[3]{}, *rho_f[3]{}, *beta_f[3]{};
   double *fx[3]{}, *frhs[3]{}, *cx = nullptr, *crhs = nullptr, *tmp = nullptr;
   bool fused = false;                         // two-colour streaming sweeps (sb_sweep.cu)
+  bool wave = false;                          // wavefront red-black sweeps (sb_wave.cu)
+  int* wsteps[4]{};                           // step tables: face components 0..2, cells (3)
+  int wnsteps[4]{};
+  int* wctr = nullptr;                        // work counter + per-plane red counters
   double *fxa[3]{}, *cxa = nullptr;           // ping-pong partners of the iterate
 };
 
@@ -92,6 +96,10 @@ struct sb_ctx {
   double *sc0 = nullptr, *sc1 = nullptr, *scR = nullptr, *scC = nullptr;
   double *sf0[3]{}, *sf1[3]{}, *sfR[3]{}, *sfC[3]{};
   double* splane = nullptr;   // staging for one wall plane of BoundaryValues
+  // one-CTA coarse tail of the V-cycles (levels >= coarse_ls; -1 = off)
+  int coarse_ls = -1;
+  CoarseChain* dchain_face = nullptr;
+  CoarseChain* dchain_cell = nullptr;
   bool scratch = false, scratch_mg = false;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -151,6 +159,14 @@ void make_level(sb_ctx* c, const int* n, double h) {
     return e && e[0] == '1';
   }();
   L.fused = fused_on && !L.two_phase && sweep2_supported(L.d, c->dim, c->form);
+  // wavefront sweeps (sb_wave.cu) on levels with >= SB_WAVE_MIN planes; opt-in
+  // (default 0 = off): they halve the sweep's HBM traffic but measured no
+  // faster than the per-colour passes
+  const int wave_min = [] {  // read per context: tests compare both paths in one process
+    const char* e = std::getenv("SB_WAVE_MIN");
+    return e ? std::atoi(e) : 0;
+  }();
+  L.wave = !L.fused && wave_min > 0 && n[0] >= wave_min && wave_supported(L.d, c->dim, c->form);
   c->lv.push_back(L);
 }
 
@@ -176,6 +192,21 @@ void alloc_level(sb_ctx* c, Level& L, bool first) {
     L.crhs = dalloc(c, B);
   }
   if (L.two_phase) L.tmp = dalloc(c, B);
+  if (L.wave) {
+    const char* ek = std::getenv("SB_WAVE_K");  // red lookahead in planes
+    const int K = std::max(1, ek ? std::atoi(ek) : 8);
+    for (int k = 0; k < 4; ++k) {
+      const bool wallA = k < 3 && k >= 3 - c->dim && L.d.bclo[k] != BC_PER;
+      const int np = L.d.n[0] - (k == 0 && wallA ? 1 : 0);
+      const std::vector<int> st = wave_steps(np, L.d.bclo[0] == BC_PER, K);
+      L.wsteps[k] = reinterpret_cast<int*>(dalloc(c, ((long long)st.size() + 1) / 2));
+      // same stream as dalloc's zero fill, then wait: the host vector dies here
+      CK(cudaMemcpyAsync(L.wsteps[k], st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      L.wnsteps[k] = (int)st.size();
+    }
+    L.wctr = reinterpret_cast<int*>(dalloc(c, (L.d.n[0] + 2) / 2 + 1));
+  }
   if (L.fused) {
     for (int a = 3 - c->dim; a < 3; ++a) L.fxa[a] = dalloc(c, B);
     L.cxa = dalloc(c, B);
@@ -377,6 +408,23 @@ double cell_pass_bytes(const sb_ctx* c, const Level& L) {
 // sweep out of place into alt[] and swap the pointers (ping-pong).
 void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* const* rhs, double omega) {
   Level& L = c->lv[l];
+  if (L.wave) {
+    for (int A = 3 - c->dim; A < 3; ++A) {
+      cudaEvent_t ea = nullptr;
+      if (c->profiling) {
+        ea = next_event(c);
+        CK(cudaEventRecord(ea, c->st));
+      }
+      Ptr3 u{{cur[0], cur[1], cur[2]}};
+      launch_face_wave(c->st, L.d, c->form, A, u, rhs[A], omega, L.wsteps[A], L.wnsteps[A], L.wctr);
+      if (c->profiling) {
+        cudaEvent_t eb = next_event(c);
+        CK(cudaEventRecord(eb, c->st));
+        c->prof.push_back({ea, eb, 0, l == 0, 2 * face_pass_bytes(c, L)});
+      }
+    }
+    return;
+  }
   const int per_launch = L.fused ? 2 : 1;
   for (int A = 3 - c->dim; A < 3; ++A) {
     for (int parity = 0; parity < 2; parity += per_launch) {
@@ -405,6 +453,20 @@ void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* cons
 
 void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs, double omega) {
   Level& L = c->lv[l];
+  if (L.wave) {
+    cudaEvent_t ea = nullptr;
+    if (c->profiling) {
+      ea = next_event(c);
+      CK(cudaEventRecord(ea, c->st));
+    }
+    launch_cell_wave(c->st, L.d, cur, rhs, omega, L.wsteps[3], L.wnsteps[3], L.wctr);
+    if (c->profiling) {
+      cudaEvent_t eb = next_event(c);
+      CK(cudaEventRecord(eb, c->st));
+      c->prof.push_back({ea, eb, 1, l == 0, 2 * cell_pass_bytes(c, L)});
+    }
+    return;
+  }
   const int per_launch = L.fused ? 2 : 1;
   for (int parity = 0; parity < 2; parity += per_launch) {
     cudaEvent_t ea = nullptr;
@@ -429,7 +491,59 @@ void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs,
 }
 
 // multigrid.py:409-439 -- x is written (zero initial guess)
+double chain_face_bytes(sb_ctx* c, const sb_smoother& sm) {
+  double b = 0;
+  const int last = (int)c->lv.size() - 1;
+  for (int l = c->coarse_ls; l <= last; ++l) {
+    const int sw = l == last ? sm.bottom_sweeps : sm.sweeps_down + sm.sweeps_up;
+    b += 2.0 * c->dim * sw * face_pass_bytes(c, c->lv[l]);
+  }
+  return b;
+}
+double chain_cell_bytes(sb_ctx* c, const sb_smoother& sm) {
+  double b = 0;
+  const int last = (int)c->lv.size() - 1;
+  for (int l = c->coarse_ls; l <= last; ++l) {
+    const int sw = l == last ? sm.bottom_sweeps : sm.sweeps_down + sm.sweeps_up;
+    b += 2.0 * sw * cell_pass_bytes(c, c->lv[l]);
+  }
+  return b;
+}
+
+// the coarse tail in one launch when level l is the chain's top level and the
+// buffers are the level's own (the V-cycle recursion's)
+bool coarse_tail(sb_ctx* c, int l, int kind, const double* const* rhs, double* const* x, const sb_smoother& sm) {
+  if (l != c->coarse_ls || l <= 0) return false;
+  Level& L = c->lv[l];
+  if (kind == SB_KIND_FACE) {
+    for (int A = 3 - c->dim; A < 3; ++A)
+      if (rhs[A] != L.frhs[A] || x[A] != L.fx[A]) return false;
+  } else if (rhs[0] != L.crhs || x[0] != L.cx) {
+    return false;
+  }
+  cudaEvent_t ea = nullptr;
+  if (c->profiling) {
+    ea = next_event(c);
+    CK(cudaEventRecord(ea, c->st));
+  }
+  bool pa = true;
+  for (int a = 0; a < 3; ++a) pa = pa && c->bc[a][0] == BC_PER;
+  if (kind == SB_KIND_FACE)
+    launch_coarse_face(c->st, c->dim, c->form, pa, c->dchain_face, sm.sweeps_down, sm.sweeps_up, sm.bottom_sweeps,
+                       sm.omega);
+  else
+    launch_coarse_cell(c->st, c->dim, pa, c->dchain_cell, sm.sweeps_down, sm.sweeps_up, sm.bottom_sweeps, sm.omega);
+  if (c->profiling) {
+    cudaEvent_t eb = next_event(c);
+    CK(cudaEventRecord(eb, c->st));
+    c->prof.push_back({ea, eb, kind == SB_KIND_FACE ? 0 : 1, false,
+                       kind == SB_KIND_FACE ? chain_face_bytes(c, sm) : chain_cell_bytes(c, sm)});
+  }
+  return true;
+}
+
 void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, const sb_smoother& sm) {
+  if (coarse_tail(c, l, SB_KIND_FACE, rhs, x, sm)) return;
   Level& L = c->lv[l];
   double* cur[3] = {x[0], x[1], x[2]};
   double* alt[3] = {L.fxa[0], L.fxa[1], L.fxa[2]};
@@ -453,6 +567,11 @@ void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, c
 }
 
 void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smoother& sm) {
+  {
+    const double* r3[3] = {rhs, nullptr, nullptr};
+    double* x3[3] = {x, nullptr, nullptr};
+    if (coarse_tail(c, l, SB_KIND_CELL, r3, x3, sm)) return;
+  }
   Level& L = c->lv[l];
   double* cur = x;
   double* alt = L.cxa;
@@ -1028,6 +1147,52 @@ int guard(F&& f) {
 // Coarsen the level-0 coefficients (already on the device) down the hierarchy,
 // derive 1/rho_face, run the zero-diagonal / positive-density checks and the
 // velocity null space (multigrid.py:92-169, :70-89; operators.py:368-388).
+// choose the coarse tail (first level >= 1 with <= kCoarseCells cells) and
+// upload its level table; SB_COARSE_KERNEL=0 keeps every level multi-kernel
+void upload_chains(sb_ctx* c) {
+  const bool enabled = [] {
+    const char* e = std::getenv("SB_COARSE_KERNEL");
+    return !(e && e[0] == '0');
+  }();
+  c->coarse_ls = -1;
+  const int nlev = (int)c->lv.size();
+  if (!enabled || c->lv[0].d.dist0 || nlev < 2) return;
+  int ls = -1;
+  for (int l = 1; l < nlev; ++l) {
+    long long cells = 1;
+    for (int a = 3 - c->dim; a < 3; ++a) cells *= c->lv[l].d.n[a];
+    if (cells <= kCoarseCells) {
+      ls = l;
+      break;
+    }
+  }
+  if (ls < 0 || nlev - ls > kCoarseMaxLevels) return;
+  CoarseChain hf{}, hc{};
+  hf.nl = hc.nl = nlev - ls;
+  for (int l = ls; l < nlev; ++l) {
+    const Level& L = c->lv[l];
+    CoarseLv& f = hf.lv[l - ls];
+    CoarseLv& k = hc.lv[l - ls];
+    f.d = k.d = L.d;
+    for (int a = 0; a < 3; ++a) {
+      f.x[a] = L.fx[a];
+      f.rhs[a] = L.frhs[a];
+    }
+    k.x[0] = L.cx;
+    k.rhs[0] = L.crhs;
+    f.tmp = k.tmp = L.tmp;
+    f.block = k.block = L.block;
+    f.two_phase = k.two_phase = L.two_phase ? 1 : 0;
+  }
+  const long long nd = (long long)(sizeof(CoarseChain) + 7) / 8;
+  if (!c->dchain_face) c->dchain_face = reinterpret_cast<CoarseChain*>(dalloc(c, nd));
+  if (!c->dchain_cell) c->dchain_cell = reinterpret_cast<CoarseChain*>(dalloc(c, nd));
+  CK(cudaMemcpyAsync(c->dchain_face, &hf, sizeof(hf), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->dchain_cell, &hc, sizeof(hc), cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->coarse_ls = ls;
+}
+
 void build_from_level0(sb_ctx* c) {
     for (size_t l = 0; l + 1 < c->lv.size(); ++l) {
       Level& F = c->lv[l];
@@ -1041,6 +1206,7 @@ void build_from_level0(sb_ctx* c) {
         launch_coarsen_edge(c->st, F.d, C.d, 2, 0, F.mu_e[0], C.mu_e[0]);
       }
     }
+    upload_chains(c);
     CK(cudaMemsetAsync(c->dflags, 0, 16, c->st));
     int hf[4] = {0, 0, 0, 0};
     for (size_t l = 0; l < c->lv.size(); ++l) {
