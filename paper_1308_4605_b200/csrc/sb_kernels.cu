@@ -390,13 +390,96 @@ __device__ __forceinline__ void face_pa_at(const LevelDev& Lf, const LevelDev& L
   fine[f] = fine[f] + v;
 }
 
+// The two coarse neighbours used by the fine faces 2J (J-1) and 2J+1 (J+1)
+// along tangential axis ax (tang_pair for both parities at once).
+__device__ __forceinline__ void tang_nbrs(const LevelDev& Lc, int ax, int J, int& jm, int& jp) {
+  jm = J - 1;
+  jp = J + 1;
+  const int n = Lc.n[ax];
+  if (ax == 0 && Lc.dist0) {
+    // ghost planes hold the neighbouring slabs' values
+  } else if (Lc.bclo[ax] == BC_PER) {
+    if (jm < 0) jm += n;
+    if (jp >= n) jp -= n;
+  } else {
+    jm = jm < 0 ? 0 : jm;
+    jp = jp > n - 1 ? n - 1 : jp;
+  }
+}
+
+// Prolongation + add, one thread per coarse position C = (I along A, J1, J2):
+// the 2^d fine faces (2I+{0,1}, 2J1+{0,1}, 2J2+{0,1}) from 2 x 3^(d-1) coarse
+// values (instead of up to 8 per fine face).  Same expressions, same order as
+// face_pa_at, so bit-identical.
 template <int DIM, int A>
 __global__ void __launch_bounds__(kThreads)
-k_face_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
-          Box fb, unsigned total) {
-  int F[3];
-  if (!box_point(fb, F)) return;
-  face_pa_at<DIM, A>(Lf, Lc, coarse, fine, F);
+k_face_pa8(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine, Box cb) {
+  using O = Others<DIM, A>;
+  int C[3];
+  if (!box_point(cb, C)) return;
+  const int I = C[A];
+  int I2 = I + 1;
+  if (Lc.bclo[A] == BC_PER && I2 == Lc.n[A] && !(A == 0 && Lc.dist0)) I2 = 0;
+  int jm1, jp1, jm2 = 0, jp2 = 0;
+  tang_nbrs(Lc, O::B1, C[O::B1], jm1, jp1);
+  if (DIM == 3) tang_nbrs(Lc, O::B2, C[O::B2], jm2, jp2);
+  double T[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    int c[3] = {C[0], C[1], C[2]};
+    c[A] = a ? I2 : I;
+    if (DIM == 3) {
+      const int b1[3] = {jm1, C[O::B1], jp1}, b2[3] = {jm2, C[O::B2], jp2};
+      double x[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          c[O::B1] = b1[u];
+          c[O::B2] = b2[v];
+          x[u][v] = __ldg(coarse + lin(Lc, c));
+        }
+#pragma unroll
+      for (int p1 = 0; p1 < 2; ++p1)
+#pragma unroll
+        for (int p2 = 0; p2 < 2; ++p2) {
+          const int n1 = p1 ? 2 : 0, n2 = p2 ? 2 : 0;
+          const double ta = 0.75 * x[1][1] + 0.25 * x[n1][1];
+          const double tb = 0.75 * x[1][n2] + 0.25 * x[n1][n2];
+          T[a][p1][p2] = 0.75 * ta + 0.25 * tb;
+        }
+    } else {
+      const int b1[3] = {jm1, C[O::B1], jp1};
+      double x[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        c[O::B1] = b1[u];
+        x[u] = __ldg(coarse + lin(Lc, c));
+      }
+#pragma unroll
+      for (int p1 = 0; p1 < 2; ++p1) {
+        T[a][p1][0] = 0.75 * x[1] + 0.25 * x[p1 ? 2 : 0];
+        T[a][p1][1] = T[a][p1][0];
+      }
+    }
+  }
+  const bool wallA = Lf.bclo[A] != BC_PER;
+#pragma unroll
+  for (int pa = 0; pa < 2; ++pa) {
+    if (wallA && pa == 0 && I == 0) continue;  // fine wall face, not an unknown
+#pragma unroll
+    for (int p1 = 0; p1 < 2; ++p1)
+#pragma unroll
+      for (int p2 = 0; p2 < (DIM == 3 ? 2 : 1); ++p2) {
+        int F[3] = {0, 0, 0};
+        F[A] = 2 * I + pa;
+        F[O::B1] = 2 * C[O::B1] + p1;
+        if (DIM == 3) F[O::B2] = 2 * C[O::B2] + p2;
+        const double v = pa == 0 ? T[0][p1][p2] : 0.5 * (T[0][p1][p2] + T[1][p1][p2]);
+        const int f = lin(Lf, F);
+        fine[f] = fine[f] + v;
+      }
+  }
 }
 
 template <int DIM, bool NC = true>
@@ -1752,9 +1835,15 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
     const L3 c3 = cfg3(1, eT, e2);
     // chunk along A: enough CTAs to fill the machine, at least 4 coarse faces per thread
     long long cols = (long long)c3.g.x * c3.g.y;
-    int nchunk = (int)std::max<long long>(1, std::min<long long>(eA / 4, (kSMs * 8 + cols - 1) / cols));
-    if (nchunk < 1) nchunk = 1;
-    const int chunk = (eA + nchunk - 1) / nchunk;
+    // chunks of 4 coarse faces (measured best at 256^3: 2 -> 8 spans 5 %);
+    // more when the grid would not fill the machine otherwise
+    int nchunk = (int)std::max<long long>(1, std::max<long long>(eA / 4, (kSMs * 8 + cols - 1) / cols));
+    nchunk = std::min(nchunk, eA);
+    static const int chunk_env = [] {
+      const char* e = std::getenv("SB_RR_CHUNK");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int chunk = chunk_env > 0 ? std::min(chunk_env, eA) : (eA + nchunk - 1) / nchunk;
     nchunk = (eA + chunk - 1) / chunk;
     dim3 g(c3.g.x, c3.g.y, nchunk);
     if (all_periodic(Lf)) k_face_rr_m<DIM, FM, A, true><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
@@ -1795,15 +1884,20 @@ void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
 void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
                              const double* coarseA, double* fineA) {
   ++g_kernel_launches;
-  Box fb = face_box(Lf, dim, A);
-  const unsigned total = box_count(fb);
+  // one thread per coarse position (I along A, J1, J2), 2^d fine faces each
+  Box cb;
+  for (int a = 0; a < 3; ++a) {
+    cb.lo[a] = 0;
+    cb.hi[a] = Lc.n[a] - 1;
+  }
+  if (dim == 2) cb.hi[0] = 0;
   if (dim == 3) {
-    if (A == 0) k_face_pa<3, 0><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else if (A == 1) k_face_pa<3, 1><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else k_face_pa<3, 2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    if (A == 0) k_face_pa8<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
+    else if (A == 1) k_face_pa8<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
+    else k_face_pa8<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
   } else {
-    if (A == 1) k_face_pa<2, 1><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
-    else k_face_pa<2, 2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarseA, fineA, fb, total);
+    if (A == 1) k_face_pa8<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
+    else k_face_pa8<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
   }
 }
 
