@@ -283,6 +283,43 @@ def gen_gmres():
              restart=case.restart, status=hist.status, iterations=hist.iterations, c=spec.c)
 
 
+FORM_SOLVES = [  # (cells, bc, form, theta, precond, schur sign, restart)
+    ((32, 32), ["nn", "nn"], "laplacian", 0.0, "P1", "minus", 20),
+    ((32, 48), ["ff", "pp"], "stress_bulk", 0.5, "P2", "minus", 20),
+    ((32, 32), ["fn", "nf"], "stress", 2.0, "P3", "minus", 30),
+    ((32, 32), ["pp", "nn"], "stress_bulk", 1.0, "P4", "plus", 30),
+    ((32, 32), ["nn", "ff"], "laplacian", 0.3, "P5", "minus", 30),
+    ((8, 8, 8), ["nn", "nn", "nn"], "laplacian", 0.0, "P1", "minus", 20),
+    ((8, 8, 16), ["pp", "ff", "nn"], "stress_bulk", 1.0, "P2", "minus", 20),
+    ((8, 16, 8), ["fn", "pp", "pp"], "stress", 0.0, "P4", "plus", 30),
+    ((16, 8, 8), ["pp", "pp", "pp"], "stress", 0.7, "P5", "minus", 30),
+]
+
+
+def gen_form_solves():
+    """GMRES solves beyond the BASELINE recipes: every viscous form, mixed
+    no-slip / free-slip / periodic walls, steady and unsteady, P1..P5 and both
+    Schur signs, each with the reference's own coefficient averaging and rhs."""
+    rng = np.random.default_rng(8217)
+    for k, (cells, bc, form, theta, kind, sign, restart) in enumerate(FORM_SOLVES):
+        g = grid(cells, bc, 1.0 / cells[0])
+        c = rand_coeff(g, rng, theta, form)
+        rhs, _ = PR.make_rhs(g, c, seed=100 + k)
+        cs, rs, spec = OP.rescale(c, rhs)
+        name = f"gf{k}_{form}_{kind}"
+        put_coeff(name, cs)
+        put_face(name, "bu", rs.u)
+        put(name, "bp", rs.p.data)
+        gcfg = sm.GmresConfig(restart=restart, max_iters=300, rtol=1e-9, atol=0.0, track_true_residual=True)
+        pcfg = PC.PrecondConfig(kind=PC.PrecondKind(kind), schur=sm.SchurConfig(sign=sm.SchurSign(sign)))
+        x, hist = sm.gmres_solve(rs, cs, pcfg, gcfg)
+        put_face(name, "xu", x.u)
+        put(name, "xp", x.p.data)
+        put(name, "hist", np.array(hist.rows(), dtype=np.float64))
+        meta(name, "gmres", g, bc, cs.theta, form, precond=kind, schur_sign=sign, restart=restart,
+             status=hist.status, iterations=hist.iterations, c=spec.c)
+
+
 DRIVER_CONFIGS = [
     {"problem": {"kind": "bubble", "dim": 2, "cells": 32, "bc": "no_slip", "seed": 3},
      "solver": {"gmres": {"restart": 10, "rtol": 1e-9}},
@@ -325,6 +362,7 @@ def main():
     gen_gmres()
     gen_affine()
     gen_driver()
+    gen_form_solves()
     np.savez_compressed(OUT / "golden.npz", **store)
     (OUT / "golden.json").write_text(json.dumps(index, indent=1))
     print(len(index), "cases,", len(store), "arrays ->", OUT / "golden.npz")

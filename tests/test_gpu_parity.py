@@ -143,8 +143,10 @@ def test_gmres_vs_golden(e):
     c = pkg_coeff(e, grid=g)
     n = e["name"]
     rhs = StokesVector(FaceField(g, tuple(face(n, "bu", g.dim))), CellField(g, arr(n, "bp")))
-    x, hist = gmres_solve(rhs, c, PrecondConfig(kind=PrecondKind(e["precond"])),
-                          GmresConfig(restart=e["restart"], track_true_residual=True))
+    from paper_1308_4605_b200.schur import SchurConfig, SchurSign
+    pc = PrecondConfig(kind=PrecondKind(e["precond"]),
+                       schur=SchurConfig(sign=SchurSign(e.get("schur_sign", "minus"))))
+    x, hist = gmres_solve(rhs, c, pc, GmresConfig(restart=e["restart"], track_true_residual=True))
     assert hist.status == e["status"]
     assert abs(hist.iterations - e["iterations"]) <= 1
     ref = StokesVector(FaceField(g, tuple(face(n, "xu", g.dim))), CellField(g, arr(n, "xp")))

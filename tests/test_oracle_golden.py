@@ -107,7 +107,8 @@ def test_gmres_solves(e):
     geo, c = oracle_geo(e), oracle_coef(e)
     d, n = geo.dim, e["name"]
     bu, bp = face(n, "bu", d), arr(n, "bp")
-    u, p, hist = O.gmres_solve(geo, c, bu, bp, O.PrecondOpts(kind=e["precond"]),
+    sign = -1.0 if e.get("schur_sign", "minus") == "minus" else 1.0
+    u, p, hist = O.gmres_solve(geo, c, bu, bp, O.PrecondOpts(kind=e["precond"], sign=sign),
                                O.GmresOpts(restart=e["restart"], track_true_residual=True))
     assert hist.status == e["status"]
     assert hist.iterations == e["iterations"]
