@@ -886,23 +886,6 @@ __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double 
 
 __global__ void k_add_scalar(double* y, const double* x) { *y += *x; }
 
-// per-block means of the deferred null-space projection: mean[b] = sum[slot[b]]
-// * inv_count (k_box_sub_mean's expression), 0 for blocks without a null space
-struct Slots4 { int s[4]; };
-__global__ void k_block_means(const double* __restrict__ sums, Slots4 slot, double inv_count, double* mean) {
-  const int b = threadIdx.x;
-  if (b < 4) mean[b] = slot.s[b] >= 0 ? sums[slot.s[b]] * inv_count : 0.0;
-}
-
-// v[e] -= mean[block of e] over a pad-free flat vector (materialise the projection)
-__global__ void __launch_bounds__(kThreads)
-k_sub_block_means(double* __restrict__ v, const double* __restrict__ mean, long long block, long long n) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const double m = __ldg(mean + (e >= block) + (e >= 2 * block) + (e >= 3 * block));
-    v[e] = v[e] - m;
-  }
-}
-
 __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, Box b, unsigned total) {
   {
     int ci[3];
@@ -1223,18 +1206,77 @@ k_dcgs_b_l2(const double* __restrict__ Q, long long vstride, int nv, const doubl
   }
 }
 
-// Gram variant, pass A: like k_dcgs_a (q_k finished in place, d = Q^T w), plus
-// the dots Q_l . s_k (l < k) and s_k . s_k of the provisional vector, from
-// which the host extends the Gram matrix of the basis.  Partial slots:
-// [0..k] d, [k+1..2k] Q_l . s_k, [2k+1] s_k . s_k.  Register-chunked: every
-// thread owns CH double2 of each vector per step, so the two warp reductions
-// per basis vector are amortised over 2*CH elements and CH independent loads
-// are in flight.
+// Gram variant, pass A: like k_dcgs_a, plus the dots Q_l . s_k (l < k) and
+// s_k . s_k of the provisional vector, from which the host extends the Gram
+// matrix of the basis.  Partial slots: [0..k] Q.w with the finished q_k,
+// [k+1..2k] Q_l . s_k, [2k+1] s_k . s_k.
+__global__ void __launch_bounds__(kThreads)
+k_dcgs_a_g(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+           const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nslot = 2 * k + 2;
+  for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long step = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e - threadIdx.x < n2; e += 2 * step) {
+    const long long e1 = e + step;
+    const bool ok0 = e < n2, ok1 = e1 < n2;
+    const double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    const double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    const double2 sa = ok0 ? s2[e] : make_double2(0.0, 0.0);
+    const double2 sb = ok1 ? s2[e1] : make_double2(0.0, 0.0);
+    double2 q0 = sa, q1 = sb;
+    for (int i = 0; i < k; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
+      const double2 b = ok1 ? __ldg(v2 + e1) : make_double2(0.0, 0.0);
+      const double ci = cs[i];
+      q0.x -= ci * a.x;
+      q0.y -= ci * a.y;
+      q1.x -= ci * b.x;
+      q1.y -= ci * b.y;
+      const double dw = warp_sum((a.x * w0.x + a.y * w0.y) + (b.x * wv1.x + b.y * wv1.y));
+      const double dsv = warp_sum((a.x * sa.x + a.y * sa.y) + (b.x * sb.x + b.y * sb.y));
+      if (lane == 0) {
+        acc[i][warp] += dw;
+        acc[k + 1 + i][warp] += dsv;
+      }
+    }
+    if (k > 0) {
+      q0.x *= inv_gamma;
+      q0.y *= inv_gamma;
+      q1.x *= inv_gamma;
+      q1.y *= inv_gamma;
+      if (ok0) s2[e] = q0;
+      if (ok1) s2[e1] = q1;
+    }
+    const double dq = warp_sum((q0.x * w0.x + q0.y * w0.y) + (q1.x * wv1.x + q1.y * wv1.y));
+    const double ss = warp_sum((sa.x * sa.x + sa.y * sa.y) + (sb.x * sb.x + sb.y * sb.y));
+    if (lane == 0) {
+      acc[k][warp] += dq;
+      acc[2 * k + 1][warp] += ss;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
+// Same as k_dcgs_a_g, register-chunked: every thread owns CH double2 of each
+// vector per step, so the two warp reductions per basis vector are amortised
+// over 2*CH elements (instead of 4) and CH independent loads are in flight.
 template <int CH>
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
-            const double* __restrict__ w, long long n2, double* __restrict__ partials,
-            const double* __restrict__ bmean, long long b2) {
+            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1253,11 +1295,6 @@ k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __re
       const long long e = base + t * blockDim.x + threadIdx.x;
       ok[t] = e < n2;
       wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
-      if (bmean != nullptr && ok[t]) {  // deferred null-space projection of w
-        const double m = __ldg(bmean + (e >= b2) + (e >= 2 * b2) + (e >= 3 * b2));
-        wv[t].x = wv[t].x - m;
-        wv[t].y = wv[t].y - m;
-      }
       sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
       q[t] = sv[t];
     }
@@ -1312,8 +1349,7 @@ k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __re
 // (one streaming read of the basis).
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
-           const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials,
-           const double* __restrict__ bmean, long long b2) {
+           const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
   __shared__ double acc[kThreads / 32];
   __shared__ double ds[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1328,18 +1364,6 @@ k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double
     const bool ok0 = e < n2, ok1 = e1 < n2;
     double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
     double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
-    if (bmean != nullptr) {  // deferred null-space projection of w
-      if (ok0) {
-        const double m = __ldg(bmean + (e >= b2) + (e >= 2 * b2) + (e >= 3 * b2));
-        w0.x = w0.x - m;
-        w0.y = w0.y - m;
-      }
-      if (ok1) {
-        const double m = __ldg(bmean + (e1 >= b2) + (e1 >= 2 * b2) + (e1 >= 3 * b2));
-        wv1.x = wv1.x - m;
-        wv1.y = wv1.y - m;
-      }
-    }
     for (int i = 0; i < nv; ++i) {
       const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
       const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
@@ -2077,17 +2101,6 @@ void launch_sum_abs_partial(cudaStream_t s, const double* x, long long n, double
   k_sum_abs_partial<<<kRedBlocks, kThreads, 0, s>>>(x, n, partials, kRedBlocks);
 }
 
-void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* mean) {
-  ++g_kernel_launches;
-  Slots4 sl{{slot[0], slot[1], slot[2], slot[3]}};
-  k_block_means<<<1, 32, 0, s>>>(sums, sl, inv_count, mean);
-}
-
-void launch_sub_block_means(cudaStream_t s, double* v, const double* mean, long long block, long long n) {
-  ++g_kernel_launches;
-  k_sub_block_means<<<grid_for(n), kThreads, 0, s>>>(v, mean, block, n);
-}
-
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x) {
   ++g_kernel_launches;
   k_add_scalar<<<1, 1, 0, s>>>(y, x);
@@ -2144,16 +2157,20 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
 }
 
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
-                     const double* w, long long n, double* partials, const double* bmean, long long block) {
+                     const double* w, long long n, double* partials) {
   ++g_kernel_launches;
-  k_dcgs_a_g2<4><<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials, bmean,
-                                                 block / 2);
+  static const bool chunked = [] {
+    const char* e = std::getenv("SB_DCGS_A");
+    return !(e && e[0] == '0');
+  }();
+  if (chunked) k_dcgs_a_g2<4><<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+  else k_dcgs_a_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
-                     double* out, long long n, double* partials, const double* bmean, long long block) {
+                     double* out, long long n, double* partials) {
   ++g_kernel_launches;
-  k_dcgs_b_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials, bmean, block / 2);
+  k_dcgs_b_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {

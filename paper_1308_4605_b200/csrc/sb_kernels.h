@@ -114,17 +114,10 @@ void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int n
                        double* w, long long n, double* partials, int mode);  // mode 0: dots, 1: norm
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out);
 // Gram-matrix variant of the delayed-reorthogonalisation passes
-// bmean (optional): per-block means subtracted from w on load (deferred null
-// projection of a pad-free vector of blocks of `block` elements)
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
-                     const double* w, long long n, double* partials, const double* bmean = nullptr,
-                     long long block = 0);
+                     const double* w, long long n, double* partials);
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
-                     double* out, long long n, double* partials, const double* bmean = nullptr,
-                     long long block = 0);
-// deferred null projection: means from block sums, and its materialisation
-void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* mean);
-void launch_sub_block_means(cudaStream_t s, double* v, const double* mean, long long block, long long n);
+                     double* out, long long n, double* partials);
 // delayed-reorthogonalisation Arnoldi passes (see sb_solver.cu gmres())
 void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                    const double* w, long long n, double* partials);

@@ -96,10 +96,6 @@ struct sb_ctx {
   double *sc0 = nullptr, *sc1 = nullptr, *scR = nullptr, *scC = nullptr;
   double *sf0[3]{}, *sf1[3]{}, *sfR[3]{}, *sfC[3]{};
   double* splane = nullptr;   // staging for one wall plane of BoundaryValues
-  // deferred null-space projection of P^-1 outputs (pad-free layouts, Gram
-  // Arnoldi): the graph leaves the means in dmean, the passes subtract them
-  bool proj_defer = false, gdefer = false;
-  double* dmean = nullptr;
   // one-CTA coarse tail of the V-cycles (levels >= coarse_ls; -1 = off)
   int coarse_ls = -1;
   CoarseChain* dchain_face = nullptr;
@@ -676,15 +672,6 @@ long long precond_cost(const sb_ctx* c, const sb_precond& pc) {
   }
 }
 
-// every element of every block of a level-0 vector is an unknown (no pads, no
-// wall faces): a flat per-block mean subtraction equals the box one
-bool pad_free(const sb_ctx* c) {
-  const Level& L = c->lv[0];
-  for (int a = 0; a < 3; ++a)
-    if (c->bc[a][0] != BC_PER) return false;
-  return L.P[2] == L.d.n[2];
-}
-
 void project_nulls(sb_ctx* c, double* x) {
   const Level& L = c->lv[0];
   Box cb;
@@ -694,19 +681,6 @@ void project_nulls(sb_ctx* c, double* x) {
   }
   const double ncell = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
   double* xp = vpres(c, x);
-  if (c->proj_defer) {
-    // sums now, subtraction by the consumers (dcgs passes / sub_block_means)
-    int slot[4] = {-1, -1, -1, -1};
-    block_sum(c, xp, L.block, 0);
-    slot[c->dim] = 0;
-    int k = 1;
-    for (int A : c->null_comps) {
-      block_sum(c, vcomp(c, x, A), L.block, k);
-      slot[A - c->off] = k++;
-    }
-    launch_block_means(c->st, dmisc(c), slot, 1.0 / ncell, c->dmean);
-    return;
-  }
   block_sum(c, xp, L.block, 0);
   launch_box_add_scalar(c->st, L.d, cb, xp, dmisc(c) + 0, 1.0 / ncell);
   int slot = 1;
@@ -802,17 +776,13 @@ void drop_graph(sb_ctx* c) {
 }
 
 // vw = P^{-1} vMv, through the cached CUDA graph when enabled
-// deferred_ok: the caller subtracts c->dmean itself (Arnoldi passes);
-// otherwise a deferred projection is materialised here
-void precond_apply_graph(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm, bool deferred_ok = false) {
-  const bool materialise = c->proj_defer && !deferred_ok && pc.kind != SB_IDENTITY;
+void precond_apply_graph(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm) {
   if (!c->use_graphs || c->profiling) {
     precond_dev(c, pc, sm, c->vMv, c->vw);
-    if (materialise) launch_sub_block_means(c->st, c->vw, c->dmean, c->lv[0].block, c->vlen);
     return;
   }
   const bool same = c->gexec && std::memcmp(&c->gpc, &pc, sizeof(pc)) == 0 &&
-                    std::memcmp(&c->gsm, &sm, sizeof(sm)) == 0 && c->gdefer == c->proj_defer;
+                    std::memcmp(&c->gsm, &sm, sizeof(sm)) == 0;
   if (!same) {
     drop_graph(c);
     ensure_scratch(c);
@@ -845,11 +815,9 @@ void precond_apply_graph(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm,
     c->gnodes = nk;
     c->gpc = pc;
     c->gsm = sm;
-    c->gdefer = c->proj_defer;
   }
   CK(cudaGraphLaunch(c->gexec, c->st));
   c->graph_launches += c->gnodes;
-  if (materialise) launch_sub_block_means(c->st, c->vw, c->dmean, c->lv[0].block, c->vlen);
 }
 
 // ---- GMRES (krylov.py:81-214) -----------------------------------------------------
@@ -958,23 +926,6 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     if (nr < max_rows) rows[nr] = sb_history_row{it, *vcyc, rp, rt, rf ? 1 : 0};
     ++nr;
   };
-  static const bool cgs2 = [] {
-    const char* e = std::getenv("SB_ORTHO");
-    return e && std::strcmp(e, "cgs2") == 0;
-  }();
-  // default: Gram variant; SB_ORTHO=dcgs re-reads the basis for c', =cgs2 three passes
-  static const bool gram = [] {
-    const char* e = std::getenv("SB_ORTHO");
-    return !(e && (std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
-  }();
-  // null-space means of P^-1 outputs subtracted inside the Arnoldi passes
-  // (saves a read+write pass per projected block; SB_DEFER_PROJ=0 disables)
-  const bool defer_env = [] {  // read per solve: tests compare both paths in one process
-    const char* e = std::getenv("SB_DEFER_PROJ");
-    return !(e && e[0] == '0');
-  }();
-  c->proj_defer = defer_env && gram && !cgs2 && pad_free(c) && pc.kind != SB_IDENTITY;
-  if (c->proj_defer && !c->dmean) c->dmean = dalloc(c, 4);  // before any graph capture
   vec_in(c, bu, bp, c->vb);
   vec_norm2(c, c->vb, 0);
   const double bnorm = std::sqrt(fetch_misc(c, 0));
@@ -1000,8 +951,16 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
   const double bd_tol = std::max(gc.atol, 1e-14 * rp0);
 
   std::vector<double> H((m + 1) * m), Horig((m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1), cpend(m + 1);
+  static const bool cgs2 = [] {
+    const char* e = std::getenv("SB_ORTHO");
+    return e && std::strcmp(e, "cgs2") == 0;
+  }();
+  // default: Gram variant; SB_ORTHO=dcgs re-reads the basis for c', =cgs2 three passes
+  static const bool gram = [] {
+    const char* e = std::getenv("SB_ORTHO");
+    return !(e && (std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
+  }();
   std::vector<double> G((m + 1) * (m + 1), 0.0);
-  const double* bmean = nullptr;
   double gam = 1.0;
   int k = 0;
   bool first = true;
@@ -1027,8 +986,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     int ydim = 0;  // columns in the last least-squares solve
     while (j < m && k < gc.max_iters) {
       apply_M_vec(c, V + (long long)j * vl, c->vMv);
-      precond_apply_graph(c, pc, sm, c->proj_defer);
-      bmean = c->proj_defer ? c->dmean : nullptr;
+      precond_apply_graph(c, pc, sm);
       *vcyc += precond_cost(c, pc);
       ++k;
       double hn;
@@ -1060,10 +1018,9 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         if (j > 0) CK(cudaMemcpyAsync(dh2(c), hy(c), j * 8, cudaMemcpyHostToDevice, c->st));
         double cc = 0.0, ww;
         if (gram) {
-          launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart, bmean, c->lv[0].block);
+          launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
           launch_finalize(c->st, c->dpart, 2 * j + 2, dh1(c));
-          launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart, bmean,
-                          c->lv[0].block);
+          launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
           launch_finalize(c->st, c->dpart, 1, dh2(c) + kMaxVec - 1);
           CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
           sync(c);

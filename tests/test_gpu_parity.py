@@ -281,29 +281,3 @@ def test_fused_two_colour_sweeps_vs_oracle(cells, bc, form, theta):
     wy = y.copy()
     O.sweep_cell(geo, oc, wy, yr, O.diag_cell(geo, oc), 1.0)
     assert relerr(gy.data, wy) <= 1e-13
-
-
-@pytest.mark.parametrize("name", ["gm_C5_16_P1", "gm_C3_16_P1", "gf8_stress_P5"])
-def test_deferred_null_projection_bit_identical(name, monkeypatch):
-    """The null-space means of P^-1 outputs subtracted inside the Arnoldi passes
-    (pad-free grids, SB_DEFER_PROJ) give the same solve, to the bit, as the
-    explicit subtraction pass in the preconditioner graph."""
-    from paper_1308_4605_b200 import operators
-    from paper_1308_4605_b200.grid import CellField, FaceField, StokesVector, pack_stokes
-    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
-    from paper_1308_4605_b200.precond import PrecondConfig, PrecondKind
-    e = [x for x in cases("gmres") if x["name"] == name][0]
-    g = pkg_grid(e)
-    c = pkg_coeff(e, grid=g)
-    n = e["name"]
-    rhs = StokesVector(FaceField(g, tuple(face(n, "bu", g.dim))), CellField(g, arr(n, "bp")))
-    pc, gc = PrecondConfig(kind=PrecondKind(e["precond"])), GmresConfig(restart=e["restart"])
-    out = {}
-    for v in ("1", "0"):
-        monkeypatch.setenv("SB_DEFER_PROJ", v)
-        operators._POOL.clear()
-        x, h = gmres_solve(rhs, c, pc, gc)
-        out[v] = (pack_stokes(x), h.iterations, [r[2] for r in h.rows()])
-    assert out["1"][1] == out["0"][1] == e["iterations"]
-    assert out["1"][2] == out["0"][2]
-    assert np.array_equal(out["1"][0], out["0"][0])
