@@ -147,7 +147,7 @@ def _oracle_case(config, n, precond):
     return case, geo, oc, list(rs.u.components), rs.p.data
 
 
-def cpu_sample(config, n_target, n_sample, k, precond, iterations):
+def cpu_sample(config, target_cells, n_sample, k, precond, iterations):
     """Time the oracle on the same recipe at n_sample^d: hierarchy setup, then a
     GMRES run capped at k iterations (k+1 preconditioned-operator applications);
     extrapolate linearly in cell count (every kernel is O(N)) to a full solve of
@@ -163,13 +163,13 @@ def cpu_sample(config, n_target, n_sample, k, precond, iterations):
                                                           track_true_residual=False))
     t2 = time.perf_counter()
     t_app = (t2 - t1) / (k + 1)
-    scale = (n_target / n_sample) ** geo.dim
+    scale = float(math.prod(target_cells)) / float(n_sample) ** geo.dim
     restarts = max(0, (iterations - 1) // case.restart)
     t_full = scale * ((t1 - t0) + (iterations + 1 + restarts) * t_app)
     sample = (f"oracle (NumPy port of stokesmg, 1 thread) on the {config} recipe at {n_sample}^{geo.dim}: "
               f"hierarchy setup {t1 - t0:.2f}s + {k} GMRES iterations ({k + 1} P^-1 M applications, "
               f"{t_app:.2f}s each), extrapolated x{scale:g} in cells to {iterations} iterations at "
-              f"{n_target}^{geo.dim}")
+              f"{'x'.join(map(str, target_cells))}")
     return t_full, t2 - t0, sample
 
 
@@ -185,16 +185,28 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    n_target = args.n or (256 if args.config in ("C4", "C5") else (128 if args.config == "C3" else
-                                                                   (64 if args.config == "C1" else 256)))
+    from paper_1308_4605_b200 import problems as PR
+    n_gpus = max(args.gpus, world)
+    # the device arm's workload: the single-GPU recipe, or C5's weak-scaling
+    # grid for N GPUs (bench.py --gpus N runs c5_cells(N) globally)
+    if n_gpus > 1 and args.config == "C5":
+        cells = tuple(PR.c5_cells(n_gpus))
+        restart, walls_s = 50, "periodic"
+    else:
+        n_t = args.n or (256 if args.config in ("C4", "C5") else (128 if args.config == "C3" else
+                                                                 (64 if args.config == "C1" else 256)))
+        dim = 2 if args.config in ("C1", "C2") else 3
+        cells = (n_t,) * dim
+        restart = 50 if args.config in ("C3", "C5") else 30
+        walls_s = "periodic" if args.config in ("C1", "C3", "C5") else "walls"
     its, its_src = bench_iterations(args.config, args.precond, 40)
-    n_sample = min(n_target, 128) if args.config in ("C3", "C4", "C5") else n_target
+    n_sample = min(cells[0], 128) if args.config in ("C3", "C4", "C5") else cells[0]
     for _ in range(args.warmup):
-        cpu_sample(args.config, n_target, max(8, n_sample // 4), 1, args.precond, its)
+        cpu_sample(args.config, cells, max(8, n_sample // 4), 1, args.precond, its)
     vals, walls = [], []
     desc = ""
     for _ in range(args.steps):
-        v, w, desc = cpu_sample(args.config, n_target, n_sample, 1, args.precond, its)
+        v, w, desc = cpu_sample(args.config, cells, n_sample, 1, args.precond, its)
         vals.append(v)
         walls.append(w)
     v = statistics.mean(vals)
@@ -203,8 +215,10 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded recipe, SURVEY §8d)",
-        "config": {"workload": f"{args.config} {n_target}^3 P1 GMRES({50 if args.config in ('C3', 'C5') else 30})",
-                   "precond": args.precond, "iterations_assumed": its, "iterations_source": its_src},
+        "config": {"workload": f"{args.config} {'x'.join(map(str, cells))} {walls_s} {args.precond} "
+                               f"GMRES({restart}) rtol 1e-9",
+                   "precond": args.precond, "cells": list(cells), "iterations_assumed": its,
+                   "iterations_source": its_src},
         "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
                          "sample_wall_s": statistics.mean(walls)},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -372,7 +386,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_t = case.grid.cells[0]
         n_s = min(n_t, 128) if g.dim == 3 else n_t
-        v, wall, desc = cpu_sample(args.config, n_t, n_s, 2, args.precond, iters)
+        v, wall, desc = cpu_sample(args.config, tuple(case.grid.cells), n_s, 2, args.precond, iters)
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
                "sample_wall_s": wall}
 
