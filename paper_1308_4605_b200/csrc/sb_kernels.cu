@@ -593,6 +593,106 @@ k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Pt
   }
 }
 
+// Residual of all face components into memory (rhs - A x; the fused
+// residual->restriction's face_resid_at expression), for the split
+// residual / restriction path on large levels: one face row per thread at
+// full occupancy instead of the latency-bound marching kernels.
+template <int DIM, int FORM, bool PA>
+__global__ void __launch_bounds__(kThreads)
+k_face_res3(LevelDev L, CPtr3 x, CPtr3 rhs, Ptr3 out, Box b) {
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  const int f = lin(L, ci);
+#pragma unroll
+  for (int A = 3 - DIM; A < 3; ++A) {
+    if (!in_face(L, A, ci) || is_wall_face(L, A, ci)) continue;
+    double au;
+    double dg;
+    if (A == 0) au = face_row<DIM, FORM, (DIM == 3 ? 0 : 1), PA>(L, x.p, f, ci, dg);
+    else if (A == 1) au = face_row<DIM, FORM, 1, PA>(L, x.p, f, ci, dg);
+    else au = face_row<DIM, FORM, 2, PA>(L, x.p, f, ci, dg);
+    out.p[A][f] = __ldg(rhs.p[A] + f) - au;
+  }
+}
+
+// Face restriction of a residual field (multigrid.py:195-233): the tangential
+// 2^(d-1) mean on the three fine normal planes, weights (1/4, 1/2, 1/4).
+template <int DIM, int A>
+__global__ void __launch_bounds__(kThreads)
+k_face_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* __restrict__ coarse, Box cb) {
+  using O = Others<DIM, A>;
+  int C[3];
+  if (!box_point(cb, C)) return;
+  double tv[3];
+#pragma unroll
+  for (int o = -1; o <= 1; ++o) {
+    int fa = 2 * C[A] + o;
+    if (fa < 0 && !(A == 0 && Lf.dist0)) fa += Lf.n[A];
+    int fi[3] = {2 * C[0], 2 * C[1], 2 * C[2]};
+    if (DIM == 2) fi[0] = 0;
+    fi[A] = fa;
+    if (DIM == 3) {
+      double p[2];
+#pragma unroll
+      for (int t2 = 0; t2 < 2; ++t2) {
+        int q0[3] = {fi[0], fi[1], fi[2]};
+        q0[O::B2] += t2;
+        int q1[3] = {q0[0], q0[1], q0[2]};
+        q1[O::B1] += 1;
+        p[t2] = 0.5 * (__ldg(r + lin(Lf, q0)) + __ldg(r + lin(Lf, q1)));
+      }
+      tv[o + 1] = 0.5 * (p[0] + p[1]);
+    } else {
+      int q1[3] = {fi[0], fi[1], fi[2]};
+      q1[O::B1] += 1;
+      tv[o + 1] = 0.5 * (__ldg(r + lin(Lf, fi)) + __ldg(r + lin(Lf, q1)));
+    }
+  }
+  coarse[lin(Lc, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
+}
+
+template <int DIM, bool PA>
+__global__ void __launch_bounds__(kThreads)
+k_cell_res(LevelDev L, const double* x, const double* __restrict__ rhs, double* __restrict__ out, Box b) {
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  out[lin(L, ci)] = cell_resid_at<DIM, PA>(L, x, rhs, ci);
+}
+
+// cell restriction of a residual field (multigrid.py:177-182), cell_rr_at's order
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+k_cell_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* __restrict__ coarse, Box cb) {
+  int C[3];
+  if (!box_point(cb, C)) return;
+  double out;
+  if (DIM == 3) {
+    double s[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double q[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        int a0[3] = {2 * C[0], 2 * C[1] + j, 2 * C[2] + k};
+        int a1[3] = {2 * C[0] + 1, 2 * C[1] + j, 2 * C[2] + k};
+        q[j] = 0.5 * (__ldg(r + lin(Lf, a0)) + __ldg(r + lin(Lf, a1)));
+      }
+      s[k] = 0.5 * (q[0] + q[1]);
+    }
+    out = 0.5 * (s[0] + s[1]);
+  } else {
+    double q[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      int a0[3] = {0, 2 * C[1], 2 * C[2] + k};
+      int a1[3] = {0, 2 * C[1] + 1, 2 * C[2] + k};
+      q[k] = 0.5 * (__ldg(r + lin(Lf, a0)) + __ldg(r + lin(Lf, a1)));
+    }
+    out = 0.5 * (q[0] + q[1]);
+  }
+  coarse[lin(Lc, C)] = out;
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_residual(LevelDev L, const double* x, const double* rhs, double* out, Box b, unsigned total) {
@@ -1878,6 +1978,62 @@ void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
       else face_rr_t<2, FM, 2>(s, Lf, Lc, u, rhsA, coarseA);
     }
   });
+}
+
+void launch_face_res3(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 x, CPtr3 rhs, Ptr3 out) {
+  ++g_kernel_launches;
+  Box b;
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = 0;
+    b.hi[a] = L.n[a] - 1 + (L.bclo[a] != BC_PER ? 1 : 0);
+  }
+  if (dim == 2) b.hi[0] = 0;
+  const bool pa = all_periodic(L);
+  SB_DISPATCH_FORM(form, {
+    if (dim == 3) {
+      if (pa) k_face_res3<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      else k_face_res3<3, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+    } else {
+      if (pa) k_face_res3<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      else k_face_res3<2, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+    }
+  });
+}
+
+void launch_face_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A, const double* r,
+                          double* coarse) {
+  ++g_kernel_launches;
+  Box cb = face_box(Lc, dim, A);
+  if (dim == 3) {
+    if (A == 0) k_face_restrict<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+    else if (A == 1) k_face_restrict<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+    else k_face_restrict<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+  } else {
+    if (A == 1) k_face_restrict<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+    else k_face_restrict<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+  }
+}
+
+void launch_cell_res(cudaStream_t s, const LevelDev& L, int dim, const double* x, const double* rhs,
+                     double* out) {
+  ++g_kernel_launches;
+  Box b = cell_box(L);
+  const bool pa = all_periodic(L);
+  if (dim == 3) {
+    if (pa) k_cell_res<3, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+    else k_cell_res<3, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+  } else {
+    if (pa) k_cell_res<2, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+    else k_cell_res<2, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+  }
+}
+
+void launch_cell_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, const double* r,
+                          double* coarse) {
+  ++g_kernel_launches;
+  Box cb = cell_box(Lc);
+  if (dim == 3) k_cell_restrict<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+  else k_cell_restrict<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
 }
 
 void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,

@@ -61,6 +61,14 @@ void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
                                 int form, int A, CPtr3 u, const double* rhsA, double* coarseA);
 void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
                                 const double* phi, const double* rhs, double* coarse);
+// split residual / restriction (large levels): residual field to memory, then restrict
+void launch_face_res3(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 x, CPtr3 rhs, Ptr3 out);
+void launch_face_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A, const double* r,
+                          double* coarse);
+void launch_cell_res(cudaStream_t s, const LevelDev& L, int dim, const double* x, const double* rhs,
+                     double* out);
+void launch_cell_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, const double* r,
+                          double* coarse);
 // prolongation + add (multigrid.py:185-192, :236-295, :431-436)
 void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
                              const double* coarseA, double* fineA);

@@ -55,6 +55,8 @@ struct Level {
   double *mu_c = nullptr, *gam_c = nullptr, *mu_e[3]{}, *rho_f[3]{}, *beta_f[3]{};
   double *fx[3]{}, *frhs[3]{}, *cx = nullptr, *crhs = nullptr, *tmp = nullptr;
   bool fused = false;                         // two-colour streaming sweeps (sb_sweep.cu)
+  bool split_rr = false;                      // residual to memory, then restrict (large levels)
+  double *fres[3]{}, *cres = nullptr;
   bool wave = false;                          // wavefront red-black sweeps (sb_wave.cu)
   int* wsteps[4]{};                           // step tables: face components 0..2, cells (3)
   int wnsteps[4]{};
@@ -167,6 +169,17 @@ void make_level(sb_ctx* c, const int* n, double h) {
     return e ? std::atoi(e) : 0;
   }();
   L.wave = !L.fused && wave_min > 0 && n[0] >= wave_min && wave_supported(L.d, c->dim, c->form);
+  // split residual / restriction on levels with >= SB_RR_SPLIT cells (default
+  // 64^3; 0 = always fused): full-occupancy residual kernel + light restriction
+  const long long split_min = [] {
+    const char* e = std::getenv("SB_RR_SPLIT");
+    return e ? std::atoll(e) : 262144LL;
+  }();
+  {
+    long long cells = 1;
+    for (int a = 3 - c->dim; a < 3; ++a) cells *= n[a];
+    L.split_rr = split_min > 0 && cells >= split_min && can_coarsen(n, c->dim);
+  }
   c->lv.push_back(L);
 }
 
@@ -192,6 +205,10 @@ void alloc_level(sb_ctx* c, Level& L, bool first) {
     L.crhs = dalloc(c, B);
   }
   if (L.two_phase) L.tmp = dalloc(c, B);
+  if (L.split_rr) {
+    for (int a = 3 - c->dim; a < 3; ++a) L.fres[a] = dalloc(c, B);
+    L.cres = dalloc(c, B);
+  }
   if (L.wave) {
     const char* ek = std::getenv("SB_WAVE_K");  // red lookahead in planes
     const int K = std::max(1, ek ? std::atoi(ek) : 8);
@@ -555,8 +572,15 @@ void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, c
     for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
     Level& Lc = c->lv[l + 1];
     CPtr3 xc{{cur[0], cur[1], cur[2]}};
-    for (int A = 3 - c->dim; A < 3; ++A)
-      launch_face_resid_restrict(c->st, L.d, Lc.d, c->dim, c->form, A, xc, rhs[A], Lc.frhs[A]);
+    if (L.split_rr) {
+      CPtr3 rr{{rhs[0], rhs[1], rhs[2]}};
+      Ptr3 res{{L.fres[0], L.fres[1], L.fres[2]}};
+      launch_face_res3(c->st, L.d, c->dim, c->form, xc, rr, res);
+      for (int A = 3 - c->dim; A < 3; ++A) launch_face_restrict(c->st, L.d, Lc.d, c->dim, A, L.fres[A], Lc.frhs[A]);
+    } else {
+      for (int A = 3 - c->dim; A < 3; ++A)
+        launch_face_resid_restrict(c->st, L.d, Lc.d, c->dim, c->form, A, xc, rhs[A], Lc.frhs[A]);
+    }
     vcycle_face(c, l + 1, Lc.frhs, Lc.fx, sm);
     for (int A = 3 - c->dim; A < 3; ++A)
       launch_face_prolong_add(c->st, L.d, Lc.d, c->dim, A, Lc.fx[A], cur[A]);
@@ -582,7 +606,12 @@ void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smooth
   } else {
     for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
     Level& Lc = c->lv[l + 1];
-    launch_cell_resid_restrict(c->st, L.d, Lc.d, c->dim, cur, rhs, Lc.crhs);
+    if (L.split_rr) {
+      launch_cell_res(c->st, L.d, c->dim, cur, rhs, L.cres);
+      launch_cell_restrict(c->st, L.d, Lc.d, c->dim, L.cres, Lc.crhs);
+    } else {
+      launch_cell_resid_restrict(c->st, L.d, Lc.d, c->dim, cur, rhs, Lc.crhs);
+    }
     vcycle_cell(c, l + 1, Lc.crhs, Lc.cx, sm);
     launch_cell_prolong_add(c->st, L.d, Lc.d, c->dim, Lc.cx, cur);
     for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);

@@ -281,3 +281,37 @@ def test_fused_two_colour_sweeps_vs_oracle(cells, bc, form, theta):
     wy = y.copy()
     O.sweep_cell(geo, oc, wy, yr, O.diag_cell(geo, oc), 1.0)
     assert relerr(gy.data, wy) <= 1e-13
+
+
+@pytest.mark.parametrize("cells,bc", [((16, 16, 24), "pp pp pp"), ((16, 24, 32), "nn pp pp"),
+                                      ((24, 16, 16), "pp nn ff"), ((32, 48), "pp nn"), ((24, 16), "fn nf")])
+@pytest.mark.parametrize("form,theta", [("stress", 0.0), ("laplacian", 0.4), ("stress_bulk", 1.0)])
+def test_split_residual_restriction_bit_identical(cells, bc, form, theta, monkeypatch):
+    """Residual field + restriction (large levels, SB_RR_SPLIT) == the fused
+    residual->restriction kernels, to the bit, through whole face and cell V-cycles."""
+    from paper_1308_4605_b200 import multigrid as MG
+    from paper_1308_4605_b200.grid import BoundaryCondition, CellField, FaceField, GridSpec
+    from paper_1308_4605_b200.operators import ViscousForm, make_coefficients
+    names = {"p": "periodic", "n": "no_slip", "f": "free_slip"}
+    pairs = [(names[x[0]], names[x[1]]) for x in bc.split()]
+    g = GridSpec(cells, 1.0 / cells[0], tuple((BoundaryCondition(a), BoundaryCondition(b)) for a, b in pairs))
+    rng = np.random.default_rng(sum(cells) + len(form))
+    rho, mu, gam = 0.5 + rng.random(cells), 0.5 + rng.random(cells), rng.random(cells)
+    c = make_coefficients(g, theta, CellField(g, rho), CellField(g, mu), CellField(g, gam), ViscousForm(form))
+    rf = FaceField(g, tuple(rng.standard_normal(g.face_shape(a)) for a in range(g.dim)))
+    for a in range(g.dim):
+        if not g.periodic(a):
+            rf.components[a][(slice(None),) * a + (0,)] = 0.0
+            rf.components[a][(slice(None),) * a + (-1,)] = 0.0
+    rc = CellField(g, rng.standard_normal(cells))
+    rc.data[...] -= rc.data.mean()
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("SB_RR_SPLIT", v)
+        h = MG.build_hierarchy(g, c)
+        vf = MG.vcycle(rf, h, MG.SmootherParams(), "face")
+        vc = MG.vcycle(rc, h, MG.SmootherParams(), "cell")
+        out[v] = ([np.array(x) for x in vf.components], np.array(vc.data))
+    for a in range(g.dim):
+        assert np.array_equal(out["1"][0][a], out["0"][0][a]), a
+    assert np.array_equal(out["1"][1], out["0"][1])
