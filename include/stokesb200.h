@@ -182,6 +182,13 @@ int sb_gmres_solve(sb_ctx* ctx, const sb_precond* pc, const sb_gmres* gc,
 int sb_num_levels(sb_ctx* ctx);
 int sb_level_cells(sb_ctx* ctx, int level, int* cells);
 
+/* 1 when the face rows of a level derive the edge viscosities from mu_cell
+ * (all-periodic level whose mu_edge equals the four-cell mean of
+ * operators.py:90-104 to 4e-15 relative, checked on every
+ * sb_set_coefficients; SB_MUE_DERIVED=0 disables), 0 when they read mu_edge,
+ * -1 on a bad level */
+int sb_mue_derived(sb_ctx* ctx, int level);
+
 /* download the coarsened coefficients of one level (multigrid.py:127-169) */
 int sb_get_level_coefficients(sb_ctx* ctx, int level, double* const* rho_face,
                               double* mu_cell, double* const* mu_edge, double* gamma_cell);

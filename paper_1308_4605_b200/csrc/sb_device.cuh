@@ -22,6 +22,7 @@ struct LevelDev {
   int dist0;         // axis 0 is slab-distributed: neighbours come from 2 ghost planes, no wrap
   int bclo[3], bchi[3];
   int s0, s1;        // strides of axes 0 and 1 (axis 2 is contiguous); boxes < 2^31 points
+  int mue_derived;   // mu_e equals edge_mean(mu_c) to roundoff on this level (checked at setup)
   double h, inv_h, inv_h2, theta;
   const double* mu_c;
   const double* gam_c;
@@ -58,6 +59,17 @@ __device__ __forceinline__ int dminus(const LevelDev& L, int c) {
 __device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + i); }
 
 __host__ __device__ constexpr int edge_of(int a, int b) { return 3 - a - b; }
+
+// Edge (3D) / node (2D) viscosity as the mean of the four cells around it,
+// averaged first along the lower axis of the edge plane, then the higher
+// (operators.py:90-104 average_cell_to_node_edge, :133-145 _avg_to_stagger,
+// periodic branch).  dlo / dhi: index offsets of the -1 neighbour along the
+// lower / higher axis (wraps applied).
+__device__ __forceinline__ double edge_mean(const double* mu, int i, int dlo, int dhi) {
+  const double a = 0.5 * (__ldg(mu + i) + __ldg(mu + i + dlo));
+  const double b = 0.5 * (__ldg(mu + i + dhi) + __ldg(mu + i + dlo + dhi));
+  return 0.5 * (a + b);
+}
 
 // (D u)(c) * h accumulated in axis order: ((d0 + d1) + d2)  (operators.py:182-188)
 template <int DIM, bool PA = false>
@@ -113,25 +125,58 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // NC: the u_B operands go through the read-only (non-coherent) path.  The
 // single-CTA coarse-level kernel updates u inside the launch and reads it
 // back after __syncthreads, so it instantiates NC = false (plain loads).
-template <int DIM, int A, bool PA = false, bool NC = true>
+// DE: the edge viscosities are derived from mu_c (edge_mean) instead of read
+// from the mu_e arrays -- only on all-periodic levels whose mu_e matched that
+// mean at setup (LevelDev::mue_derived); mu_c's neighbours come from L1/L2,
+// so the face row streams one coefficient array instead of three.
+template <int DIM, int A, bool PA = false, bool NC = true, bool DE = false>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
   int f;
   const int* ci;
   int dmA;
+  double mf, mfa;      // DE: mu_c at f, f - e_A (loaded once)
+  double me[3][2];     // DE: derived edge viscosities [B][hi edge]
   __device__ __forceinline__ GAcc(const LevelDev& L_, const double* const* u_, int f_, const int* ci_)
       : L(L_), u(u_), f(f_), ci(ci_) {
     dmA = (A == 0) ? dminus<0, PA>(L, ci[0]) : (A == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
+    if (DE) {
+      // every mu_c operand of the row loaded once: f, f-e_A, f-+e_B, f-+e_B-e_A
+      mf = ld(L.mu_c, f);
+      mfa = ld(L.mu_c, f + dmA);
+#pragma unroll
+      for (int B = 3 - DIM; B < 3; ++B) {
+        if (B == A) continue;
+        const int pB = B == 0 ? dplus<0, PA>(L, ci[0]) : (B == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
+        const int mB = B == 0 ? dminus<0, PA>(L, ci[0]) : (B == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
+        const double fbm = ld(L.mu_c, f + mB), fbma = ld(L.mu_c, f + mB + dmA);
+        const double fbp = ld(L.mu_c, f + pB), fbpa = ld(L.mu_c, f + pB + dmA);
+        // edge_mean order: lower plane axis first (see edge_mean)
+        if (A < B) {
+          me[B][0] = 0.5 * (0.5 * (mf + mfa) + 0.5 * (fbm + fbma));
+          me[B][1] = 0.5 * (0.5 * (fbp + fbpa) + 0.5 * (mf + mfa));
+        } else {
+          me[B][0] = 0.5 * (0.5 * (mf + fbm) + 0.5 * (mfa + fbma));
+          me[B][1] = 0.5 * (0.5 * (fbp + mf) + 0.5 * (fbpa + mfa));
+        }
+      }
+    }
   }
   template <int B>
   __device__ __forceinline__ int eB() const {
     return B == 0 ? dplus<0, PA>(L, ci[0]) : (B == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
   }
-  __device__ __forceinline__ double mu(bool lo) const { return ld(L.mu_c, lo ? f + dmA : f); }
+  __device__ __forceinline__ double mu(bool lo) const {
+    if (DE) return lo ? mfa : mf;
+    return ld(L.mu_c, lo ? f + dmA : f);
+  }
   __device__ __forceinline__ double gam(bool lo) const { return ld(L.gam_c, lo ? f + dmA : f); }
   template <int B>
-  __device__ __forceinline__ double mue(bool hi) const { return ld(L.mu_e[edge_of(A, B)], hi ? f + eB<B>() : f); }
+  __device__ __forceinline__ double mue(bool hi) const {
+    if (!DE) return ld(L.mu_e[edge_of(A, B)], hi ? f + eB<B>() : f);
+    return me[B][hi ? 1 : 0];
+  }
   template <int B>
   __device__ __forceinline__ double ub(bool hi, bool lowA) const {
     const int e = hi ? f + eB<B>() : f;
@@ -235,16 +280,16 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A, bool PA = false, bool NC = true>
+template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool DE = false>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
-  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC>(L, u, f, ci), ci, diag);
+  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE>(L, u, f, ci), ci, diag);
 }
 
-template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool CG = false>
+template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool CG = false, bool DE = false>
 __device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, int f, const int* ci,
                                            double& diag) {
-  return face_row_core<DIM, FORM, A, PA, NC>(L, gather_ua<DIM, A, PA, CG>(L, u[A], f, ci), u, f, ci, diag);
+  return face_row_core<DIM, FORM, A, PA, NC, DE>(L, gather_ua<DIM, A, PA, CG>(L, u[A], f, ci), u, f, ci, diag);
 }
 
 // beta = 1/rho_face accessor for the cell row: beta_a at the low face (c) or

@@ -101,7 +101,7 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 // same-colour faces couple through the wrap): phase 0 stores the new values in
 // tmp, phase 1 copies them in -- exactly the reference's compute-all-then-
 // update-masked order.
-template <int DIM, int FORM, int A, int PHASE, bool PA>
+template <int DIM, int FORM, int A, int PHASE, bool PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -122,7 +122,7 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
     }
     const double* uc[3] = {u.p[0], u.p[1], u.p[2]};
     double dg;
-    const double au = face_row<DIM, FORM, A, PA>(L, uc, f, ci, dg);
+    const double au = face_row<DIM, FORM, A, PA, true, false, DE>(L, uc, f, ci, dg);
     const double res = __ldg(rhs + f) - au;
     const double nv = uc[A][f] + omega * (res / dg);
     if (PHASE == 2) tmp[f] = nv;
@@ -525,7 +525,7 @@ __device__ __forceinline__ double grad_at(const LevelDev& L, const double* q, in
   return (__ldg(q + f) - __ldg(q + f + dm)) * L.inv_h;
 }
 
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, bool PA, bool DE>
 __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u, const double* p,
                                        double* out, const int* ci) {
   if (!in_face(L, A, ci)) return;
@@ -535,20 +535,20 @@ __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u
     return;
   }
   double dg;
-  const double au = face_row<DIM, FORM, A, PA>(L, u, f, ci, dg);
+  const double au = face_row<DIM, FORM, A, PA, true, false, DE>(L, u, f, ci, dg);
   out[f] = au + grad_at<A>(L, p, f, ci);
 }
 
-template <int DIM, int FORM, bool PA>
+template <int DIM, int FORM, bool PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_apply_M(LevelDev L, CPtr3 u, const double* __restrict__ p, Ptr3 out_u, double* __restrict__ out_p,
           Box b, unsigned total) {
   {
     int ci[3];
     if (!box_point(b, ci)) return;
-    if (DIM == 3) m_face<3, FORM, 0, PA>(L, u.p, p, out_u.p[0], ci);
-    m_face<DIM, FORM, 1, PA>(L, u.p, p, out_u.p[1], ci);
-    m_face<DIM, FORM, 2, PA>(L, u.p, p, out_u.p[2], ci);
+    if (DIM == 3) m_face<3, FORM, 0, PA, DE>(L, u.p, p, out_u.p[0], ci);
+    m_face<DIM, FORM, 1, PA, DE>(L, u.p, p, out_u.p[1], ci);
+    m_face<DIM, FORM, 2, PA, DE>(L, u.p, p, out_u.p[2], ci);
     if (in_cell(L, ci)) {
       const int c = lin(L, ci);
       out_p[c] = -(div_sum<DIM, PA>(L, u.p, c, ci) * L.inv_h);
@@ -597,7 +597,7 @@ k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Pt
 // residual->restriction's face_resid_at expression), for the split
 // residual / restriction path on large levels: one face row per thread at
 // full occupancy instead of the latency-bound marching kernels.
-template <int DIM, int FORM, bool PA>
+template <int DIM, int FORM, bool PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_face_res3(LevelDev L, CPtr3 x, CPtr3 rhs, Ptr3 out, Box b) {
   int ci[3];
@@ -608,9 +608,9 @@ k_face_res3(LevelDev L, CPtr3 x, CPtr3 rhs, Ptr3 out, Box b) {
     if (!in_face(L, A, ci) || is_wall_face(L, A, ci)) continue;
     double au;
     double dg;
-    if (A == 0) au = face_row<DIM, FORM, (DIM == 3 ? 0 : 1), PA>(L, x.p, f, ci, dg);
-    else if (A == 1) au = face_row<DIM, FORM, 1, PA>(L, x.p, f, ci, dg);
-    else au = face_row<DIM, FORM, 2, PA>(L, x.p, f, ci, dg);
+    if (A == 0) au = face_row<DIM, FORM, (DIM == 3 ? 0 : 1), PA, true, false, DE>(L, x.p, f, ci, dg);
+    else if (A == 1) au = face_row<DIM, FORM, 1, PA, true, false, DE>(L, x.p, f, ci, dg);
+    else au = face_row<DIM, FORM, 2, PA, true, false, DE>(L, x.p, f, ci, dg);
     out.p[A][f] = __ldg(rhs.p[A] + f) - au;
   }
 }
@@ -911,6 +911,31 @@ __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
       if (dg == 0.0) atomicOr(flags, 2);
     }
   }
+}
+
+// Does every edge (3D) / node (2D) viscosity of an all-periodic level equal
+// the four-cell mean of mu_c (edge_mean) to roundoff?  The reference builds
+// mu_e exactly that way (operators.py:90-104) and rescale multiplies both by
+// c (operators.py:532-550), so on the finest level they agree to a few ulp;
+// coarse levels inject mu_e (multigrid.py:150-169) and do not.  flag |= 1 on
+// any point further apart than 4e-15 relative.
+template <int DIM>
+__global__ void k_check_mue(LevelDev L, int* flag, Box b) {
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  const int i = lin(L, ci);
+  const int m0 = dminus<0, true>(L, ci[0]), m1 = dminus<1, true>(L, ci[1]), m2 = dminus<2, true>(L, ci[2]);
+  bool bad = false;
+#pragma unroll
+  for (int e = (DIM == 3 ? 0 : 0); e < (DIM == 3 ? 3 : 1); ++e) {
+    // edge plane axes (lo, hi) = the two axes other than e
+    const int dlo = e == 0 ? m1 : m0;
+    const int dhi = e == 2 ? m1 : m2;
+    const double d = edge_mean(L.mu_c, i, dlo, dhi);
+    const double v = __ldg(L.mu_e[e] + i);
+    bad |= !(fabs(d - v) <= 4e-15 * fabs(v));
+  }
+  if (bad) atomicOr(flag, 1);
 }
 
 __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned total) {
@@ -1828,6 +1853,8 @@ static int wave_grid(K kernel) {
 static bool all_periodic(const LevelDev& L) {
   return L.bclo[0] == BC_PER && L.bclo[1] == BC_PER && L.bclo[2] == BC_PER;
 }
+// all-periodic level whose edge viscosities are derived from mu_c (DE kernels)
+static bool derive_mue(const LevelDev& L) { return all_periodic(L) && L.mue_derived && !L.dist0; }
 
 static bool odd_periodic(const LevelDev& L, int dim) {
   for (int a = 3 - dim; a < 3; ++a)
@@ -1845,7 +1872,8 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
   const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    if (all_periodic(L)) k_face_colour<DIM, FM, A, 0, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    if (derive_mue(L)) k_face_colour<DIM, FM, A, 0, true, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    else if (all_periodic(L)) k_face_colour<DIM, FM, A, 0, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
     else k_face_colour<DIM, FM, A, 0, false><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
   } else {
     ++g_kernel_launches;
@@ -1860,6 +1888,10 @@ void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, in
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
   // the solver routes those levels through launch_face_colour_tmp below.
+  if (rowv_colour_supported(L, dim, form)) {
+    launch_face_colour_rv(s, L, form, A, u, rhsA, parity, omega);
+    return;
+  }
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
       if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega);
@@ -1988,13 +2020,19 @@ void launch_face_res3(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr
     b.hi[a] = L.n[a] - 1 + (L.bclo[a] != BC_PER ? 1 : 0);
   }
   if (dim == 2) b.hi[0] = 0;
-  const bool pa = all_periodic(L);
+  if (rowv_supported(L, dim, form)) {
+    launch_face_res3_rv(s, L, form, x, rhs, out);
+    return;
+  }
+  const bool pa = all_periodic(L), de = derive_mue(L);
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (pa) k_face_res3<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      if (de) k_face_res3<3, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      else if (pa) k_face_res3<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
       else k_face_res3<3, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
     } else {
-      if (pa) k_face_res3<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      if (de) k_face_res3<2, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      else if (pa) k_face_res3<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
       else k_face_res3<2, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
     }
   });
@@ -2119,10 +2157,17 @@ static Box full_box(const LevelDev& L) {
 void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 u, const double* p,
                     Ptr3 out_u, double* out_p) {
   ++g_kernel_launches;
+  if (rowv_supported(L, dim, form)) {
+    launch_apply_M_rv(s, L, form, u, p, out_u, out_p);
+    return;
+  }
   Box b = full_box(L);
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
-    if (all_periodic(L)) {
+    if (derive_mue(L)) {
+      if (dim == 3) k_apply_M<3, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+      else k_apply_M<2, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
+    } else if (all_periodic(L)) {
       if (dim == 3) k_apply_M<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
       else k_apply_M<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
     } else {
@@ -2235,6 +2280,13 @@ void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int
     if (dim == 3) k_check_diag<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
     else k_check_diag<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
   });
+}
+
+void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag) {
+  ++g_kernel_launches;
+  const Box b = cell_box(L);
+  if (dim == 3) k_check_mue<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flag, b);
+  else k_check_mue<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flag, b);
 }
 
 void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double v) {

@@ -56,6 +56,15 @@ void launch_face_wave(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u
                       double omega, const int* steps, int nsteps, int* ctr);
 void launch_cell_wave(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double omega,
                       const int* steps, int nsteps, int* ctr);
+// row-vector kernels for large all-periodic 3D levels (sb_rowv.cu; the callers
+// are launch_face_colour / launch_face_res3 / launch_apply_M, which count the launch)
+bool rowv_supported(const LevelDev& L, int dim, int form);         // residual field, apply_M
+bool rowv_colour_supported(const LevelDev& L, int dim, int form);  // colour passes (opt-in)
+void launch_face_colour_rv(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u, const double* rhsA,
+                           int parity, double omega);
+void launch_face_res3_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 rhs, Ptr3 out);
+void launch_apply_M_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 u, const double* p, Ptr3 out_u,
+                       double* out_p);
 // fused residual -> restriction (multigrid.py:403-406 + :177-233)
 void launch_face_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
                                 int form, int A, CPtr3 u, const double* rhsA, double* coarseA);
@@ -103,6 +112,8 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
                          const double* fine, double* coarse);
 void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag);
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags);
+// all-periodic level: flag |= 1 unless mu_e == edge_mean(mu_c) to roundoff everywhere
+void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag);
 // box utilities
 void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double v);
 void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, const double* sum,

@@ -1,0 +1,586 @@
+// sb_rowv.cu -- row-vector stencil kernels for large all-periodic 3D levels
+// (sm_100a): the face residual field of the split residual -> restriction
+// and apply_M (default), and the face colour passes (opt-in).
+//
+// The one-face-per-thread kernels (sb_kernels.cu) issue one load per stencil
+// operand; a colour pass reads every other face of a row, so each warp-wide
+// load touches four 128-B lines for 256 useful bytes, and the all-face
+// kernels evaluate three face rows per thread from ~70 separate loads.  Here
+// a warp owns a contiguous row segment and every operand ROW is read once,
+// contiguously: a colour pass maps lane t to the face pair (2t, 2t+1) of a
+// 64-face segment (one 16-B load per row), the all-face kernels map lane t to
+// face t of a 32-face segment; the +-1 neighbours along the contiguous axis
+// come from the neighbouring lane (__shfl), the segment ends from one
+// uniform-address load.  Each operand array contributes only the rows its
+// stencil touches (compile-time masks).  All loads are issued before any
+// shuffle (Rows::issue / finish) so they are in flight together.
+//
+// Measured (ncu, C5 256^3 finest level, tools/rv_ab.sh): residual field
+// 465 -> 426 us, apply_M 533 -> 490 us; the colour pass is NOT faster than
+// the per-face kernel with derived edge viscosities (173-195 vs 155-164 us:
+// 74-80 registers, 24 resident warps, latency bound), so it is opt-in
+// (SB_ROWV_COLOUR=1).
+//
+// The arithmetic is face_row_t (sb_device.cuh) on the same operand values,
+// in the same order: results are bit-identical to the per-face kernels
+// (tests/test_gpu_rowv.py).
+//
+// Scope: 3D, all axes periodic, no slab decomposition, LAPLACIAN / STRESS
+// forms, contiguous extent a multiple of 64 (rowv_supported).
+#include <cuda_runtime.h>
+#include <cstdlib>
+#include "sb_kernels.h"
+
+namespace sb {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int RT = 256;  // threads per CTA
+
+// ---- compile-time operand masks -------------------------------------------
+// A stencil operand at offset (o0, o1, o2) from the thread's face lives in
+// row r = (o0+1)*3 + (o1+1) of the 3x3 row neighbourhood (axes 0, 1), at
+// contiguous offset o2 in {-1, 0, +1}: bit r of Need.m / .c / .p.
+struct Need {
+  unsigned m, c, p;
+};
+__host__ __device__ constexpr int rix(int o0, int o1) { return (o0 + 1) * 3 + (o1 + 1); }
+__host__ __device__ constexpr Need add(Need n, int o0, int o1, int o2) {
+  const unsigned b = 1u << rix(o0, o1);
+  if (o2 < 0) n.m |= b;
+  else if (o2 > 0) n.p |= b;
+  else n.c |= b;
+  return n;
+}
+__host__ __device__ constexpr Need orn(Need a, Need b) { return Need{a.m | b.m, a.c | b.c, a.p | b.p}; }
+__host__ __device__ constexpr int e(int axis, int a) { return axis == a ? 1 : 0; }
+// f + sa e_A + sb e_B
+__host__ __device__ constexpr Need add2(Need n, int A, int sa, int B, int sb) {
+  return add(n, sa * e(0, A) + sb * e(0, B), sa * e(1, A) + sb * e(1, B), sa * e(2, A) + sb * e(2, B));
+}
+__host__ __device__ constexpr int oth1(int A) { return A == 0 ? 1 : 0; }
+__host__ __device__ constexpr int oth2(int A) { return A == 2 ? 1 : 2; }
+
+// u_A neighbourhood (UA7)
+__host__ __device__ constexpr Need need_ua(int A) {
+  Need n{0, 0, 0};
+  (void)A;
+  n = add(n, 0, 0, 0);
+  n = add(n, 1, 0, 0);
+  n = add(n, -1, 0, 0);
+  n = add(n, 0, 1, 0);
+  n = add(n, 0, -1, 0);
+  n = add(n, 0, 0, 1);
+  n = add(n, 0, 0, -1);
+  return n;
+}
+// mu_c: f, f - e_A; derived edges add f -+ e_B, f -+ e_B - e_A per tangent B
+__host__ __device__ constexpr Need need_mu(int A, bool DE) {
+  Need n{0, 0, 0};
+  n = add2(n, A, 0, A, 0);
+  n = add2(n, A, -1, A, 0);
+  if (DE) {
+    for (int k = 0; k < 2; ++k) {
+      const int B = k == 0 ? oth1(A) : oth2(A);
+      n = add2(n, A, 0, B, -1);
+      n = add2(n, A, -1, B, -1);
+      n = add2(n, A, 0, B, 1);
+      n = add2(n, A, -1, B, 1);
+    }
+  }
+  return n;
+}
+// stored edge viscosity mu_e(A,B): f and f + e_B
+__host__ __device__ constexpr Need need_mue(int A, int B) {
+  Need n{0, 0, 0};
+  n = add2(n, A, 0, B, 0);
+  n = add2(n, A, 0, B, 1);
+  return n;
+}
+// u_B cross terms of row A: f, f - e_A, f + e_B, f + e_B - e_A
+__host__ __device__ constexpr Need need_ub(int A, int B) {
+  Need n{0, 0, 0};
+  n = add2(n, A, 0, B, 0);
+  n = add2(n, A, -1, B, 0);
+  n = add2(n, A, 0, B, 1);
+  n = add2(n, A, -1, B, 1);
+  return n;
+}
+// what the face row of component A needs from u_X (X = 0, 1, 2)
+__host__ __device__ constexpr Need need_u(int A, int X, int FORM) {
+  if (X == A) return need_ua(A);
+  return FORM == F_LAP ? Need{0, 0, 0} : need_ub(A, X);
+}
+// (D u) at the cell of the thread (apply_M): u_X at f and f + e_X
+__host__ __device__ constexpr Need need_div(int X) {
+  Need n{0, 0, 0};
+  n = add2(n, X, 0, X, 0);
+  n = add2(n, X, 1, X, 0);
+  return n;
+}
+// grad p at face A: p at f and f - e_A
+__host__ __device__ constexpr Need need_grad(int A) {
+  Need n{0, 0, 0};
+  n = add2(n, A, 0, A, 0);
+  n = add2(n, A, -1, A, 0);
+  return n;
+}
+
+// ---- row loads ------------------------------------------------------------
+struct RowV {
+  double m, c, p;
+};
+
+// Per-thread geometry: the linear index of (i, j, s) (row start + segment
+// start), the wrapped row offsets for o0 / o1 = -1, 0, +1, and the segment.
+struct Seg {
+  int base;
+  int di[3], dj[3];
+  int t;    // lane
+  int k0;   // PAIR: own face of the pair (colour); ALL: 0
+  int wl;   // offset from a segment's first element to the wrapped element before it
+  int wr;   // offset from a segment's first element to the wrapped element after its end
+};
+
+template <int W>
+__device__ __forceinline__ Seg make_seg(const LevelDev& L, int i, int j, int s, int t, int k0) {
+  Seg g;
+  g.base = i * L.s0 + j * L.s1 + s;
+  g.di[0] = (i == 0 ? L.n[0] - 1 : -1) * L.s0;
+  g.di[1] = 0;
+  g.di[2] = (i == L.n[0] - 1 ? -(L.n[0] - 1) : 1) * L.s0;
+  g.dj[0] = (j == 0 ? L.n[1] - 1 : -1) * L.s1;
+  g.dj[1] = 0;
+  g.dj[2] = (j == L.n[1] - 1 ? -(L.n[1] - 1) : 1) * L.s1;
+  g.t = t;
+  g.k0 = k0;
+  g.wl = s == 0 ? L.n[2] - 1 : -1;
+  g.wr = s + W == L.n[2] ? -s : W;
+  return g;
+}
+
+// PAIR (colour passes): lane t reads faces (2t, 2t+1) of a 64-face segment
+// with one 16-B load; c is the face of colour k0, m / p its neighbours.
+// ALL: lane t reads face t of a 32-face segment.  NC: read-only path.
+template <bool PAIR, bool NC, bool NM, bool NP>
+__device__ __forceinline__ RowV load_row(const double* __restrict__ a, int rp, const Seg& g) {
+  // branch-free: every lane issues the segment-end load at the same (uniform)
+  // address -- one sector, one wavefront -- so the loads of all rows can be
+  // in flight together; only the end lane keeps the value
+  RowV r;
+  r.m = r.p = 0.0;
+  if (PAIR) {
+    const double2* q = reinterpret_cast<const double2*>(a + rp) + g.t;
+    const double2 v = NC ? __ldg(q) : *q;
+    const bool hi = g.k0 != 0;  // warp-uniform
+    r.c = hi ? v.y : v.x;
+    const double o = hi ? v.x : v.y;  // the pair's other face: m (hi) or p (lo)
+    if (NM || NP) {  // (unconditional in hi: keeps the loads hoistable)
+      const double nb = __shfl_sync(FULL, o, hi ? g.t + 1 : g.t - 1);
+      const int ei = rp + (hi ? g.wr : g.wl);
+      const double ev = NC ? __ldg(a + ei) : a[ei];
+      const double x = g.t == (hi ? 31 : 0) ? ev : nb;
+      r.m = hi ? o : x;
+      r.p = hi ? x : o;
+    } else {
+      r.m = hi ? o : 0.0;
+      r.p = hi ? 0.0 : o;
+    }
+  } else {
+    r.c = NC ? __ldg(a + rp + g.t) : a[rp + g.t];
+    if (NM) {
+      const double w = __shfl_up_sync(FULL, r.c, 1);
+      const double ev = NC ? __ldg(a + rp + g.wl) : a[rp + g.wl];
+      r.m = g.t == 0 ? ev : w;
+    }
+    if (NP) {
+      const double w = __shfl_down_sync(FULL, r.c, 1);
+      const double ev = NC ? __ldg(a + rp + g.wr) : a[rp + g.wr];
+      r.p = g.t == 31 ? ev : w;
+    }
+  }
+  return r;
+}
+
+// The rows of one operand array selected by the masks (M, C, P).
+template <unsigned M, unsigned C, unsigned P>
+struct Rows {
+  RowV r[9];
+  double2 v[9];  // raw loads: PAIR the 16-B pair, ALL v.x
+  double el[9], er[9];  // segment-end values (uniform-address loads)
+  // Phase 1: issue every load of the selected rows (no dependent work, so all
+  // rows of all operands can be in flight together)
+  template <bool PAIR, bool NC>
+  __device__ __forceinline__ void issue(const double* __restrict__ a, const Seg& g) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      if (((M | C | P) >> q) & 1u) {
+        const int rp = g.base + g.di[q / 3] + g.dj[q % 3];
+        const bool nm = (M >> q) & 1u, np = (P >> q) & 1u;
+        if (PAIR) {
+          const double2* qq = reinterpret_cast<const double2*>(a + rp) + g.t;
+          v[q] = NC ? __ldg(qq) : *qq;
+          if (nm || np) {
+            const int ei = rp + (g.k0 ? g.wr : g.wl);
+            el[q] = NC ? __ldg(a + ei) : a[ei];
+          }
+        } else {
+          v[q].x = NC ? __ldg(a + rp + g.t) : a[rp + g.t];
+          if (nm) el[q] = NC ? __ldg(a + rp + g.wl) : a[rp + g.wl];
+          if (np) er[q] = NC ? __ldg(a + rp + g.wr) : a[rp + g.wr];
+        }
+      }
+    }
+  }
+  // Phase 2: neighbours along the contiguous axis by warp shuffle
+  template <bool PAIR>
+  __device__ __forceinline__ void finish(const Seg& g) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      if (((M | C | P) >> q) & 1u) {
+        const bool nm = (M >> q) & 1u, np = (P >> q) & 1u;
+        RowV& o = r[q];
+        o.m = o.p = 0.0;
+        if (PAIR) {
+          const bool hi = g.k0 != 0;  // warp-uniform
+          o.c = hi ? v[q].y : v[q].x;
+          const double ot = hi ? v[q].x : v[q].y;  // the pair's other face: m (hi) or p (lo)
+          double x = 0.0;
+          if (nm || np) {
+            const double nb = __shfl_sync(FULL, ot, hi ? g.t + 1 : g.t - 1);
+            x = g.t == (hi ? 31 : 0) ? el[q] : nb;
+          }
+          o.m = hi ? ot : x;
+          o.p = hi ? x : ot;
+        } else {
+          o.c = v[q].x;
+          if (nm) {
+            const double w = __shfl_up_sync(FULL, o.c, 1);
+            o.m = g.t == 0 ? el[q] : w;
+          }
+          if (np) {
+            const double w = __shfl_down_sync(FULL, o.c, 1);
+            o.p = g.t == 31 ? er[q] : w;
+          }
+        }
+      }
+    }
+  }
+  template <bool PAIR, bool NC>
+  __device__ __forceinline__ void load(const double* __restrict__ a, const Seg& g) {
+    issue<PAIR, NC>(a, g);
+    finish<PAIR>(g);
+  }
+  // value at offset (o0, o1, o2)
+  __device__ __forceinline__ double at(int o0, int o1, int o2) const {
+    const RowV& v = r[rix(o0, o1)];
+    return o2 < 0 ? v.m : (o2 > 0 ? v.p : v.c);
+  }
+  // value at f + sa e_A + sb e_B
+  __device__ __forceinline__ double at2(int A, int sa, int B, int sb) const {
+    return at(sa * e(0, A) + sb * e(0, B), sa * e(1, A) + sb * e(1, B), sa * e(2, A) + sb * e(2, B));
+  }
+};
+
+#define SB_ROWS(name, need) Rows<(need).m, (need).c, (need).p> name
+
+// Operand values of the face row of component A, in face_row_t's accessor
+// interface (GAcc, sb_device.cuh).
+struct RAcc {
+  double mu_hi, mu_lo, rho_v;
+  double mue_v[3][2];     // [B][hi edge]
+  double ub_v[3][2][2];   // [B][hi][lowA]
+  __device__ __forceinline__ double mu(bool lo) const { return lo ? mu_lo : mu_hi; }
+  __device__ __forceinline__ double gam(bool) const { return 0.0; }
+  __device__ __forceinline__ double divh(bool) const { return 0.0; }
+  template <int B>
+  __device__ __forceinline__ double mue(bool hi) const { return mue_v[B][hi ? 1 : 0]; }
+  template <int B>
+  __device__ __forceinline__ double ub(bool hi, bool lowA) const { return ub_v[B][hi ? 1 : 0][lowA ? 1 : 0]; }
+  __device__ __forceinline__ double rho() const { return rho_v; }
+};
+
+// edge_mean (sb_device.cuh) on operand values: lower plane axis first
+__device__ __forceinline__ double emean(double i, double ilo, double ihi, double ilohi) {
+  const double a = 0.5 * (i + ilo);
+  const double b = 0.5 * (ihi + ilohi);
+  return 0.5 * (a + b);
+}
+
+// Fill UA7 + RAcc for component A from the loaded rows.  UR: rows of u_A;
+// UB1/UB2: rows of the tangential components (ascending axis); MU: mu_c;
+// E1/E2: stored mu_e(A,B) rows (unused when DE).
+template <int FORM, int A, bool DE, class UR, class UB1, class UB2, class MU, class E1, class E2>
+__device__ __forceinline__ void face_vals(const UR& ua, const UB1& u1, const UB2& u2, const MU& mu, const E1& e1,
+                                          const E2& e2, UA7& s, RAcc& acc) {
+  s.c = ua.at(0, 0, 0);
+  s.p[0] = ua.at(1, 0, 0);
+  s.m[0] = ua.at(-1, 0, 0);
+  s.p[1] = ua.at(0, 1, 0);
+  s.m[1] = ua.at(0, -1, 0);
+  s.p[2] = ua.at(0, 0, 1);
+  s.m[2] = ua.at(0, 0, -1);
+  acc.mu_hi = mu.at2(A, 0, A, 0);
+  acc.mu_lo = mu.at2(A, -1, A, 0);
+  acc.rho_v = 0.0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int B = k == 0 ? oth1(A) : oth2(A);
+    double lo, hi;
+    if (DE) {
+      const double f = acc.mu_hi, fa = acc.mu_lo;
+      const double fbm = mu.at2(A, 0, B, -1), fbma = mu.at2(A, -1, B, -1);
+      const double fbp = mu.at2(A, 0, B, 1), fbpa = mu.at2(A, -1, B, 1);
+      if (A < B) {
+        lo = emean(f, fa, fbm, fbma);
+        hi = emean(fbp, fbpa, f, fa);
+      } else {
+        lo = emean(f, fbm, fa, fbma);
+        hi = emean(fbp, f, fbpa, fa);
+      }
+    } else {
+      lo = k == 0 ? e1.at2(A, 0, B, 0) : e2.at2(A, 0, B, 0);
+      hi = k == 0 ? e1.at2(A, 0, B, 1) : e2.at2(A, 0, B, 1);
+    }
+    acc.mue_v[B][0] = lo;
+    acc.mue_v[B][1] = hi;
+    if (FORM != F_LAP) {
+      const double b00 = k == 0 ? u1.at2(A, 0, B, 0) : u2.at2(A, 0, B, 0);
+      const double b0a = k == 0 ? u1.at2(A, -1, B, 0) : u2.at2(A, -1, B, 0);
+      const double b10 = k == 0 ? u1.at2(A, 0, B, 1) : u2.at2(A, 0, B, 1);
+      const double b1a = k == 0 ? u1.at2(A, -1, B, 1) : u2.at2(A, -1, B, 1);
+      acc.ub_v[B][0][0] = b00;
+      acc.ub_v[B][0][1] = b0a;
+      acc.ub_v[B][1][0] = b10;
+      acc.ub_v[B][1][1] = b1a;
+    } else {
+      acc.ub_v[B][0][0] = acc.ub_v[B][0][1] = acc.ub_v[B][1][0] = acc.ub_v[B][1][1] = 0.0;
+    }
+  }
+}
+
+constexpr Need NONE{0, 0, 0};
+
+// ---- colour pass (multigrid.py:327-340; k_face_colour's expression) --------
+template <int FORM, int A, bool DE, int MINB>
+__global__ void __launch_bounds__(RT, MINB)
+k_face_colour_rv(LevelDev L, Ptr3 u, const double* __restrict__ rhs, int parity, double omega, int nseg) {
+  // a CTA = 8 warps on 8 consecutive rows j of one segment: the +-1 rows
+  // along axis 1 are shared through L1
+  const int t = threadIdx.x & 31;
+  const int nj = (L.n[1] + 7) >> 3;
+  const int seg = (int)blockIdx.x % nseg, rest = (int)blockIdx.x / nseg;
+  const int i = rest / nj, j = (rest - i * nj) * 8 + (threadIdx.x >> 5);
+  if (j >= L.n[1]) return;  // whole warps
+  const int k0 = (parity - i - j) & 1;
+  const Seg g = make_seg<64>(L, i, j, seg * 64, t, k0);
+  constexpr int B1 = oth1(A), B2 = oth2(A);
+  constexpr Need nua = need_ua(A), nb1 = need_u(A, B1, FORM), nb2 = need_u(A, B2, FORM);
+  constexpr Need nmu = need_mu(A, DE);
+  constexpr Need ne1 = DE ? NONE : need_mue(A, B1), ne2 = DE ? NONE : need_mue(A, B2);
+  SB_ROWS(ua, nua);
+  SB_ROWS(ub1, nb1);
+  SB_ROWS(ub2, nb2);
+  SB_ROWS(mu, nmu);
+  SB_ROWS(me1, ne1);
+  SB_ROWS(me2, ne2);
+  // u_A is relaxed in place: this pass writes only faces of colour k0, and the
+  // values used from u_A are the other colour (neighbours) or the thread's own
+  // face, so plain loads see no race on any value they use
+  ua.template issue<true, false>(u.p[A], g);
+  if (FORM != F_LAP) {
+    ub1.template issue<true, true>(u.p[B1], g);
+    ub2.template issue<true, true>(u.p[B2], g);
+  }
+  mu.template issue<true, true>(L.mu_c, g);
+  if (!DE) {
+    me1.template issue<true, true>(L.mu_e[edge_of(A, B1)], g);
+    me2.template issue<true, true>(L.mu_e[edge_of(A, B2)], g);
+  }
+  const int f = g.base + 2 * t + k0;
+  const double rhs_f = __ldg(rhs + f);
+  ua.template finish<true>(g);
+  if (FORM != F_LAP) {
+    ub1.template finish<true>(g);
+    ub2.template finish<true>(g);
+  }
+  mu.template finish<true>(g);
+  if (!DE) {
+    me1.template finish<true>(g);
+    me2.template finish<true>(g);
+  }
+  UA7 s;
+  RAcc acc;
+  face_vals<FORM, A, DE>(ua, ub1, ub2, mu, me1, me2, s, acc);
+  if (L.theta != 0.0) acc.rho_v = __ldg(L.rho_f[A] + f);
+  const int ci[3] = {i, j, seg * 64 + 2 * t + k0};
+  double dg;
+  const double au = face_row_t<3, FORM, A, true>(L, s, acc, ci, dg);
+  const double res = rhs_f - au;
+  u.p[A][f] = s.c + omega * (res / dg);
+}
+
+// ---- all faces: residual field (k_face_res3) and apply_M (k_apply_M) -------
+template <int FORM, bool DE, bool MODE_M, int MINB>
+__global__ void __launch_bounds__(RT, MINB)
+k_face_all_rv(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3 out, double* __restrict__ out_p,
+              int nseg) {
+  const int t = threadIdx.x & 31;
+  const int nj = (L.n[1] + 7) >> 3;
+  const int seg = (int)blockIdx.x % nseg, rest = (int)blockIdx.x / nseg;
+  const int i = rest / nj, j = (rest - i * nj) * 8 + (threadIdx.x >> 5);
+  if (j >= L.n[1]) return;
+  const Seg g = make_seg<32>(L, i, j, seg * 32, t, 0);
+  // union of the three face rows' (and the divergence's) operand rows
+  constexpr Need n0 = orn(orn(need_u(0, 0, FORM), need_u(1, 0, FORM)), orn(need_u(2, 0, FORM), MODE_M ? need_div(0) : NONE));
+  constexpr Need n1 = orn(orn(need_u(0, 1, FORM), need_u(1, 1, FORM)), orn(need_u(2, 1, FORM), MODE_M ? need_div(1) : NONE));
+  constexpr Need n2 = orn(orn(need_u(0, 2, FORM), need_u(1, 2, FORM)), orn(need_u(2, 2, FORM), MODE_M ? need_div(2) : NONE));
+  constexpr Need nmu = orn(need_mu(0, DE), orn(need_mu(1, DE), need_mu(2, DE)));
+  // stored mu_e arrays by normal axis e: edge (A,B) with e = 3-A-B
+  constexpr Need ne0 = DE ? NONE : orn(need_mue(1, 2), need_mue(2, 1));
+  constexpr Need ne1 = DE ? NONE : orn(need_mue(0, 2), need_mue(2, 0));
+  constexpr Need ne2 = DE ? NONE : orn(need_mue(0, 1), need_mue(1, 0));
+  constexpr Need np = MODE_M ? orn(need_grad(0), orn(need_grad(1), need_grad(2))) : NONE;
+  SB_ROWS(u0, n0);
+  SB_ROWS(u1, n1);
+  SB_ROWS(u2, n2);
+  SB_ROWS(mu, nmu);
+  SB_ROWS(e0, ne0);
+  SB_ROWS(e1, ne1);
+  SB_ROWS(e2, ne2);
+  SB_ROWS(pr, np);
+  u0.template issue<false, true>(x.p[0], g);
+  u1.template issue<false, true>(x.p[1], g);
+  u2.template issue<false, true>(x.p[2], g);
+  mu.template issue<false, true>(L.mu_c, g);
+  if (!DE) {
+    e0.template issue<false, true>(L.mu_e[0], g);
+    e1.template issue<false, true>(L.mu_e[1], g);
+    e2.template issue<false, true>(L.mu_e[2], g);
+  }
+  if (MODE_M) pr.template issue<false, true>(p, g);
+  u0.template finish<false>(g);
+  u1.template finish<false>(g);
+  u2.template finish<false>(g);
+  mu.template finish<false>(g);
+  if (!DE) {
+    e0.template finish<false>(g);
+    e1.template finish<false>(g);
+    e2.template finish<false>(g);
+  }
+  if (MODE_M) pr.template finish<false>(g);
+  const int f = g.base + t;
+  const int ci[3] = {i, j, seg * 32 + t};
+  UA7 s;
+  RAcc acc;
+  double dg;
+  // component 0: tangents 1, 2 -> mu_e normals 2 (edge (0,1)) and 1 (edge (0,2))
+  face_vals<FORM, 0, DE>(u0, u1, u2, mu, e2, e1, s, acc);
+  if (L.theta != 0.0) acc.rho_v = __ldg(L.rho_f[0] + f);
+  double a0 = face_row_t<3, FORM, 0, true>(L, s, acc, ci, dg);
+  // component 1: tangents 0, 2 -> edges (0,1) normal 2, (1,2) normal 0
+  face_vals<FORM, 1, DE>(u1, u0, u2, mu, e2, e0, s, acc);
+  if (L.theta != 0.0) acc.rho_v = __ldg(L.rho_f[1] + f);
+  double a1 = face_row_t<3, FORM, 1, true>(L, s, acc, ci, dg);
+  // component 2: tangents 0, 1 -> edges (0,2) normal 1, (1,2) normal 0
+  face_vals<FORM, 2, DE>(u2, u0, u1, mu, e1, e0, s, acc);
+  if (L.theta != 0.0) acc.rho_v = __ldg(L.rho_f[2] + f);
+  double a2 = face_row_t<3, FORM, 2, true>(L, s, acc, ci, dg);
+  if (MODE_M) {
+    // m_face: A u + G p; (G p)_A = (p(f) - p(f - e_A)) / h
+    out.p[0][f] = a0 + (pr.at(0, 0, 0) - pr.at(-1, 0, 0)) * L.inv_h;
+    out.p[1][f] = a1 + (pr.at(0, 0, 0) - pr.at(0, -1, 0)) * L.inv_h;
+    out.p[2][f] = a2 + (pr.at(0, 0, 0) - pr.at(0, 0, -1)) * L.inv_h;
+    // div_sum: ((d0 + d1) + d2)
+    double acc_d = u0.at(1, 0, 0) - u0.at(0, 0, 0);
+    acc_d = acc_d + (u1.at(0, 1, 0) - u1.at(0, 0, 0));
+    acc_d = acc_d + (u2.at(0, 0, 1) - u2.at(0, 0, 0));
+    out_p[f] = -(acc_d * L.inv_h);
+  } else {
+    out.p[0][f] = __ldg(rhs.p[0] + f) - a0;
+    out.p[1][f] = __ldg(rhs.p[1] + f) - a1;
+    out.p[2][f] = __ldg(rhs.p[2] + f) - a2;
+  }
+}
+
+int blocks_for(const LevelDev& L, int seglen) {
+  return L.n[0] * ((L.n[1] + 7) / 8) * (L.n[2] / seglen);
+}
+
+// read per launch: tests compare both paths in one process
+bool rowv_on() {  // SB_ROWV=0: per-face kernels everywhere
+  const char* e = std::getenv("SB_ROWV");
+  return !(e && e[0] == '0');
+}
+
+template <int FM, int A>
+void colour_rv_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, int parity, double omega) {
+  const int nseg = L.n[2] / 64;
+  const int nb = blocks_for(L, 64);
+  if (L.mue_derived) k_face_colour_rv<FM, A, true, 3><<<nb, RT, 0, s>>>(L, u, rhs, parity, omega, nseg);
+  else k_face_colour_rv<FM, A, false, 3><<<nb, RT, 0, s>>>(L, u, rhs, parity, omega, nseg);
+}
+
+}  // namespace
+
+// The colour passes stay on the per-face kernel (k_face_colour with derived
+// mu_e, 40 registers, 48 resident warps per SM): the row-vector colour pass
+// moves half the L1 wavefronts but needs 74-80 registers and is latency bound
+// (ncu, C5 256^3: 173-195 us vs 155-164 us per pass).
+// SB_ROWV_COLOUR=1 selects it.
+bool rowv_colour_on() {
+  const char* e = std::getenv("SB_ROWV_COLOUR");
+  return e && e[0] == '1';
+}
+
+bool rowv_supported(const LevelDev& L, int dim, int form) {
+  if (dim != 3 || form == F_BULK || L.dist0 || !rowv_on()) return false;
+  for (int a = 0; a < 3; ++a)
+    if (L.bclo[a] != BC_PER || L.n[a] < 2) return false;
+  return L.n[2] % 64 == 0;
+}
+
+bool rowv_colour_supported(const LevelDev& L, int dim, int form) {
+  return rowv_colour_on() && rowv_supported(L, dim, form);
+}
+
+void launch_face_colour_rv(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u, const double* rhsA,
+                           int parity, double omega) {
+  if (form == F_LAP) {
+    if (A == 0) colour_rv_t<F_LAP, 0>(s, L, u, rhsA, parity, omega);
+    else if (A == 1) colour_rv_t<F_LAP, 1>(s, L, u, rhsA, parity, omega);
+    else colour_rv_t<F_LAP, 2>(s, L, u, rhsA, parity, omega);
+  } else {
+    if (A == 0) colour_rv_t<F_STRESS, 0>(s, L, u, rhsA, parity, omega);
+    else if (A == 1) colour_rv_t<F_STRESS, 1>(s, L, u, rhsA, parity, omega);
+    else colour_rv_t<F_STRESS, 2>(s, L, u, rhsA, parity, omega);
+  }
+}
+
+template <bool MODE_M>
+static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 rhs, const double* p, Ptr3 out,
+                   double* out_p) {
+  const int nseg = L.n[2] / 32;
+  const int nb = blocks_for(L, 32);
+  const bool de = L.mue_derived != 0;
+  if (form == F_LAP) {
+    if (de) k_face_all_rv<F_LAP, true, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+    else k_face_all_rv<F_LAP, false, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+  } else {
+    if (de) k_face_all_rv<F_STRESS, true, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+    else k_face_all_rv<F_STRESS, false, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+  }
+}
+
+void launch_face_res3_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 rhs, Ptr3 out) {
+  all_rv<false>(s, L, form, x, rhs, nullptr, out, nullptr);
+}
+
+void launch_apply_M_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 u, const double* p, Ptr3 out_u,
+                       double* out_p) {
+  CPtr3 none{{nullptr, nullptr, nullptr}};
+  all_rv<true>(s, L, form, u, none, p, out_u, out_p);
+}
+
+}  // namespace sb

@@ -46,6 +46,7 @@ struct ArgErr : std::runtime_error {
   } while (0)
 
 constexpr int kMaxVec = 128;
+constexpr int kFlagInts = 64;  // dflags: 16 setup-check slots + one mu_e check flag per level
 
 struct Level {
   LevelDev d{};
@@ -1243,8 +1244,30 @@ void build_from_level0(sb_ctx* c) {
       for (int A = c->off; A < 3; ++A) launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2);
     }
     for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
+    // levels whose edge viscosities are the four-cell mean of mu_c: the face
+    // rows derive them instead of streaming mu_e (SB_MUE_DERIVED=0: never)
+    const bool derive_on = [] {  // read per upload: tests compare both paths in one process
+      const char* e = std::getenv("SB_MUE_DERIVED");
+      return !(e && e[0] == '0');
+    }();
+    const bool per_all = c->bc[0][0] == BC_PER && c->bc[1][0] == BC_PER && c->bc[2][0] == BC_PER;
+    const int nl = (int)c->lv.size();
+    if (derive_on && per_all) {
+      CK(cudaMemsetAsync(c->dflags + 16, 0, 4 * nl, c->st));
+      for (int l = 0; l < nl; ++l) launch_check_mue(c->st, c->lv[l].d, c->dim, c->dflags + 16 + l);
+    }
+    int hm[kFlagInts - 16];
     CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
+    if (derive_on && per_all) CK(cudaMemcpyAsync(hm, c->dflags + 16, 4 * nl, cudaMemcpyDeviceToHost, c->st));
     sync(c);
+    bool changed = false;
+    for (int l = 0; l < nl; ++l) {
+      const int d = (derive_on && per_all && hm[l] == 0) ? 1 : 0;
+      changed |= d != c->lv[l].d.mue_derived;
+      c->lv[l].d.mue_derived = d;
+    }
+    // the captured P^-1 graph holds the LevelDev kernel parameters
+    if (changed) drop_graph(c);
     c->flag_face = hf[0] & 1;
     c->flag_cell = (hf[0] >> 1) & 1;
     c->flag_rho = hf[2] & 1;
@@ -1311,7 +1334,7 @@ sb_ctx* sb_create(int dim, const int* cells, double h, const int* bc, int viscou
     }
     for (size_t l = 0; l < c->lv.size(); ++l) alloc_level(c, c->lv[l], l == 0);
     int* fl = nullptr;
-    CK(cudaMalloc(&fl, 16));
+    CK(cudaMalloc(&fl, 4 * kFlagInts));
     c->allocs.push_back(fl);
     c->dflags = fl;
     c->dpart = dalloc(c, (long long)(2 * kMaxVec + 2) * reduce_blocks());
@@ -1525,6 +1548,11 @@ int sb_gmres_solve(sb_ctx* c, const sb_precond* pc, const sb_gmres* gc, const sb
     return gmres(c, *pc, *gc, *sm, b_u, b_p, x_u, x_p, rows, max_rows, n_rows, status,
                  scalar_vcycles ? scalar_vcycles : &dummy);
   });
+}
+
+int sb_mue_derived(sb_ctx* c, int level) {
+  if (!c || level < 0 || level >= (int)c->lv.size()) return -1;
+  return c->lv[level].d.mue_derived;
 }
 
 int sb_num_levels(sb_ctx* c) { return (int)c->lv.size(); }

@@ -227,6 +227,12 @@ class DeviceContext:
     def num_levels(self) -> int:
         return self.lib.sb_num_levels(self.h)
 
+    def mue_derived(self, level: int = 0) -> bool:
+        """True when the face rows of ``level`` derive the edge viscosities from
+        mu_cell instead of reading mu_edge (all-periodic levels whose mu_edge is
+        the four-cell mean, operators.py:90-104)."""
+        return self.lib.sb_mue_derived(self.h, level) == 1
+
     def level_cells(self, level):
         import ctypes as C
         out = (C.c_int * 3)()

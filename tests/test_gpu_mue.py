@@ -1,0 +1,107 @@
+"""Edge viscosities derived from mu_cell on all-periodic levels.
+
+The face rows of an all-periodic level whose uploaded mu_edge equals the
+four-cell mean of mu_cell (operators.py:90-104) to 4e-15 relative compute the
+edge viscosities from mu_cell instead of streaming the three mu_edge arrays.
+Rescaled coefficients (operators.py:532-550) differ from that mean by a few
+ulp, so the operator changes at roundoff level only: the derived and the
+stored path must agree to 1e-13 (operators, one P^-1) and give the same GMRES
+iteration count with solutions within 1e-12; coefficient sets whose mu_edge is
+not the cell mean must keep the stored path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(name, n, derive, monkeypatch, edit=None):
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case = PR.make_case(name, n)
+    cs, rs, spec = PR.prepare(case)
+    if edit is not None:
+        cs = edit(cs)
+    monkeypatch.setenv("SB_MUE_DERIVED", "1" if derive else "0")
+    P = Preconditioner(cs, PrecondConfig(kind=P1))
+    monkeypatch.delenv("SB_MUE_DERIVED")
+    return case, cs, rs, P
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _pack(x):
+    from paper_1308_4605_b200.grid import pack_stokes
+    return pack_stokes(x)
+
+
+@pytest.mark.parametrize("name,n", [("C5", 32), ("C3", 64), ("C1", 64)])
+def test_derived_matches_stored(name, n, monkeypatch):
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    out = {}
+    for derive in (False, True):
+        case, cs, rs, P = _setup(name, n, derive, monkeypatch)
+        assert P.ctx.mue_derived(0) == derive
+        if name != "C1":  # variable mu: coarse levels inject mu_e (multigrid.py:150-169)
+            assert not P.ctx.mue_derived(1)
+        m = OPS.apply_M(rs, cs, ctx=P.ctx)
+        z = P.apply(rs)
+        gcfg = GmresConfig(restart=case.restart, max_iters=500, rtol=1e-9, track_true_residual=False)
+        x, hist = gmres_solve(rs, cs, None, gcfg, precond=P)
+        out[derive] = (_pack(m), _pack(z), _pack(x), hist.iterations, hist.status)
+        del P
+    (m0, z0, x0, i0, s0), (m1, z1, x1, i1, s1) = out[False], out[True]
+    assert _rel(m1, m0) <= 1e-13
+    assert _rel(z1, z0) <= 1e-13
+    assert s0 == s1 == "converged"
+    assert i1 == i0
+    assert _rel(x1, x0) <= 1e-12
+
+
+def test_constant_mu_derives_every_level(monkeypatch):
+    case, cs, rs, P = _setup("C1", 64, True, monkeypatch)
+    assert all(P.ctx.mue_derived(l) for l in range(P.ctx.num_levels()))
+
+
+def test_walls_and_foreign_edges_keep_stored_path(monkeypatch):
+    from dataclasses import replace
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200.grid import NodeEdgeField
+    # a wall-bounded level never derives
+    _, _, _, P = _setup("C4", 16, True, monkeypatch)
+    assert not P.ctx.mue_derived(0)
+    del P
+
+    # harmonic edge means: not the arithmetic cell mean -> stored path, and the
+    # operator is the one of the given mu_edge (oracle)
+    def harmonic(cs):
+        arrs = {k: 1.0 / (1.0 / v + 1e-3) for k, v in cs.mu_node_edge.arrays.items()}
+        return replace(cs, mu_node_edge=NodeEdgeField(cs.grid, arrs))
+
+    case, cs, rs, P = _setup("C5", 16, True, monkeypatch, edit=harmonic)
+    assert not P.ctx.mue_derived(0)
+    from oracle import stokes_oracle as O
+    g = case.grid
+    geo = O.Geo(g.cells, g.h, tuple((lo.value, hi.value) for lo, hi in g.bc))
+    oc = O.Coef(cs.theta, cs.rho_cell.data, list(cs.rho_face.components), cs.mu_cell.data,
+                dict(cs.mu_node_edge.arrays), cs.gamma_cell.data, "stress")
+    mu, mp = O.apply_M(geo, oc, list(rs.u.components), rs.p.data)
+    m = OPS.apply_M(rs, cs, ctx=P.ctx)
+    for a in range(3):
+        assert _rel(m.u.components[a], mu[a]) <= 1e-12
+
+    # one perturbed edge value also disables it
+    def one_off(cs):
+        arrs = {k: v.copy() for k, v in cs.mu_node_edge.arrays.items()}
+        k0 = sorted(arrs)[0]
+        arrs[k0][3, 4, 5] *= 1.0 + 1e-12
+        return replace(cs, mu_node_edge=NodeEdgeField(cs.grid, arrs))
+
+    _, _, _, P2 = _setup("C5", 16, True, monkeypatch, edit=one_off)
+    assert not P2.ctx.mue_derived(0)

@@ -1,0 +1,95 @@
+"""Row-vector kernels (sb_rowv.cu) vs the one-face-per-thread kernels.
+
+On all-periodic 3D levels whose contiguous extent is a multiple of 64 the face
+residual field and apply_M (and, opt-in, the colour passes) run as row-vector kernels
+(a warp per row segment, operand rows loaded once, +-1 neighbours by warp
+shuffle).  Same operands, same arithmetic order: the results must be
+bit-identical to the per-face kernels (SB_ROWV=0), with stored and with derived
+edge viscosities, for both viscous forms the kernels cover, at segment
+boundaries and periodic wraps (odd row counts, extents 64 and 128).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRIDS = [(64, 64, 64), (6, 10, 128), (4, 6, 64)]
+
+
+def _case(cells, form, derive, theta, monkeypatch):
+    from dataclasses import replace
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.operators import ViscousForm
+    case = PR.make_case("C5", cells)
+    cs, rs, spec = PR.prepare(case)
+    cs = replace(cs, viscous_form=ViscousForm(form), theta=theta)
+    monkeypatch.setenv("SB_MUE_DERIVED", "1" if derive else "0")
+    return case, cs, rs
+
+
+def _run(cells, form, derive, theta, rowv, monkeypatch):
+    from paper_1308_4605_b200 import multigrid as MG
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200.grid import FaceField
+    case, cs, rs = _case(cells, form, derive, theta, monkeypatch)
+    g = case.grid
+    monkeypatch.setenv("SB_ROWV", "1" if rowv else "0")
+    monkeypatch.setenv("SB_ROWV_COLOUR", "1" if rowv else "0")  # opt-in colour pass
+    ctx = OPS.DeviceContext(g, cs.viscous_form)
+    ctx.set_coefficients(cs)
+    assert ctx.mue_derived(0) == derive
+    hier = MG.MgHierarchy(ctx, cs)
+    rng = np.random.default_rng(7)
+    x = FaceField(g, tuple(rng.standard_normal(g.face_shape(a)) for a in range(3)))
+    out = {}
+    m = OPS.apply_M(rs, cs, ctx=ctx)
+    out["Mu"] = [c.copy() for c in m.u.components] + [m.p.data.copy()]
+    for omega in (1.0, 0.8):
+        y = MG.smooth(hier, 0, "face", x, rs.u, omega)
+        out[f"sm{omega}"] = [c.copy() for c in y.components]
+    if all(c % 2 == 0 and c >= 4 for c in cells):
+        rr = MG.residual_restrict(hier, 0, "face", x, rs.u)
+        out["rr"] = [c.copy() for c in rr.components]
+    ctx.close()
+    monkeypatch.delenv("SB_ROWV")
+    monkeypatch.delenv("SB_ROWV_COLOUR")
+    return out
+
+
+@pytest.mark.parametrize("cells", GRIDS, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("form,derive,theta", [("stress", True, 0.0), ("stress", False, 0.0),
+                                               ("laplacian", True, 0.0), ("stress", True, 3.5)])
+def test_rowv_bit_identical(cells, form, derive, theta, monkeypatch):
+    a = _run(cells, form, derive, theta, True, monkeypatch)
+    b = _run(cells, form, derive, theta, False, monkeypatch)
+    assert a.keys() == b.keys()
+    for k in a:
+        for u, v in zip(a[k], b[k]):
+            assert np.array_equal(u, v), k
+
+
+def test_rowv_gmres_matches_per_face(monkeypatch):
+    """Full C5-recipe solves at 64^3 (P^-1 graph captured per context): identical
+    iteration counts and solutions to the bit."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import pack_stokes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case = PR.make_case("C5", 64)
+    cs, rs, spec = PR.prepare(case)
+    res = {}
+    for rowv in ("1", "0"):
+        monkeypatch.setenv("SB_ROWV", rowv)
+        monkeypatch.setenv("SB_ROWV_COLOUR", rowv)
+        P = Preconditioner(cs, PrecondConfig(kind=P1))
+        P.set_graphs(False)  # drop a graph captured under the other setting
+        P.set_graphs(True)
+        x, h = gmres_solve(rs, cs, None, GmresConfig(restart=50, rtol=1e-9), precond=P)
+        res[rowv] = (pack_stokes(x), h.iterations, [r.resid_precond for r in h.entries])
+        del P
+    assert res["1"][1] == res["0"][1]
+    assert res["1"][2] == res["0"][2]
+    assert np.array_equal(res["1"][0], res["0"][0])

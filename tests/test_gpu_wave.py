@@ -15,6 +15,13 @@ from conftest import arr, cases, face, pkg_coeff, pkg_grid, relerr
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _stored_edge_viscosity(monkeypatch):
+    """The wave kernels (opt-in) read the stored mu_e arrays; compare them with
+    per-colour passes that do the same (no derived edge viscosities)."""
+    monkeypatch.setenv("SB_MUE_DERIVED", "0")
+
 NAMES = {"p": "periodic", "n": "no_slip", "f": "free_slip"}
 
 
