@@ -182,12 +182,17 @@ int sb_gmres_solve(sb_ctx* ctx, const sb_precond* pc, const sb_gmres* gc,
 int sb_num_levels(sb_ctx* ctx);
 int sb_level_cells(sb_ctx* ctx, int level, int* cells);
 
-/* 1 when the face rows of a level derive the edge viscosities from mu_cell
- * (all-periodic level whose mu_edge equals the four-cell mean of
- * operators.py:90-104 to 4e-15 relative, checked on every
- * sb_set_coefficients; SB_MUE_DERIVED=0 disables), 0 when they read mu_edge,
- * -1 on a bad level */
-int sb_mue_derived(sb_ctx* ctx, int level);
+/* Per-level operand specialisations chosen at sb_set_coefficients (bit mask;
+ * -1 on a bad level).  Both are exact restatements of the uploaded arrays:
+ *  SB_LEVEL_MUE_DERIVED: all-periodic level whose mu_edge equals the
+ *    four-cell mean of mu_cell (operators.py:90-104) to 4e-15 relative; the
+ *    face rows compute it instead of reading mu_edge (SB_MUE_DERIVED=0: off).
+ *  SB_LEVEL_CONST_RHO: every non-wall rho_face of the level is the same value;
+ *    the cell rows use its 1/rho instead of reading the 1/rho_face arrays
+ *    (bit-identical; SB_CONST_BETA=0: off). */
+#define SB_LEVEL_MUE_DERIVED 1
+#define SB_LEVEL_CONST_RHO 2
+int sb_level_flags(sb_ctx* ctx, int level);
 
 /* download the coarsened coefficients of one level (multigrid.py:127-169) */
 int sb_get_level_coefficients(sb_ctx* ctx, int level, double* const* rho_face,

@@ -24,7 +24,7 @@ STATUS = {0: "converged", 1: "breakdown", 2: "maxiter"}
 EXPORTS = (
     "sb_create", "sb_destroy", "sb_last_error", "sb_set_coefficients", "sb_apply_M",
     "sb_apply_A", "sb_apply_A_affine", "sb_homogenize", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
-    "sb_num_levels", "sb_mue_derived", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
+    "sb_num_levels", "sb_level_flags", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
     "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
@@ -81,7 +81,7 @@ _SIGS = {
                                  _PP, _P, _PP, _P, C.POINTER(HistoryRow), C.c_int,
                                  C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
     "sb_num_levels": (C.c_int, [_P]),
-    "sb_mue_derived": (C.c_int, [_P, C.c_int]),
+    "sb_level_flags": (C.c_int, [_P, C.c_int]),
     "sb_level_cells": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int)]),
     "sb_get_level_coefficients": (C.c_int, [_P, C.c_int, _PP, _P, _PP, _P]),
     "sb_smooth": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, _PP, _PP]),

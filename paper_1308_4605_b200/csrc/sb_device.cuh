@@ -23,6 +23,8 @@ struct LevelDev {
   int bclo[3], bchi[3];
   int s0, s1;        // strides of axes 0 and 1 (axis 2 is contiguous); boxes < 2^31 points
   int mue_derived;   // mu_e equals edge_mean(mu_c) to roundoff on this level (checked at setup)
+  int beta_const;    // every non-wall 1/rho_face of the level equals beta_val (checked at setup)
+  double beta_val;
   double h, inv_h, inv_h2, theta;
   const double* mu_c;
   const double* gam_c;
@@ -302,6 +304,12 @@ struct GBeta {
   __device__ __forceinline__ GBeta(const LevelDev& L_, int c_, const int* ci_) : L(L_), c(c_), ci(ci_) {}
   template <int AX>
   __device__ __forceinline__ double beta(bool hi) const {
+    // constant density (LevelDev::beta_const): the level's single 1/rho_face
+    // value, 0 on wall faces like the stored array -- no beta stream at all
+    if (L.beta_const) {
+      const bool wall = !perq<PA>(L, AX) && (hi ? ci[AX] == L.n[AX] - 1 : ci[AX] == 0);
+      return wall ? 0.0 : L.beta_val;
+    }
     return ld(L.beta_f[AX], hi ? c + dplus<AX, PA>(L, ci[AX]) : c);
   }
 };

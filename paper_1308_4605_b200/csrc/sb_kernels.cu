@@ -874,8 +874,10 @@ __global__ void k_coarsen_edge(LevelDev Lf, LevelDev Lc, int e, const double* __
   }
 }
 
+// beta = 1/rho_face (0 on wall faces); flag |= 1 on rho_face <= 0 (operators.py:209-210);
+// cflag |= 1 when a non-wall rho_face differs from *ref (the level is not constant-density)
 __global__ void k_beta(LevelDev L, int A, const double* __restrict__ rho, double* __restrict__ beta,
-                       int* flag, Box b, unsigned total) {
+                       int* flag, int* cflag, const double* ref, Box b, unsigned total) {
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -884,6 +886,7 @@ __global__ void k_beta(LevelDev L, int A, const double* __restrict__ rho, double
     if (!(r > 0.0)) atomicOr(flag, 1);
     const bool wall = L.bclo[A] != BC_PER && (ci[A] == 0 || ci[A] == L.n[A]);
     beta[f] = wall ? 0.0 : 1.0 / r;
+    if (cflag && !wall && !(r == __ldg(ref))) atomicOr(cflag, 1);
   }
 }
 
@@ -2264,11 +2267,12 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
   else k_coarsen_edge<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
 }
 
-void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag) {
+void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag,
+                 int* cflag, const double* ref) {
   Box b = cell_box(L);
   if (L.bclo[A] != BC_PER) b.hi[A] = L.n[A];
   const unsigned total = box_count(b);
-  k_beta<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, rho, beta, flag, b, total);
+  k_beta<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, rho, beta, flag, cflag, ref, b, total);
 }
 
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags) {

@@ -110,7 +110,9 @@ void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
                          const double* fine, double* coarse);
 void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int e,
                          const double* fine, double* coarse);
-void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag);
+// cflag (nullable): |= 1 unless every non-wall rho_face equals *ref (constant-density level)
+void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag,
+                 int* cflag = nullptr, const double* ref = nullptr);
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags);
 // all-periodic level: flag |= 1 unless mu_e == edge_mean(mu_c) to roundoff everywhere
 void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag);

@@ -46,7 +46,8 @@ struct ArgErr : std::runtime_error {
   } while (0)
 
 constexpr int kMaxVec = 128;
-constexpr int kFlagInts = 64;  // dflags: 16 setup-check slots + one mu_e check flag per level
+constexpr int kMaxLevels = 24;
+constexpr int kFlagInts = 16 + 2 * kMaxLevels;  // dflags: 16 setup-check slots + mu_e / constant-rho flags per level
 
 struct Level {
   LevelDev d{};
@@ -1236,12 +1237,22 @@ void build_from_level0(sb_ctx* c) {
         launch_coarsen_edge(c->st, F.d, C.d, 2, 0, F.mu_e[0], C.mu_e[0]);
       }
     }
-    upload_chains(c);
-    CK(cudaMemsetAsync(c->dflags, 0, 16, c->st));
+    CK(cudaMemsetAsync(c->dflags, 0, 4 * kFlagInts, c->st));
     int hf[4] = {0, 0, 0, 0};
-    for (size_t l = 0; l < c->lv.size(); ++l) {
+    const int nl = (int)c->lv.size();
+    if (nl > kMaxLevels) throw ArgErr(SB_EINVAL, "too many multigrid levels");
+    // constant-density levels (cflag slot 16 + kMaxLevels + l): the cell rows
+    // use one 1/rho_face value instead of streaming the d beta arrays.  The
+    // reference face: the first interior face of component `off`.
+    std::vector<double> href(nl, 0.0);
+    for (int l = 0; l < nl; ++l) {
       Level& L = c->lv[l];
-      for (int A = c->off; A < 3; ++A) launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2);
+      const int a0 = c->off;
+      const long long st0 = a0 == 0 ? L.d.s0 : (a0 == 1 ? L.d.s1 : 1);
+      const double* ref = L.rho_f[a0] + (c->bc[a0][0] != BC_PER ? st0 : 0);
+      for (int A = c->off; A < 3; ++A)
+        launch_beta(c->st, L.d, A, L.rho_f[A], L.beta_f[A], c->dflags + 2, c->dflags + 16 + kMaxLevels + l, ref);
+      CK(cudaMemcpyAsync(&href[l], ref, 8, cudaMemcpyDeviceToHost, c->st));
     }
     for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
     // levels whose edge viscosities are the four-cell mean of mu_c: the face
@@ -1251,23 +1262,30 @@ void build_from_level0(sb_ctx* c) {
       return !(e && e[0] == '0');
     }();
     const bool per_all = c->bc[0][0] == BC_PER && c->bc[1][0] == BC_PER && c->bc[2][0] == BC_PER;
-    const int nl = (int)c->lv.size();
-    if (derive_on && per_all) {
-      CK(cudaMemsetAsync(c->dflags + 16, 0, 4 * nl, c->st));
+    if (derive_on && per_all)
       for (int l = 0; l < nl; ++l) launch_check_mue(c->st, c->lv[l].d, c->dim, c->dflags + 16 + l);
-    }
     int hm[kFlagInts - 16];
     CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
-    if (derive_on && per_all) CK(cudaMemcpyAsync(hm, c->dflags + 16, 4 * nl, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(hm, c->dflags + 16, 4 * (kFlagInts - 16), cudaMemcpyDeviceToHost, c->st));
     sync(c);
+    const bool const_on = [] {  // SB_CONST_BETA=0: always stream the beta arrays
+      const char* e = std::getenv("SB_CONST_BETA");
+      return !(e && e[0] == '0');
+    }();
     bool changed = false;
     for (int l = 0; l < nl; ++l) {
-      const int d = (derive_on && per_all && hm[l] == 0) ? 1 : 0;
-      changed |= d != c->lv[l].d.mue_derived;
-      c->lv[l].d.mue_derived = d;
+      LevelDev& d = c->lv[l].d;
+      const int de = (derive_on && per_all && hm[l] == 0) ? 1 : 0;
+      const int bc = (const_on && hm[kMaxLevels + l] == 0 && href[l] > 0.0) ? 1 : 0;
+      const double bv = bc ? 1.0 / href[l] : 0.0;  // k_beta's expression
+      changed |= de != d.mue_derived || bc != d.beta_const || bv != d.beta_val;
+      d.mue_derived = de;
+      d.beta_const = bc;
+      d.beta_val = bv;
     }
-    // the captured P^-1 graph holds the LevelDev kernel parameters
+    // the captured P^-1 graph and the coarse chains hold the LevelDev values
     if (changed) drop_graph(c);
+    upload_chains(c);
     c->flag_face = hf[0] & 1;
     c->flag_cell = (hf[0] >> 1) & 1;
     c->flag_rho = hf[2] & 1;
@@ -1550,9 +1568,10 @@ int sb_gmres_solve(sb_ctx* c, const sb_precond* pc, const sb_gmres* gc, const sb
   });
 }
 
-int sb_mue_derived(sb_ctx* c, int level) {
+int sb_level_flags(sb_ctx* c, int level) {
   if (!c || level < 0 || level >= (int)c->lv.size()) return -1;
-  return c->lv[level].d.mue_derived;
+  const LevelDev& d = c->lv[level].d;
+  return (d.mue_derived ? SB_LEVEL_MUE_DERIVED : 0) | (d.beta_const ? SB_LEVEL_CONST_RHO : 0);
 }
 
 int sb_num_levels(sb_ctx* c) { return (int)c->lv.size(); }

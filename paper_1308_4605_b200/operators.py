@@ -227,11 +227,20 @@ class DeviceContext:
     def num_levels(self) -> int:
         return self.lib.sb_num_levels(self.h)
 
+    def level_flags(self, level: int = 0) -> int:
+        """sb_level_flags: bit 0 derived edge viscosities, bit 1 constant density."""
+        return int(self.lib.sb_level_flags(self.h, level))
+
     def mue_derived(self, level: int = 0) -> bool:
         """True when the face rows of ``level`` derive the edge viscosities from
         mu_cell instead of reading mu_edge (all-periodic levels whose mu_edge is
         the four-cell mean, operators.py:90-104)."""
-        return self.lib.sb_mue_derived(self.h, level) == 1
+        return self.level_flags(level) & 1 == 1
+
+    def beta_const(self, level: int = 0) -> bool:
+        """True when every non-wall rho_face of ``level`` is one value, so the
+        cell rows use a single 1/rho instead of the 1/rho_face arrays."""
+        return self.level_flags(level) & 2 == 2
 
     def level_cells(self, level):
         import ctypes as C

@@ -1,4 +1,5 @@
-"""Edge viscosities derived from mu_cell on all-periodic levels.
+"""Per-level operand specialisations: edge viscosities derived from
+mu_cell on all-periodic levels, and one 1/rho for constant-density levels.
 
 The face rows of an all-periodic level whose uploaded mu_edge equals the
 four-cell mean of mu_cell (operators.py:90-104) to 4e-15 relative compute the
@@ -105,3 +106,54 @@ def test_walls_and_foreign_edges_keep_stored_path(monkeypatch):
 
     _, _, _, P2 = _setup("C5", 16, True, monkeypatch, edit=one_off)
     assert not P2.ctx.mue_derived(0)
+
+
+# ---- constant density: one 1/rho for the cell rows (LevelDev::beta_const) ------
+
+
+def _precond_with_env(cs, env, monkeypatch):
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = Preconditioner(cs, PrecondConfig(kind=P1))
+    for k in env:
+        monkeypatch.delenv(k)
+    return P
+
+
+@pytest.mark.parametrize("name,n", [("C5", 32), ("C4", 16), ("C2", 32)])
+def test_const_density_bit_identical(name, n, monkeypatch):
+    """C5 (rho = 1) runs every level with the constant 1/rho; C4/C2 (variable rho)
+    keep the arrays.  A constant-rho copy of C4 (walls in z) also takes the
+    constant path; in every case P^-1 and the GMRES solve are identical to the
+    bit to the array path (SB_CONST_BETA=0)."""
+    from dataclasses import replace
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import CellField, pack_stokes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.operators import average_cell_to_faces
+    case = PR.make_case(name, n)
+    cs, rs, spec = PR.prepare(case)
+    variants = [cs]
+    if name != "C5":
+        g = case.grid
+        rho = CellField(g, np.full(g.cells, 2.5))
+        variants.append(replace(cs, rho_cell=rho, rho_face=average_cell_to_faces(rho)))
+    for k, c in enumerate(variants):
+        out = {}
+        for on in ("1", "0"):
+            P = _precond_with_env(c, {"SB_CONST_BETA": on}, monkeypatch)
+            const = [P.ctx.beta_const(l) for l in range(P.ctx.num_levels())]
+            if on == "0":
+                assert not any(const)
+            elif name == "C5" or k == 1:
+                assert all(const)
+            else:
+                assert not const[0]
+            z = P.apply(rs)
+            x, h = gmres_solve(rs, c, None, GmresConfig(restart=case.restart, rtol=1e-9), precond=P)
+            out[on] = (pack_stokes(z), pack_stokes(x), h.iterations)
+            del P
+        assert np.array_equal(out["1"][0], out["0"][0])
+        assert np.array_equal(out["1"][1], out["0"][1])
+        assert out["1"][2] == out["0"][2]
