@@ -729,7 +729,8 @@ template <int A>
 __device__ __forceinline__ void glue_face(const LevelDev& L, double* xu, const double* phi, const int* ci) {
   if (!in_face(L, A, ci) || is_wall_face(L, A, ci)) return;
   const int f = lin(L, ci);
-  xu[f] = xu[f] - grad_at<A>(L, phi, f, ci) * __ldg(L.beta_f[A] + f);
+  const double beta = L.beta_const ? L.beta_val : __ldg(L.beta_f[A] + f);  // non-wall face
+  xu[f] = xu[f] - grad_at<A>(L, phi, f, ci) * beta;
 }
 
 template <int DIM>
@@ -1474,15 +1475,20 @@ k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __re
 }
 
 // Gram variant, pass B: w' = w - sum_i d_i Q_i written to `out`, ||w'||^2 only
-// (one streaming read of the basis).
+// (one streaming read of the basis).  means (nullable): the null-space
+// projection of w deferred from P^-1 -- w - means[b] on the b-th block of
+// bb double2 (the k_box_sub_mean expression, so w' is unchanged to the bit).
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
-           const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+           const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials,
+           const double* __restrict__ means, long long bb) {
   __shared__ double acc[kThreads / 32];
   __shared__ double ds[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kThreads / 32) acc[threadIdx.x] = 0.0;
   for (int i = threadIdx.x; i < nv; i += blockDim.x) ds[i] = d[i];
+  const double m0 = means ? means[0] : 0.0, m1 = means ? means[1] : 0.0;
+  const double m2 = means ? means[2] : 0.0, m3 = means ? means[3] : 0.0;
   __syncthreads();
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* o2 = reinterpret_cast<double2*>(out);
@@ -1492,6 +1498,20 @@ k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double
     const bool ok0 = e < n2, ok1 = e1 < n2;
     double2 w0 = ok0 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
     double2 wv1 = ok1 ? __ldg(w2 + e1) : make_double2(0.0, 0.0);
+    if (means) {
+      const int b0 = (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
+      const int b1 = (e1 >= bb) + (e1 >= 2 * bb) + (e1 >= 3 * bb);
+      const double ma = b0 == 0 ? m0 : (b0 == 1 ? m1 : (b0 == 2 ? m2 : m3));
+      const double mb = b1 == 0 ? m0 : (b1 == 1 ? m1 : (b1 == 2 ? m2 : m3));
+      if (ok0) {
+        w0.x = w0.x - ma;
+        w0.y = w0.y - ma;
+      }
+      if (ok1) {
+        wv1.x = wv1.x - mb;
+        wv1.y = wv1.y - mb;
+      }
+    }
     for (int i = 0; i < nv; ++i) {
       const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
       const double2 a = ok0 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
@@ -2403,11 +2423,25 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
-                     double* out, long long n, double* partials) {
+                     double* out, long long n, double* partials, const double* means, long long block) {
   ++g_kernel_launches;
   static const int grid_b = wave_grid(k_dcgs_b_g);
   g_red_blocks_used = grid_b;
-  k_dcgs_b_g<<<grid_b, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+  k_dcgs_b_g<<<grid_b, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2);
+}
+
+__global__ void k_block_means(const double* __restrict__ sums, int4 slot, double inv_count, double* __restrict__ means) {
+  if (threadIdx.x == 0) {
+    means[0] = slot.x >= 0 ? sums[slot.x] * inv_count : 0.0;
+    means[1] = slot.y >= 0 ? sums[slot.y] * inv_count : 0.0;
+    means[2] = slot.z >= 0 ? sums[slot.z] * inv_count : 0.0;
+    means[3] = slot.w >= 0 ? sums[slot.w] * inv_count : 0.0;
+  }
+}
+
+void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* means) {
+  ++g_kernel_launches;
+  k_block_means<<<1, 32, 0, s>>>(sums, make_int4(slot[0], slot[1], slot[2], slot[3]), inv_count, means);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {

@@ -137,8 +137,13 @@ void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out
 // Gram-matrix variant of the delayed-reorthogonalisation passes
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                      const double* w, long long n, double* partials);
+// means (nullable): per-block values subtracted from w first (deferred null projection,
+// blocks of `block` elements, at most 4)
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
-                     double* out, long long n, double* partials);
+                     double* out, long long n, double* partials, const double* means = nullptr,
+                     long long block = 0);
+// means[b] = sums[slot[b]] * inv_count (0 where slot[b] < 0), b < 4
+void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* means);
 // delayed-reorthogonalisation Arnoldi passes (see sb_solver.cu gmres())
 void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                    const double* w, long long n, double* partials);

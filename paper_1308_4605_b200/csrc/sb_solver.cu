@@ -89,6 +89,10 @@ struct sb_ctx {
   double theta = 0.0;
   int flag_rho = 0, flag_face = 0, flag_cell = 0;
   std::vector<int> null_comps;  // internal axes
+  // null-space projection deferred from P^-1 into the Arnoldi pass B (pad-free
+  // all-periodic level 0 only: the pass subtracts per-block means from every
+  // element of a block, pads included)
+  bool defer_nulls = false;
   int* dflags = nullptr;
   double* dpart = nullptr;
   double* dsmall = nullptr;   // [h1 kMaxVec][h2 kMaxVec][misc 64][y kMaxVec]
@@ -724,7 +728,41 @@ void project_nulls(sb_ctx* c, double* x) {
   }
 }
 
-// x = P^{-1} r on level-0 vectors (all device, stream-ordered, graph-capturable)
+double* dmeans(sb_ctx* c) { return dmisc(c) + 32; }
+
+// The sums of project_nulls only, and the per-block means the deferred
+// subtraction uses (Arnoldi pass B or finish_projection); same slots.
+void project_sums(sb_ctx* c, double* x) {
+  const Level& L = c->lv[0];
+  const double ncell = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+  int slot[4] = {-1, -1, -1, -1};
+  block_sum(c, vpres(c, x), L.block, 0);
+  slot[c->dim] = 0;
+  int k = 1;
+  for (int A : c->null_comps) {
+    block_sum(c, vcomp(c, x, A), L.block, k);
+    slot[A - c->off] = k++;
+  }
+  launch_block_means(c->st, dmisc(c), slot, 1.0 / ncell, dmeans(c));
+}
+
+// the subtraction half of project_nulls, after project_sums (bit-identical result)
+void finish_projection(sb_ctx* c, double* x) {
+  if (!c->defer_nulls) return;
+  const Level& L = c->lv[0];
+  Box cb;
+  for (int a = 0; a < 3; ++a) {
+    cb.lo[a] = 0;
+    cb.hi[a] = L.d.n[a] - 1;
+  }
+  const double ncell = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+  launch_box_add_scalar(c->st, L.d, cb, vpres(c, x), dmisc(c) + 0, 1.0 / ncell);
+  int slot = 1;
+  for (int A : c->null_comps) launch_box_add_scalar(c->st, L.d, cb, vcomp(c, x, A), dmisc(c) + slot++, 1.0 / ncell);
+}
+
+// x = P^{-1} r on level-0 vectors (all device, stream-ordered, graph-capturable);
+// with defer_nulls the null-space means are computed but not yet subtracted
 void precond_dev(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm, double* r, double* x) {
   const Level& L = c->lv[0];
   const int d = c->dim, o = c->off;
@@ -798,7 +836,8 @@ void precond_dev(sb_ctx* c, const sb_precond& pc, const sb_smoother& sm, double*
     default:
       throw ArgErr(SB_EINVAL, "unknown preconditioner kind");
   }
-  project_nulls(c, x);
+  if (c->defer_nulls) project_sums(c, x);
+  else project_nulls(c, x);
 }
 
 void drop_graph(sb_ctx* c) {
@@ -963,6 +1002,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
   // z0 = P^{-1} b
   CK(cudaMemcpyAsync(c->vMv, c->vb, vl * 8, cudaMemcpyDeviceToDevice, c->st));
   precond_apply_graph(c, pc, sm);
+  finish_projection(c, c->vw);
   *vcyc += precond_cost(c, pc);
   CK(cudaMemcpyAsync(c->vz0, c->vw, vl * 8, cudaMemcpyDeviceToDevice, c->st));
   vec_norm2(c, c->vz0, 0);
@@ -1018,6 +1058,10 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     while (j < m && k < gc.max_iters) {
       apply_M_vec(c, V + (long long)j * vl, c->vMv);
       precond_apply_graph(c, pc, sm);
+      // the Gram pass B subtracts the deferred null-space means while it
+      // streams w (P^-1 M Q has zero means in exact arithmetic, so pass A's
+      // dots with the basis are unaffected); the other variants project here
+      if (!gram) finish_projection(c, c->vw);
       *vcyc += precond_cost(c, pc);
       ++k;
       double hn;
@@ -1051,7 +1095,8 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         if (gram) {
           launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
           launch_finalize(c->st, c->dpart, 2 * j + 2, dh1(c));
-          launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart);
+          launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart,
+                          c->defer_nulls ? dmeans(c) : nullptr, c->lv[0].block);
           launch_finalize(c->st, c->dpart, 1, dh2(c) + kMaxVec - 1);
           CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec) * 8, cudaMemcpyDeviceToHost, c->st));
           sync(c);
@@ -1152,6 +1197,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     // r = z0 - P^{-1} M x
     apply_M_vec(c, c->vx, c->vMv);
     precond_apply_graph(c, pc, sm);
+    finish_projection(c, c->vw);
     *vcyc += precond_cost(c, pc);
     launch_sub(c->st, c->vz0, c->vw, c->vt, vl);
     r = c->vt;
@@ -1351,6 +1397,14 @@ sb_ctx* sb_create(int dim, const int* cells, double h, const int* bc, int viscou
       }
     }
     for (size_t l = 0; l < c->lv.size(); ++l) alloc_level(c, c->lv[l], l == 0);
+    {
+      // pad-free level 0 (every axis periodic, contiguous extent a multiple of 4)
+      const Level& L0 = c->lv[0];
+      bool padfree = true;
+      for (int a = 0; a < 3; ++a) padfree &= c->bc[a][0] == BC_PER && L0.P[a] == L0.d.n[a];
+      const char* e = std::getenv("SB_DEFER_NULLS");
+      c->defer_nulls = padfree && !(e && e[0] == '0');
+    }
     int* fl = nullptr;
     CK(cudaMalloc(&fl, 4 * kFlagInts));
     c->allocs.push_back(fl);
@@ -1551,6 +1605,7 @@ int sb_precond_apply(sb_ctx* c, const sb_precond* pc, const sb_smoother* sm, con
     ensure_vectors(c);
     vec_in(c, r_u, r_p, c->vMv);
     precond_apply_graph(c, *pc, *sm);
+    finish_projection(c, c->vw);
     vec_out(c, c->vw, x_u, x_p);
     sync(c);
     if (scalar_vcycles) *scalar_vcycles += precond_cost(c, *pc);
