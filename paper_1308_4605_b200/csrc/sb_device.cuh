@@ -34,9 +34,17 @@ struct LevelDev {
 };
 
 __host__ __device__ __forceinline__ bool per(const LevelDev& L, int a) { return L.bclo[a] == BC_PER; }
-// PA: every axis of the level is periodic (compile-time) -> wall logic compiled out
-template <bool PA>
-__host__ __device__ __forceinline__ bool perq(const LevelDev& L, int a) { return PA || L.bclo[a] == BC_PER; }
+// PA (compile-time boundary pattern): 1 = every axis of the level is periodic
+// (wall logic compiled out), 0 = any boundary conditions (runtime checks),
+// 2 + m = only the axes in bit mask m may be walls (PA_W2: walls along the
+// contiguous axis 2 only -- C2's y and C4's z walls).
+constexpr int PA_W2 = 2 + 4;
+template <int PA>
+__host__ __device__ __forceinline__ bool perq(const LevelDev& L, int a) {
+  if (PA == 1) return true;
+  if (PA >= 2 && !(((PA - 2) >> a) & 1)) return true;
+  return L.bclo[a] == BC_PER;
+}
 
 template <int AX>
 __device__ __forceinline__ int stride(const LevelDev& L) {
@@ -45,17 +53,29 @@ __device__ __forceinline__ int stride(const LevelDev& L) {
 
 // index shift to the +1 / -1 neighbour along AX of coordinate c (periodic wrap)
 // periodic wrap along AX, except along a slab-distributed axis 0 (ghosts)
-template <int AX, bool PA = false>
+template <int AX, int PA = false>
 __device__ __forceinline__ bool wraps(const LevelDev& L) {
   return perq<PA>(L, AX) && !(AX == 0 && L.dist0);
 }
-template <int AX, bool PA = false>
+template <int AX, int PA = false>
 __device__ __forceinline__ int dplus(const LevelDev& L, int c) {
   return (wraps<AX, PA>(L) && c == L.n[AX] - 1) ? -(L.n[AX] - 1) * stride<AX>(L) : stride<AX>(L);
 }
-template <int AX, bool PA = false>
+template <int AX, int PA = false>
 __device__ __forceinline__ int dminus(const LevelDev& L, int c) {
   return (wraps<AX, PA>(L) && c == 0) ? (L.n[AX] - 1) * stride<AX>(L) : -stride<AX>(L);
+}
+
+// Programmatic dependent launch: the solve's kernels are
+// launched with programmatic stream serialization (launch_k, sb_kernels.h),
+// so a kernel's CTAs are scheduled while its predecessor drains.
+// griddepcontrol.wait holds them until the predecessor grid has completed and
+// its writes are visible; it must be the first, unconditional statement of
+// every kernel so the ordering stays transitive.  Then the kernel lets its
+// own dependent launch early.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ double ld(const double* p, int i) { return __ldg(p + i); }
@@ -74,7 +94,7 @@ __device__ __forceinline__ double edge_mean(const double* mu, int i, int dlo, in
 }
 
 // (D u)(c) * h accumulated in axis order: ((d0 + d1) + d2)  (operators.py:182-188)
-template <int DIM, bool PA = false>
+template <int DIM, int PA = false>
 __device__ __forceinline__ double div_sum(const LevelDev& L, const double* const* u, int c,
                                           const int* ci) {
   double acc = 0.0;
@@ -103,7 +123,7 @@ struct UA7 {
 template <bool CG>
 __device__ __forceinline__ double ldu(const double* p, int i) { return CG ? __ldcg(p + i) : p[i]; }
 
-template <int DIM, int A, bool PA = false, bool CG = false>
+template <int DIM, int A, int PA = false, bool CG = false>
 __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, int f, const int* ci) {
   UA7 s;
   s.c = ldu<CG>(ua, f);
@@ -127,11 +147,12 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // NC: the u_B operands go through the read-only (non-coherent) path.  The
 // single-CTA coarse-level kernel updates u inside the launch and reads it
 // back after __syncthreads, so it instantiates NC = false (plain loads).
-// DE: the edge viscosities are derived from mu_c (edge_mean) instead of read
-// from the mu_e arrays -- only on all-periodic levels whose mu_e matched that
-// mean at setup (LevelDev::mue_derived); mu_c's neighbours come from L1/L2,
-// so the face row streams one coefficient array instead of three.
-template <int DIM, int A, bool PA = false, bool NC = true, bool DE = false>
+// DE: the edge viscosities are derived from mu_c (edge_mean; on a wall the
+// two-cell boundary mean) instead of read from the mu_e arrays -- only on
+// levels whose mu_e matched that derivation at setup (LevelDev::mue_derived,
+// k_check_mue); mu_c's neighbours come from L1/L2, so the face row streams
+// one coefficient array instead of three.
+template <int DIM, int A, int PA = false, bool NC = true, bool DE = false>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
@@ -147,20 +168,29 @@ struct GAcc {
       // every mu_c operand of the row loaded once: f, f-e_A, f-+e_B, f-+e_B-e_A
       mf = ld(L.mu_c, f);
       mfa = ld(L.mu_c, f + dmA);
+      const double mA = 0.5 * (mf + mfa);  // lower-axis-first mean along A (both orders start so)
 #pragma unroll
       for (int B = 3 - DIM; B < 3; ++B) {
         if (B == A) continue;
         const int pB = B == 0 ? dplus<0, PA>(L, ci[0]) : (B == 1 ? dplus<1, PA>(L, ci[1]) : dplus<2, PA>(L, ci[2]));
         const int mB = B == 0 ? dminus<0, PA>(L, ci[0]) : (B == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
-        const double fbm = ld(L.mu_c, f + mB), fbma = ld(L.mu_c, f + mB + dmA);
-        const double fbp = ld(L.mu_c, f + pB), fbpa = ld(L.mu_c, f + pB + dmA);
-        // edge_mean order: lower plane axis first (see edge_mean)
-        if (A < B) {
-          me[B][0] = 0.5 * (0.5 * (mf + mfa) + 0.5 * (fbm + fbma));
-          me[B][1] = 0.5 * (0.5 * (fbp + fbpa) + 0.5 * (mf + mfa));
+        // wall along B: the boundary edge (jj = 0 / n_B) is the mean of the two
+        // cells on its side -- _avg_to_stagger copies the boundary cell, so both
+        // averaging orders reduce to 0.5 (mu_c(f) + mu_c(f - e_A))
+        const bool wB = !perq<PA>(L, B);
+        const bool wlo = wB && ci[B] == 0, whi = wB && ci[B] == L.n[B] - 1;
+        if (wlo) {
+          me[B][0] = mA;
         } else {
-          me[B][0] = 0.5 * (0.5 * (mf + fbm) + 0.5 * (mfa + fbma));
-          me[B][1] = 0.5 * (0.5 * (fbp + mf) + 0.5 * (fbpa + mfa));
+          const double fbm = ld(L.mu_c, f + mB), fbma = ld(L.mu_c, f + mB + dmA);
+          // edge_mean order: lower plane axis first (see edge_mean)
+          me[B][0] = A < B ? 0.5 * (mA + 0.5 * (fbm + fbma)) : 0.5 * (0.5 * (mf + fbm) + 0.5 * (mfa + fbma));
+        }
+        if (whi) {
+          me[B][1] = mA;
+        } else {
+          const double fbp = ld(L.mu_c, f + pB), fbpa = ld(L.mu_c, f + pB + dmA);
+          me[B][1] = A < B ? 0.5 * (0.5 * (fbp + fbpa) + mA) : 0.5 * (0.5 * (fbp + mf) + 0.5 * (fbpa + mfa));
         }
       }
     }
@@ -198,7 +228,7 @@ struct GAcc {
 // jj = cB, hi edge jj = cB+1) and the matching diagonal weight
 // (operators.py:267-300, 331-340; diag :424-434).  u_hi/u_lo are u_A on the
 // two sides of the edge along B.
-template <int FORM, int A, int B, bool PA, class ACC>
+template <int FORM, int A, int B, int PA, class ACC>
 __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int cB, bool hi_edge, double u_hi,
                                           double u_lo, double& flux, double& w) {
   const int nB = L.n[B];
@@ -223,7 +253,7 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int
   }
   ft = mue * ft;
   w = mue;
-  if (!PA && side >= 0) {
+  if (side >= 0) {  // only reachable on a wall axis
     const int kind = side == 0 ? L.bclo[B] : L.bchi[B];
     if (kind == BC_FREESLIP) {
       ft = 0.0;
@@ -238,7 +268,7 @@ __device__ __forceinline__ void tang_flux(const LevelDev& L, const ACC& acc, int
 // (A u)_A at unknown face f (coords ci) from the u_A neighbourhood s and the
 // accessor, plus the smoother diagonal of that row.
 // operators.py:303-360 (row form multigrid.py:343-383), diag operators.py:408-439.
-template <int DIM, int FORM, int A, bool PA, class ACC>
+template <int DIM, int FORM, int A, int PA, class ACC>
 __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, const ACC& acc, const int* ci,
                                              double& diag) {
   const double uf = s.c, up = s.p[A], um = s.m[A];
@@ -282,13 +312,13 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool DE = false>
+template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool DE = false>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
   return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE>(L, u, f, ci), ci, diag);
 }
 
-template <int DIM, int FORM, int A, bool PA = false, bool NC = true, bool CG = false, bool DE = false>
+template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool CG = false, bool DE = false>
 __device__ __forceinline__ double face_row(const LevelDev& L, const double* const* u, int f, const int* ci,
                                            double& diag) {
   return face_row_core<DIM, FORM, A, PA, NC, DE>(L, gather_ua<DIM, A, PA, CG>(L, u[A], f, ci), u, f, ci, diag);
@@ -296,7 +326,7 @@ __device__ __forceinline__ double face_row(const LevelDev& L, const double* cons
 
 // beta = 1/rho_face accessor for the cell row: beta_a at the low face (c) or
 // the high face (c + e_a, wrapped) of cell c.
-template <bool PA = false>
+template <int PA = false>
 struct GBeta {
   const LevelDev& L;
   int c;
@@ -316,7 +346,7 @@ struct GBeta {
 
 // (L_rho phi)(c) and its diagonal from the 7-point phi neighbourhood s
 // (operators.py:206-215, 396-405).
-template <int DIM, bool PA, class BA>
+template <int DIM, int PA, class BA>
 __device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, const BA& ba, const int* ci,
                                              double& diag) {
   const double pc = s.c;
@@ -349,13 +379,13 @@ __device__ __forceinline__ double cell_row_t(const LevelDev& L, const UA7& s, co
   return acc * L.inv_h;
 }
 
-template <int DIM, bool PA = false>
+template <int DIM, int PA = false>
 __device__ __forceinline__ double cell_row_core(const LevelDev& L, const UA7& s, int c, const int* ci,
                                                 double& diag) {
   return cell_row_t<DIM, PA>(L, s, GBeta<PA>(L, c, ci), ci, diag);
 }
 
-template <int DIM, bool PA = false, bool CG = false>
+template <int DIM, int PA = false, bool CG = false>
 __device__ __forceinline__ UA7 gather_cell(const LevelDev& L, const double* phi, int c, const int* ci) {
   UA7 s;
   s.c = ldu<CG>(phi, c);
@@ -370,7 +400,7 @@ __device__ __forceinline__ UA7 gather_cell(const LevelDev& L, const double* phi,
   return s;
 }
 
-template <int DIM, bool PA = false, bool CG = false>
+template <int DIM, int PA = false, bool CG = false>
 __device__ __forceinline__ double cell_row(const LevelDev& L, const double* phi, int c, const int* ci,
                                            double& diag) {
   return cell_row_core<DIM, PA>(L, gather_cell<DIM, PA, CG>(L, phi, c, ci), c, ci, diag);

@@ -14,6 +14,14 @@
 
 namespace sb {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -101,10 +109,11 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 // same-colour faces couple through the wrap): phase 0 stores the new values in
 // tmp, phase 1 copies them in -- exactly the reference's compute-all-then-
 // update-masked order.
-template <int DIM, int FORM, int A, int PHASE, bool PA, bool DE = false>
+template <int DIM, int FORM, int A, int PHASE, int PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
+  pdl_enter();
   const int off = (L.bclo[A] == BC_PER) ? 0 : 1;
   {
     int ci[3];
@@ -130,10 +139,11 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
   }
 }
 
-template <int DIM, int PHASE, bool PA>
+template <int DIM, int PHASE, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     const int tt = (int)(blockIdx.x * blockDim.x + threadIdx.x);
@@ -161,7 +171,7 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
 // residual -> restriction (multigrid.py:195-233, 177-182, 403-406)
 // ---------------------------------------------------------------------------
 
-template <int DIM, int FORM, int A, bool PA, bool NC = true>
+template <int DIM, int FORM, int A, int PA, bool NC = true>
 __device__ __forceinline__ double face_resid_at(const LevelDev& L, const double* const* u,
                                                 const double* rhs, const int* ci) {
   const int f = lin(L, ci);
@@ -172,7 +182,7 @@ __device__ __forceinline__ double face_resid_at(const LevelDev& L, const double*
 
 // Tangential 2^(d-1) mean of fine residuals at fine normal index fa, coarse
 // tangential indices in C (mean along B1 first, then B2: multigrid.py:112-119).
-template <int DIM, int FORM, int A, bool PA, bool NC = true>
+template <int DIM, int FORM, int A, int PA, bool NC = true>
 __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* const* u, const double* rhs,
                                               const int* C, int fa) {
   using O = Others<DIM, A>;
@@ -203,10 +213,11 @@ __device__ __forceinline__ double tmean_resid(const LevelDev& Lf, const double* 
 // Small levels: one thread per coarse face, all 3 (or 2D: 3) normal offsets
 // evaluated by that thread (fine residuals on odd normal planes computed twice;
 // parallelism matters more than redundancy below ~32^3).
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_rr_s(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
             Box cb, unsigned total) {
+  pdl_enter();
   int C[3];
   if (!box_point(cb, C)) return;
   double tv[3];
@@ -222,10 +233,11 @@ k_face_rr_s(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
 // Fused residual -> restriction, each fine residual evaluated once.
 // A == 2 (contiguous axis): lanes run along coarse K; t(2K-1) is the previous
 // lane's t(2K+1) (warp shuffle), lane 0 evaluates it itself.
-template <int DIM, int FORM, bool PA>
+template <int DIM, int FORM, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
             Box cb) {
+  pdl_enter();
   constexpr int A = 2;
   int C[3];
   C[2] = cb.lo[2] + (int)(blockIdx.x * blockDim.x + threadIdx.x);
@@ -247,10 +259,11 @@ k_face_rr_c(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
 
 // A in {0, 1}: lanes along coarse axis 2 (coalesced), each thread marches a
 // chunk of coarse indices along A, carrying t(2C+1) into the next t(2C-1).
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, double* __restrict__ coarse,
             Box cb, int chunk) {
+  pdl_enter();
   constexpr int T = (A == 0) ? 1 : 0;  // the other non-contiguous axis
   int C[3];
   C[2] = cb.lo[2] + (int)(blockIdx.x * blockDim.x + threadIdx.x);
@@ -277,7 +290,7 @@ k_face_rr_m(LevelDev Lf, LevelDev Lc, CPtr3 u, const double* __restrict__ rhs, d
   }
 }
 
-template <int DIM, bool PA, bool NC = true>
+template <int DIM, int PA, bool NC = true>
 __device__ __forceinline__ double cell_resid_at(const LevelDev& L, const double* phi,
                                                 const double* rhs, const int* ci) {
   const int c = lin(L, ci);
@@ -287,7 +300,7 @@ __device__ __forceinline__ double cell_resid_at(const LevelDev& L, const double*
 }
 
 // mean of the 2^d fine residuals of coarse cell C (multigrid.py:177-182)
-template <int DIM, bool PA, bool NC = true>
+template <int DIM, int PA, bool NC = true>
 __device__ __forceinline__ double cell_rr_at(const LevelDev& Lf, const double* phi, const double* rhs,
                                              const int* C) {
   if (DIM == 3) {
@@ -315,10 +328,11 @@ __device__ __forceinline__ double cell_rr_at(const LevelDev& Lf, const double* p
   return 0.5 * (q[0] + q[1]);
 }
 
-template <int DIM, bool PA>
+template <int DIM, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_rr(LevelDev Lf, LevelDev Lc, const double* phi, const double* __restrict__ rhs,
           double* __restrict__ coarse, Box cb, unsigned total) {
+  pdl_enter();
   int C[3];
   if (!box_point(cb, C)) return;
   coarse[lin(Lc, C)] = cell_rr_at<DIM, PA>(Lf, phi, rhs, C);
@@ -414,6 +428,7 @@ __device__ __forceinline__ void tang_nbrs(const LevelDev& Lc, int ax, int J, int
 template <int DIM, int A>
 __global__ void __launch_bounds__(kThreads)
 k_face_pa8(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine, Box cb) {
+  pdl_enter();
   using O = Others<DIM, A>;
   int C[3];
   if (!box_point(cb, C)) return;
@@ -494,6 +509,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_pa(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* __restrict__ fine,
           Box fb, unsigned total) {
+  pdl_enter();
   int F[3];
   if (!box_point(fb, F)) return;
   cell_pa_at<DIM>(Lf, Lc, coarse, fine, F);
@@ -525,7 +541,7 @@ __device__ __forceinline__ double grad_at(const LevelDev& L, const double* q, in
   return (__ldg(q + f) - __ldg(q + f + dm)) * L.inv_h;
 }
 
-template <int DIM, int FORM, int A, bool PA, bool DE>
+template <int DIM, int FORM, int A, int PA, bool DE>
 __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u, const double* p,
                                        double* out, const int* ci) {
   if (!in_face(L, A, ci)) return;
@@ -539,10 +555,11 @@ __device__ __forceinline__ void m_face(const LevelDev& L, const double* const* u
   out[f] = au + grad_at<A>(L, p, f, ci);
 }
 
-template <int DIM, int FORM, bool PA, bool DE = false>
+template <int DIM, int FORM, int PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_apply_M(LevelDev L, CPtr3 u, const double* __restrict__ p, Ptr3 out_u, double* __restrict__ out_p,
           Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -584,6 +601,7 @@ template <int DIM, int FORM>
 __global__ void __launch_bounds__(kThreads)
 k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Ptr3 out, Box b,
                 unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -597,9 +615,10 @@ k_face_residual(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ q, Pt
 // residual->restriction's face_resid_at expression), for the split
 // residual / restriction path on large levels: one face row per thread at
 // full occupancy instead of the latency-bound marching kernels.
-template <int DIM, int FORM, bool PA, bool DE = false>
+template <int DIM, int FORM, int PA, bool DE = false>
 __global__ void __launch_bounds__(kThreads)
 k_face_res3(LevelDev L, CPtr3 x, CPtr3 rhs, Ptr3 out, Box b) {
+  pdl_enter();
   int ci[3];
   if (!box_point(b, ci)) return;
   const int f = lin(L, ci);
@@ -620,6 +639,7 @@ k_face_res3(LevelDev L, CPtr3 x, CPtr3 rhs, Ptr3 out, Box b) {
 template <int DIM, int A>
 __global__ void __launch_bounds__(kThreads)
 k_face_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* __restrict__ coarse, Box cb) {
+  pdl_enter();
   using O = Others<DIM, A>;
   int C[3];
   if (!box_point(cb, C)) return;
@@ -651,9 +671,10 @@ k_face_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* 
   coarse[lin(Lc, C)] = (0.25 * tv[0] + 0.5 * tv[1]) + 0.25 * tv[2];
 }
 
-template <int DIM, bool PA>
+template <int DIM, int PA>
 __global__ void __launch_bounds__(kThreads)
 k_cell_res(LevelDev L, const double* x, const double* __restrict__ rhs, double* __restrict__ out, Box b) {
+  pdl_enter();
   int ci[3];
   if (!box_point(b, ci)) return;
   out[lin(L, ci)] = cell_resid_at<DIM, PA>(L, x, rhs, ci);
@@ -663,6 +684,7 @@ k_cell_res(LevelDev L, const double* x, const double* __restrict__ rhs, double* 
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* __restrict__ coarse, Box cb) {
+  pdl_enter();
   int C[3];
   if (!box_point(cb, C)) return;
   double out;
@@ -696,6 +718,7 @@ k_cell_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ r, double* 
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_cell_residual(LevelDev L, const double* x, const double* rhs, double* out, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -710,6 +733,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_div_add(LevelDev L, CPtr3 u, const double* __restrict__ rp, double* __restrict__ out, Box b,
           unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -737,6 +761,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_p1_glue(LevelDev L, int form, Ptr3 xu, const double* __restrict__ phi, const double* __restrict__ bc,
           double* __restrict__ xp, double sign, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -754,6 +779,7 @@ k_p1_glue(LevelDev L, int form, Ptr3 xu, const double* __restrict__ phi, const d
 __global__ void __launch_bounds__(kThreads)
 k_schur(LevelDev L, int form, const double* __restrict__ r, const double* __restrict__ phi,
         double* __restrict__ out, double sign, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -780,6 +806,7 @@ __device__ __forceinline__ void subg_face(const LevelDev& L, const double* ru, c
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_face_sub_grad(LevelDev L, CPtr3 ru, const double* __restrict__ q, Ptr3 out, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -796,6 +823,7 @@ k_face_sub_grad(LevelDev L, CPtr3 ru, const double* __restrict__ q, Ptr3 out, Bo
 template <int DIM>
 __global__ void k_coarsen_cellmean(LevelDev Lf, LevelDev Lc, const double* __restrict__ fine,
                                    double* __restrict__ coarse, Box cb, unsigned total) {
+  pdl_enter();
   {
     int C[3];
     if (!box_point(cb, C)) return;
@@ -825,6 +853,7 @@ __global__ void k_coarsen_cellmean(LevelDev Lf, LevelDev Lc, const double* __res
 template <int DIM, int A>
 __global__ void k_coarsen_face(LevelDev Lf, LevelDev Lc, const double* __restrict__ fine,
                                double* __restrict__ coarse, Box cb, unsigned total) {
+  pdl_enter();
   using O = Others<DIM, A>;
   {
     int C[3];
@@ -857,6 +886,7 @@ __global__ void k_coarsen_face(LevelDev Lf, LevelDev Lc, const double* __restric
 template <int DIM>
 __global__ void k_coarsen_edge(LevelDev Lf, LevelDev Lc, int e, const double* __restrict__ fine,
                                double* __restrict__ coarse, Box cb, unsigned total) {
+  pdl_enter();
   {
     int C[3];
     if (!box_point(cb, C)) return;
@@ -879,6 +909,7 @@ __global__ void k_coarsen_edge(LevelDev Lf, LevelDev Lc, int e, const double* __
 // cflag |= 1 when a non-wall rho_face differs from *ref (the level is not constant-density)
 __global__ void k_beta(LevelDev L, int A, const double* __restrict__ rho, double* __restrict__ beta,
                        int* flag, int* cflag, const double* ref, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -903,6 +934,7 @@ __device__ __forceinline__ void chk_face(const LevelDev& L, const int* ci, int* 
 
 template <int DIM, int FORM>
 __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -917,25 +949,51 @@ __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
   }
 }
 
-// Does every edge (3D) / node (2D) viscosity of an all-periodic level equal
-// the four-cell mean of mu_c (edge_mean) to roundoff?  The reference builds
-// mu_e exactly that way (operators.py:90-104) and rescale multiplies both by
-// c (operators.py:532-550), so on the finest level they agree to a few ulp;
-// coarse levels inject mu_e (multigrid.py:150-169) and do not.  flag |= 1 on
-// any point further apart than 4e-15 relative.
+// The reference's edge (3D) / node (2D) viscosity at index ci of edge array e,
+// for any boundary conditions: _avg_to_stagger along the lower plane axis,
+// then the higher (operators.py:90-104, :133-145) -- periodic and interior
+// positions average 0.5 (x[j] + x[j-1]), a wall boundary copies its cell.
+template <int DIM>
+__device__ double edge_ref(const LevelDev& L, int e, const int* ci) {
+  const int al = DIM == 2 ? 1 : (e == 0 ? 1 : 0);
+  const int ah = DIM == 2 ? 2 : (e == 2 ? 1 : 2);
+  const bool pl = L.bclo[al] == BC_PER, ph = L.bclo[ah] == BC_PER;
+  const int jl = ci[al], jh = ci[ah], nl = L.n[al], nh = L.n[ah];
+  auto wrap = [](int j, int n) { return j < 0 ? j + n : j; };
+  auto cell = [&](int cl, int ch) {
+    int c[3] = {ci[0], ci[1], ci[2]};
+    c[al] = cl;
+    c[ah] = ch;
+    return __ldg(L.mu_c + lin(L, c));
+  };
+  auto arr1 = [&](int ch) {
+    if (!pl && jl == 0) return cell(0, ch);
+    if (!pl && jl == nl) return cell(nl - 1, ch);
+    return 0.5 * (cell(jl, ch) + cell(wrap(jl - 1, nl), ch));
+  };
+  if (!ph && jh == 0) return arr1(0);
+  if (!ph && jh == nh) return arr1(nh - 1);
+  return 0.5 * (arr1(jh) + arr1(wrap(jh - 1, nh)));
+}
+
+// Does every edge (3D) / node (2D) viscosity of a level equal edge_ref to
+// roundoff?  The reference builds mu_e exactly that way (operators.py:90-104)
+// and rescale multiplies both by c (operators.py:532-550), so on the finest
+// level they agree to a few ulp; coarse levels inject mu_e
+// (multigrid.py:150-169) and do not.  flag |= 1 on any edge further apart
+// than 4e-15 relative.  b: the cell box extended by one along wall axes.
 template <int DIM>
 __global__ void k_check_mue(LevelDev L, int* flag, Box b) {
+  pdl_enter();
   int ci[3];
   if (!box_point(b, ci)) return;
   const int i = lin(L, ci);
-  const int m0 = dminus<0, true>(L, ci[0]), m1 = dminus<1, true>(L, ci[1]), m2 = dminus<2, true>(L, ci[2]);
   bool bad = false;
 #pragma unroll
-  for (int e = (DIM == 3 ? 0 : 0); e < (DIM == 3 ? 3 : 1); ++e) {
-    // edge plane axes (lo, hi) = the two axes other than e
-    const int dlo = e == 0 ? m1 : m0;
-    const int dhi = e == 2 ? m1 : m2;
-    const double d = edge_mean(L.mu_c, i, dlo, dhi);
+  for (int e = 0; e < (DIM == 3 ? 3 : 1); ++e) {
+    const int ax = DIM == 2 ? 0 : e;  // the edge's own (cell-centred) axis
+    if (ci[ax] >= L.n[ax]) continue;
+    const double d = edge_ref<DIM>(L, e, ci);
     const double v = __ldg(L.mu_e[e] + i);
     bad |= !(fabs(d - v) <= 4e-15 * fabs(v));
   }
@@ -943,6 +1001,7 @@ __global__ void k_check_mue(LevelDev L, int* flag, Box b) {
 }
 
 __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -958,6 +1017,7 @@ __global__ void k_box_fill(LevelDev L, double* x, double v, Box b, unsigned tota
 // of A stay zero.  plane: C-order over the face extents of A with B dropped.
 __global__ void k_wall_tangent(LevelDev L, int A, int B, int side, const double* __restrict__ plane,
                                double* out, Box b, int e1, int e2) {
+  pdl_enter();
   int ci[3];
   if (!box_point(b, ci)) return;
   if (L.bclo[A] != BC_PER && (ci[A] == 0 || ci[A] == L.n[A])) return;
@@ -973,6 +1033,7 @@ __global__ void k_wall_tangent(LevelDev L, int A, int B, int side, const double*
 // block partials of sum(x) and sum(|x|) (homogenize's flux compatibility check)
 __global__ void __launch_bounds__(kThreads)
 k_sum_abs_partial(const double* __restrict__ x, long long n, double* __restrict__ partials, int stride) {
+  pdl_enter();
   __shared__ double acc[2][kThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double v = 0.0, va = 0.0;
@@ -1004,6 +1065,7 @@ k_sum_abs_partial(const double* __restrict__ x, long long n, double* __restrict_
 
 __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double inv_count, Box b,
                                unsigned total) {
+  pdl_enter();
   const double m = sum[0] * inv_count;
   {
     int ci[3];
@@ -1013,9 +1075,11 @@ __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double 
   }
 }
 
-__global__ void k_add_scalar(double* y, const double* x) { *y += *x; }
+__global__ void k_add_scalar(double* y, const double* x) {
+  pdl_enter(); *y += *x; }
 
 __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, Box b, unsigned total) {
+  pdl_enter();
   {
     int ci[3];
     if (!box_point(b, ci)) return;
@@ -1042,6 +1106,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void __launch_bounds__(kThreads)
 k_multi_dot(const double* __restrict__ V, long long vstride, int nv, const double* __restrict__ w,
             long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kMaxVec][kThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < nv * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
@@ -1075,6 +1140,7 @@ k_multi_dot(const double* __restrict__ V, long long vstride, int nv, const doubl
 __global__ void __launch_bounds__(kThreads)
 k_update_dot(const double* __restrict__ V, long long vstride, int nv, const double* __restrict__ h,
              double* __restrict__ w, long long n2, double* __restrict__ partials, int mode) {
+  pdl_enter();
   __shared__ double acc[kMaxVec][kThreads / 32];
   __shared__ double hs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1129,6 +1195,7 @@ k_update_dot(const double* __restrict__ V, long long vstride, int nv, const doub
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
          const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kMaxVec][kThreads / 32];
   __shared__ double cs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1182,6 +1249,7 @@ k_dcgs_a(double* __restrict__ Q, long long vstride, int k, const double* __restr
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
          const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kMaxVec + 1][kThreads / 32];
   __shared__ double ds[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1232,6 +1300,7 @@ constexpr int kStashThreads = 128;
 __global__ void __launch_bounds__(kStashThreads)
 k_dcgs_b_stash(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
                const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   extern __shared__ double2 stash[];  // [nv][kStashThreads]
   __shared__ double acc[kMaxVec + 1][kStashThreads / 32];
   __shared__ double ds[kMaxVec];
@@ -1277,6 +1346,7 @@ constexpr int kL2Blocks = kSMs * 2;
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_l2(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
             const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kMaxVec + 1][kThreads / 32];
   __shared__ double ds[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1342,6 +1412,7 @@ k_dcgs_b_l2(const double* __restrict__ Q, long long vstride, int nv, const doubl
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a_g(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1406,6 +1477,7 @@ template <int CH>
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
             const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1474,6 +1546,127 @@ k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __re
   }
 }
 
+// Butterfly transpose-reduction of V (power of two, <= 32) per-lane values
+// across the warp: V-1 + (5 - log2 V) shuffles instead of 5 V.  On return
+// v[0] of lane L holds the warp sum of value (L & (V-1)).
+template <int V>
+__device__ __forceinline__ double warp_sum_many(double* v, int lane) {
+#pragma unroll
+  for (int w = V, s = 1; w > 1; w >>= 1, s <<= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < w / 2; ++j) {
+      const double keep = up ? v[2 * j + 1] : v[2 * j];
+      const double send = up ? v[2 * j] : v[2 * j + 1];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int s = V; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);
+  return r;
+}
+
+// Pass A with the basis read G vectors at a time: G*CH independent 16-B loads
+// per thread in flight, and the 2G dot products of a group reduced across the
+// warp by one transpose-reduction (2G-1 + 5-log2(2G) shuffles instead of 10G).
+// q_j = (s - sum_i c_i Q_i) * inv_gamma keeps the ascending-i update order.
+template <int CH, int G, int MB = 2>
+__global__ void __launch_bounds__(kThreads, MB)
+k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+  pdl_enter();
+  __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nslot = 2 * k + 2;
+  for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long span = (long long)blockDim.x * CH;
+  for (long long base = blockIdx.x * span; base < n2; base += (long long)gridDim.x * span) {
+    double2 wv[CH], sv[CH], q[CH];
+    bool ok[CH];
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      const long long e = base + t * blockDim.x + threadIdx.x;
+      ok[t] = e < n2;
+      wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
+      q[t] = sv[t];
+    }
+    int i = 0;
+    for (; i + G <= k; i += G) {
+      double2 a[G][CH];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2* v2 = reinterpret_cast<const double2*>(Q + (i + g) * vstride);
+#pragma unroll
+        for (int t = 0; t < CH; ++t)
+          a[g][t] = ok[t] ? __ldg(v2 + base + t * blockDim.x + threadIdx.x) : make_double2(0.0, 0.0);
+      }
+      double dv[2 * G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double ci = cs[i + g];
+        double dw = 0.0, dsv = 0.0;
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+          q[t].x -= ci * a[g][t].x;
+          q[t].y -= ci * a[g][t].y;
+          dw += a[g][t].x * wv[t].x + a[g][t].y * wv[t].y;
+          dsv += a[g][t].x * sv[t].x + a[g][t].y * sv[t].y;
+        }
+        dv[2 * g] = dw;
+        dv[2 * g + 1] = dsv;
+      }
+      const double r = warp_sum_many<2 * G>(dv, lane);
+      if (lane < 2 * G) {
+        const int g = lane >> 1;
+        acc[(lane & 1) ? k + 1 + i + g : i + g][warp] += r;
+      }
+    }
+    for (; i < k; ++i) {
+      const double2* v2 = reinterpret_cast<const double2*>(Q + i * vstride);
+      double2 a[CH];
+#pragma unroll
+      for (int t = 0; t < CH; ++t) a[t] = ok[t] ? __ldg(v2 + base + t * blockDim.x + threadIdx.x) : make_double2(0.0, 0.0);
+      const double ci = cs[i];
+      double dv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        q[t].x -= ci * a[t].x;
+        q[t].y -= ci * a[t].y;
+        dv[0] += a[t].x * wv[t].x + a[t].y * wv[t].y;
+        dv[1] += a[t].x * sv[t].x + a[t].y * sv[t].y;
+      }
+      const double r = warp_sum_many<2>(dv, lane);
+      if (lane < 2) acc[lane ? k + 1 + i : i][warp] += r;
+    }
+    double dv[2] = {0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      if (k > 0) {
+        q[t].x *= inv_gamma;
+        q[t].y *= inv_gamma;
+        if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+      }
+      dv[0] += q[t].x * wv[t].x + q[t].y * wv[t].y;
+      dv[1] += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+    }
+    const double r = warp_sum_many<2>(dv, lane);
+    if (lane < 2) acc[lane ? 2 * k + 1 : k][warp] += r;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // Gram variant, pass B: w' = w - sum_i d_i Q_i written to `out`, ||w'||^2 only
 // (one streaming read of the basis).  means (nullable): the null-space
 // projection of w deferred from P^-1 -- w - means[b] on the b-th block of
@@ -1482,6 +1675,7 @@ __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
            const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials,
            const double* __restrict__ means, long long bb) {
+  pdl_enter();
   __shared__ double acc[kThreads / 32];
   __shared__ double ds[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1537,6 +1731,7 @@ k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double
 
 // out[i] = sum_b partials[i*kRedBlocks + b], fixed-order tree (deterministic)
 __global__ void k_finalize(const double* __restrict__ partials, double* __restrict__ out, int nblocks) {
+  pdl_enter();
   __shared__ double s[kThreads];
   const int i = blockIdx.x;
   double v = 0.0;
@@ -1552,6 +1747,7 @@ __global__ void k_finalize(const double* __restrict__ partials, double* __restri
 
 __global__ void __launch_bounds__(kThreads)
 k_sum_partial(const double* __restrict__ x, long long n, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double v = 0.0;
@@ -1571,6 +1767,7 @@ k_sum_partial(const double* __restrict__ x, long long n, double* __restrict__ pa
 __global__ void __launch_bounds__(kThreads)
 k_sub_norm(const double* __restrict__ a, const double* __restrict__ b, long long n,
            double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double acc[kThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double v = 0.0;
@@ -1591,6 +1788,7 @@ k_sub_norm(const double* __restrict__ a, const double* __restrict__ b, long long
 
 __global__ void __launch_bounds__(kThreads)
 k_scale_div(const double2* __restrict__ w, double d, double2* __restrict__ out, long long n2) {
+  pdl_enter();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n2;
        e += (long long)gridDim.x * blockDim.x) {
     double2 v = w[e];
@@ -1601,6 +1799,7 @@ k_scale_div(const double2* __restrict__ w, double d, double2* __restrict__ out, 
 __global__ void __launch_bounds__(kThreads)
 k_combo(double2* out, const double2* x, const double* __restrict__ V, long long vstride, int nv,
         const double* __restrict__ y, long long n2) {
+  pdl_enter();
   __shared__ double ys[kMaxVec];
   for (int i = threadIdx.x; i < nv; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
@@ -1619,6 +1818,7 @@ k_combo(double2* out, const double2* x, const double* __restrict__ V, long long 
 
 __global__ void __launch_bounds__(kThreads)
 k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out, long long n2) {
+  pdl_enter();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n2;
        e += (long long)gridDim.x * blockDim.x) {
     const double2 x = a[e], y = b[e];
@@ -1643,7 +1843,7 @@ __device__ __forceinline__ void cz_fill(double* x, long long n) {
 }
 
 // one colour pass of component A on chain level C (k_face_colour's mapping)
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, int PA>
 __device__ void cf_colour(const CoarseLv& C, double omega, int parity) {
   const LevelDev& L = C.d;
   const Box b = face_box(L, DIM, A);
@@ -1677,7 +1877,7 @@ __device__ void cf_colour(const CoarseLv& C, double omega, int parity) {
   }
 }
 
-template <int DIM, int FORM, int A, bool PA>
+template <int DIM, int FORM, int A, int PA>
 __device__ void cf_rr(const CoarseLv& F, const CoarseLv& Cc) {
   const Box cb = face_box(Cc.d, DIM, A);
   const int e1 = cb.hi[1] - cb.lo[1] + 1, e2 = cb.hi[2] - cb.lo[2] + 1;
@@ -1713,7 +1913,7 @@ __device__ void cf_pa(const CoarseLv& Cc, const CoarseLv& F) {
   }
 }
 
-template <int DIM, int FORM, bool PA>
+template <int DIM, int FORM, int PA>
 __device__ void cf_smooth(const CoarseLv& C, double omega, int sweeps) {
   for (int s = 0; s < sweeps; ++s) {
 #pragma unroll 1
@@ -1727,9 +1927,10 @@ __device__ void cf_smooth(const CoarseLv& C, double omega, int sweeps) {
   }
 }
 
-template <int DIM, int FORM, bool PA>
+template <int DIM, int FORM, int PA>
 __global__ void __launch_bounds__(kCoarseThreads, 1)
 k_coarse_face(const CoarseChain* __restrict__ gch, int sweeps_down, int sweeps_up, int bottom, double omega) {
+  pdl_enter();
   __shared__ CoarseChain ch;
   {
     const int* src = reinterpret_cast<const int*>(gch);
@@ -1762,7 +1963,7 @@ k_coarse_face(const CoarseChain* __restrict__ gch, int sweeps_down, int sweeps_u
   }
 }
 
-template <int DIM, bool PA>
+template <int DIM, int PA>
 __device__ void cc_smooth(const CoarseLv& C, double omega, int sweeps) {
   const LevelDev& L = C.d;
   const int e1 = L.n[1];
@@ -1798,9 +1999,10 @@ __device__ void cc_smooth(const CoarseLv& C, double omega, int sweeps) {
   }
 }
 
-template <int DIM, bool PA>
+template <int DIM, int PA>
 __global__ void __launch_bounds__(kCoarseThreads, 1)
 k_coarse_cell(const CoarseChain* __restrict__ gch, int sweeps_down, int sweeps_up, int bottom, double omega) {
+  pdl_enter();
   __shared__ CoarseChain ch;
   {
     const int* src = reinterpret_cast<const int*>(gch);
@@ -1876,8 +2078,21 @@ static int wave_grid(K kernel) {
 static bool all_periodic(const LevelDev& L) {
   return L.bclo[0] == BC_PER && L.bclo[1] == BC_PER && L.bclo[2] == BC_PER;
 }
-// all-periodic level whose edge viscosities are derived from mu_c (DE kernels)
-static bool derive_mue(const LevelDev& L) { return all_periodic(L) && L.mue_derived && !L.dist0; }
+// compile-time boundary pattern of a level (sb_device.cuh perq): 1 all
+// periodic, PA_W2 walls along axis 2 only, 0 anything else
+static int bc_pattern(const LevelDev& L) {
+  if (all_periodic(L)) return 1;
+  if (L.bclo[0] == BC_PER && L.bclo[1] == BC_PER) return PA_W2;
+  return 0;
+}
+#define SB_DISPATCH_PA(L, ...)                                     \
+  switch (bc_pattern(L)) {                                         \
+    case 1: { constexpr int PAT = 1; __VA_ARGS__; } break;         \
+    case PA_W2: { constexpr int PAT = PA_W2; __VA_ARGS__; } break; \
+    default: { constexpr int PAT = 0; __VA_ARGS__; } break;        \
+  }
+// level whose edge viscosities are derived from mu_c (DE kernels)
+static bool derive_mue(const LevelDev& L) { return L.mue_derived && !L.dist0; }
 
 static bool odd_periodic(const LevelDev& L, int dim) {
   for (int a = 3 - dim; a < 3; ++a)
@@ -1895,13 +2110,14 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
   const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    if (derive_mue(L)) k_face_colour<DIM, FM, A, 0, true, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
-    else if (all_periodic(L)) k_face_colour<DIM, FM, A, 0, true><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
-    else k_face_colour<DIM, FM, A, 0, false><<<g, kb, 0, s>>>(L, u, rhs, nullptr, parity, omega, b, half2, total);
+    SB_DISPATCH_PA(L, {
+      if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, PAT, true>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
+      else launch_k(k_face_colour<DIM, FM, A, 0, PAT>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
+    });
   } else {
     ++g_kernel_launches;
-    k_face_colour<DIM, FM, A, 2, false><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
-    k_face_colour<DIM, FM, A, 1, false><<<g, kb, 0, s>>>(L, u, rhs, tmp, parity, omega, b, half2, total);
+    launch_k(k_face_colour<DIM, FM, A, 2, false>, g, kb, 0, s, L, u, rhs, tmp, parity, omega, b, half2, total);
+    launch_k(k_face_colour<DIM, FM, A, 1, false>, g, kb, 0, s, L, u, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -1952,12 +2168,11 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
   const L3 c3 = cfg3(L.n[0], L.n[1], (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr) {
-    if (all_periodic(L)) k_cell_colour<DIM, 0, true><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
-    else k_cell_colour<DIM, 0, false><<<g, kb, 0, s>>>(L, phi, rhs, nullptr, parity, omega, b, half2, total);
+    SB_DISPATCH_PA(L, launch_k(k_cell_colour<DIM, 0, PAT>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total));
   } else {
     ++g_kernel_launches;
-    k_cell_colour<DIM, 2, false><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
-    k_cell_colour<DIM, 1, false><<<g, kb, 0, s>>>(L, phi, rhs, tmp, parity, omega, b, half2, total);
+    launch_k(k_cell_colour<DIM, 2, false>, g, kb, 0, s, L, phi, rhs, tmp, parity, omega, b, half2, total);
+    launch_k(k_cell_colour<DIM, 1, false>, g, kb, 0, s, L, phi, rhs, tmp, parity, omega, b, half2, total);
   }
 }
 
@@ -1983,8 +2198,8 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
   Box cb = face_box(Lc, DIM, A);
   const unsigned ncoarse = box_count(cb);
   if (ncoarse < 32768u) {  // small level: thread per coarse face
-    if (all_periodic(Lf)) k_face_rr_s<DIM, FM, A, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, ncoarse);
-    else k_face_rr_s<DIM, FM, A, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, ncoarse);
+    if (all_periodic(Lf)) launch_k(k_face_rr_s<DIM, FM, A, true>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, u, rhs, coarse, cb, ncoarse);
+    else launch_k(k_face_rr_s<DIM, FM, A, false>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, u, rhs, coarse, cb, ncoarse);
     return;
   }
   if (A == 2) {
@@ -1994,8 +2209,8 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
       b = dim3(32, kThreads / 32, 1);
       g = dim3((cb.hi[2] - cb.lo[2] + 32) / 32, (cb.hi[1] - cb.lo[1] + b.y) / b.y, cb.hi[0] - cb.lo[0] + 1);
     }
-    if (all_periodic(Lf)) k_face_rr_c<DIM, FM, true><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
-    else k_face_rr_c<DIM, FM, false><<<g, b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb);
+    if (all_periodic(Lf)) launch_k(k_face_rr_c<DIM, FM, true>, g, b, 0, s, Lf, Lc, u, rhs, coarse, cb);
+    else launch_k(k_face_rr_c<DIM, FM, false>, g, b, 0, s, Lf, Lc, u, rhs, coarse, cb);
   } else {
     constexpr int T = (A == 0) ? 1 : 0;
     const int e2 = cb.hi[2] - cb.lo[2] + 1;
@@ -2015,8 +2230,8 @@ static void face_rr_t(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, CP
     const int chunk = chunk_env > 0 ? std::min(chunk_env, eA) : (eA + nchunk - 1) / nchunk;
     nchunk = (eA + chunk - 1) / chunk;
     dim3 g(c3.g.x, c3.g.y, nchunk);
-    if (all_periodic(Lf)) k_face_rr_m<DIM, FM, A, true><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
-    else k_face_rr_m<DIM, FM, A, false><<<g, c3.b, 0, s>>>(Lf, Lc, u, rhs, coarse, cb, chunk);
+    if (all_periodic(Lf)) launch_k(k_face_rr_m<DIM, FM, A, true>, g, c3.b, 0, s, Lf, Lc, u, rhs, coarse, cb, chunk);
+    else launch_k(k_face_rr_m<DIM, FM, A, false>, g, c3.b, 0, s, Lf, Lc, u, rhs, coarse, cb, chunk);
   }
 }
 
@@ -2047,16 +2262,18 @@ void launch_face_res3(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr
     launch_face_res3_rv(s, L, form, x, rhs, out);
     return;
   }
-  const bool pa = all_periodic(L), de = derive_mue(L);
+  const bool de = derive_mue(L);
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (de) k_face_res3<3, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-      else if (pa) k_face_res3<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-      else k_face_res3<3, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      SB_DISPATCH_PA(L, {
+        if (de) launch_k(k_face_res3<3, FM, PAT, true>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b);
+        else launch_k(k_face_res3<3, FM, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b);
+      });
     } else {
-      if (de) k_face_res3<2, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-      else if (pa) k_face_res3<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-      else k_face_res3<2, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
+      SB_DISPATCH_PA(L, {
+        if (de) launch_k(k_face_res3<2, FM, PAT, true>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b);
+        else launch_k(k_face_res3<2, FM, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b);
+      });
     }
   });
 }
@@ -2066,12 +2283,12 @@ void launch_face_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc
   ++g_kernel_launches;
   Box cb = face_box(Lc, dim, A);
   if (dim == 3) {
-    if (A == 0) k_face_restrict<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
-    else if (A == 1) k_face_restrict<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
-    else k_face_restrict<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+    if (A == 0) launch_k(k_face_restrict<3, 0>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
+    else if (A == 1) launch_k(k_face_restrict<3, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
+    else launch_k(k_face_restrict<3, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
   } else {
-    if (A == 1) k_face_restrict<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
-    else k_face_restrict<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+    if (A == 1) launch_k(k_face_restrict<2, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
+    else launch_k(k_face_restrict<2, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
   }
 }
 
@@ -2079,22 +2296,16 @@ void launch_cell_res(cudaStream_t s, const LevelDev& L, int dim, const double* x
                      double* out) {
   ++g_kernel_launches;
   Box b = cell_box(L);
-  const bool pa = all_periodic(L);
-  if (dim == 3) {
-    if (pa) k_cell_res<3, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-    else k_cell_res<3, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-  } else {
-    if (pa) k_cell_res<2, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-    else k_cell_res<2, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b);
-  }
+  if (dim == 3) SB_DISPATCH_PA(L, launch_k(k_cell_res<3, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b))
+  else SB_DISPATCH_PA(L, launch_k(k_cell_res<2, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b))
 }
 
 void launch_cell_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, const double* r,
                           double* coarse) {
   ++g_kernel_launches;
   Box cb = cell_box(Lc);
-  if (dim == 3) k_cell_restrict<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
-  else k_cell_restrict<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, r, coarse, cb);
+  if (dim == 3) launch_k(k_cell_restrict<3>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
+  else launch_k(k_cell_restrict<2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, r, coarse, cb);
 }
 
 void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
@@ -2104,11 +2315,11 @@ void launch_cell_resid_restrict(cudaStream_t s, const LevelDev& Lf, const LevelD
   const unsigned total = box_count(cb);
   const bool pa = all_periodic(Lf);
   if (dim == 3) {
-    if (pa) k_cell_rr<3, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
-    else k_cell_rr<3, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+    if (pa) launch_k(k_cell_rr<3, true>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, phi, rhs, coarse, cb, total);
+    else launch_k(k_cell_rr<3, false>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, phi, rhs, coarse, cb, total);
   } else {
-    if (pa) k_cell_rr<2, true><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
-    else k_cell_rr<2, false><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, phi, rhs, coarse, cb, total);
+    if (pa) launch_k(k_cell_rr<2, true>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, phi, rhs, coarse, cb, total);
+    else launch_k(k_cell_rr<2, false>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, phi, rhs, coarse, cb, total);
   }
 }
 
@@ -2123,12 +2334,12 @@ void launch_face_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   }
   if (dim == 2) cb.hi[0] = 0;
   if (dim == 3) {
-    if (A == 0) k_face_pa8<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
-    else if (A == 1) k_face_pa8<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
-    else k_face_pa8<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
+    if (A == 0) launch_k(k_face_pa8<3, 0>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, coarseA, fineA, cb);
+    else if (A == 1) launch_k(k_face_pa8<3, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, coarseA, fineA, cb);
+    else launch_k(k_face_pa8<3, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, coarseA, fineA, cb);
   } else {
-    if (A == 1) k_face_pa8<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
-    else k_face_pa8<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, coarseA, fineA, cb);
+    if (A == 1) launch_k(k_face_pa8<2, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, coarseA, fineA, cb);
+    else launch_k(k_face_pa8<2, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, coarseA, fineA, cb);
   }
 }
 
@@ -2137,8 +2348,8 @@ void launch_cell_prolong_add(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   ++g_kernel_launches;
   Box fb = cell_box(Lf);
   const unsigned total = box_count(fb);
-  if (dim == 3) k_cell_pa<3><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
-  else k_cell_pa<2><<<cfg3(fb).g, cfg3(fb).b, 0, s>>>(Lf, Lc, coarse, fine, fb, total);
+  if (dim == 3) launch_k(k_cell_pa<3>, cfg3(fb).g, cfg3(fb).b, 0, s, Lf, Lc, coarse, fine, fb, total);
+  else launch_k(k_cell_pa<2>, cfg3(fb).g, cfg3(fb).b, 0, s, Lf, Lc, coarse, fine, fb, total);
 }
 
 void launch_coarse_face(cudaStream_t s, int dim, int form, bool pa, const CoarseChain* dchain,
@@ -2146,11 +2357,11 @@ void launch_coarse_face(cudaStream_t s, int dim, int form, bool pa, const Coarse
   ++g_kernel_launches;
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (pa) k_coarse_face<3, FM, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
-      else k_coarse_face<3, FM, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+      if (pa) launch_k(k_coarse_face<3, FM, true>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
+      else launch_k(k_coarse_face<3, FM, false>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
     } else {
-      if (pa) k_coarse_face<2, FM, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
-      else k_coarse_face<2, FM, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+      if (pa) launch_k(k_coarse_face<2, FM, true>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
+      else launch_k(k_coarse_face<2, FM, false>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
     }
   });
 }
@@ -2159,11 +2370,11 @@ void launch_coarse_cell(cudaStream_t s, int dim, bool pa, const CoarseChain* dch
                         int sweeps_up, int bottom, double omega) {
   ++g_kernel_launches;
   if (dim == 3) {
-    if (pa) k_coarse_cell<3, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
-    else k_coarse_cell<3, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    if (pa) launch_k(k_coarse_cell<3, true>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
+    else launch_k(k_coarse_cell<3, false>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
   } else {
-    if (pa) k_coarse_cell<2, true><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
-    else k_coarse_cell<2, false><<<1, kCoarseThreads, 0, s>>>(dchain, sweeps_down, sweeps_up, bottom, omega);
+    if (pa) launch_k(k_coarse_cell<2, true>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
+    else launch_k(k_coarse_cell<2, false>, 1, kCoarseThreads, 0, s, dchain, sweeps_down, sweeps_up, bottom, omega);
   }
 }
 
@@ -2187,16 +2398,15 @@ void launch_apply_M(cudaStream_t s, const LevelDev& L, int dim, int form, CPtr3 
   Box b = full_box(L);
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
-    if (derive_mue(L)) {
-      if (dim == 3) k_apply_M<3, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-      else k_apply_M<2, FM, true, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-    } else if (all_periodic(L)) {
-      if (dim == 3) k_apply_M<3, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-      else k_apply_M<2, FM, true><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-    } else {
-      if (dim == 3) k_apply_M<3, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-      else k_apply_M<2, FM, false><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, p, out_u, out_p, b, total);
-    }
+    SB_DISPATCH_PA(L, {
+      if (derive_mue(L)) {
+        if (dim == 3) launch_k(k_apply_M<3, FM, PAT, true>, cfg3(b).g, cfg3(b).b, 0, s, L, u, p, out_u, out_p, b, total);
+        else launch_k(k_apply_M<2, FM, PAT, true>, cfg3(b).g, cfg3(b).b, 0, s, L, u, p, out_u, out_p, b, total);
+      } else {
+        if (dim == 3) launch_k(k_apply_M<3, FM, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, u, p, out_u, out_p, b, total);
+        else launch_k(k_apply_M<2, FM, PAT>, cfg3(b).g, cfg3(b).b, 0, s, L, u, p, out_u, out_p, b, total);
+      }
+    });
   });
 }
 
@@ -2206,8 +2416,8 @@ void launch_face_residual(cudaStream_t s, const LevelDev& L, int dim, int form, 
   Box b = full_box(L);
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
-    if (dim == 3) k_face_residual<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, q, out, b, total);
-    else k_face_residual<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, q, out, b, total);
+    if (dim == 3) launch_k(k_face_residual<3, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, q, out, b, total);
+    else launch_k(k_face_residual<2, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, q, out, b, total);
   });
 }
 
@@ -2216,15 +2426,15 @@ void launch_cell_residual(cudaStream_t s, const LevelDev& L, int dim, const doub
   ++g_kernel_launches;
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_cell_residual<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b, total);
-  else k_cell_residual<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, rhs, out, b, total);
+  if (dim == 3) launch_k(k_cell_residual<3>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b, total);
+  else launch_k(k_cell_residual<2>, cfg3(b).g, cfg3(b).b, 0, s, L, x, rhs, out, b, total);
 }
 
 void launch_div_add(cudaStream_t s, const LevelDev& L, int dim, CPtr3 u, const double* rp, double* out) {
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_div_add<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, rp, out, b, total);
-  else k_div_add<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, u, rp, out, b, total);
+  if (dim == 3) launch_k(k_div_add<3>, cfg3(b).g, cfg3(b).b, 0, s, L, u, rp, out, b, total);
+  else launch_k(k_div_add<2>, cfg3(b).g, cfg3(b).b, 0, s, L, u, rp, out, b, total);
 }
 
 void launch_p1_glue(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 xu, const double* phi,
@@ -2232,8 +2442,8 @@ void launch_p1_glue(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 x
   ++g_kernel_launches;
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_p1_glue<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
-  else k_p1_glue<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, xu, phi, bc, xp, sign, b, total);
+  if (dim == 3) launch_k(k_p1_glue<3>, cfg3(b).g, cfg3(b).b, 0, s, L, form, xu, phi, bc, xp, sign, b, total);
+  else launch_k(k_p1_glue<2>, cfg3(b).g, cfg3(b).b, 0, s, L, form, xu, phi, bc, xp, sign, b, total);
 }
 
 void launch_schur(cudaStream_t s, const LevelDev& L, int form, const double* r, const double* phi,
@@ -2241,14 +2451,14 @@ void launch_schur(cudaStream_t s, const LevelDev& L, int form, const double* r, 
   ++g_kernel_launches;
   Box b = cell_box(L);
   const unsigned total = box_count(b);
-  k_schur<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, form, r, phi, out, sign, b, total);
+  launch_k(k_schur, cfg3(b).g, cfg3(b).b, 0, s, L, form, r, phi, out, sign, b, total);
 }
 
 void launch_face_sub_grad(cudaStream_t s, const LevelDev& L, int dim, CPtr3 ru, const double* q, Ptr3 out) {
   Box b = full_box(L);
   const unsigned total = box_count(b);
-  if (dim == 3) k_face_sub_grad<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, ru, q, out, b, total);
-  else k_face_sub_grad<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, ru, q, out, b, total);
+  if (dim == 3) launch_k(k_face_sub_grad<3>, cfg3(b).g, cfg3(b).b, 0, s, L, ru, q, out, b, total);
+  else launch_k(k_face_sub_grad<2>, cfg3(b).g, cfg3(b).b, 0, s, L, ru, q, out, b, total);
 }
 
 void launch_coarsen_cellmean(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim,
@@ -2256,8 +2466,8 @@ void launch_coarsen_cellmean(cudaStream_t s, const LevelDev& Lf, const LevelDev&
   ++g_kernel_launches;
   Box cb = cell_box(Lc);
   const unsigned total = box_count(cb);
-  if (dim == 3) k_coarsen_cellmean<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-  else k_coarsen_cellmean<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+  if (dim == 3) launch_k(k_coarsen_cellmean<3>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
+  else launch_k(k_coarsen_cellmean<2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
 }
 
 void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc, int dim, int A,
@@ -2267,12 +2477,12 @@ void launch_coarsen_face(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
   if (Lc.bclo[A] != BC_PER) cb.hi[A] = Lc.n[A];  // all faces incl. wall boundary
   const unsigned total = box_count(cb);
   if (dim == 3) {
-    if (A == 0) k_coarsen_face<3, 0><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else if (A == 1) k_coarsen_face<3, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else k_coarsen_face<3, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    if (A == 0) launch_k(k_coarsen_face<3, 0>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
+    else if (A == 1) launch_k(k_coarsen_face<3, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
+    else launch_k(k_coarsen_face<3, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
   } else {
-    if (A == 1) k_coarsen_face<2, 1><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
-    else k_coarsen_face<2, 2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, fine, coarse, cb, total);
+    if (A == 1) launch_k(k_coarsen_face<2, 1>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
+    else launch_k(k_coarsen_face<2, 2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, fine, coarse, cb, total);
   }
 }
 
@@ -2283,8 +2493,8 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
   for (int a = 3 - dim; a < 3; ++a)
     if (a != e && Lc.bclo[a] != BC_PER) cb.hi[a] = Lc.n[a];
   const unsigned total = box_count(cb);
-  if (dim == 3) k_coarsen_edge<3><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
-  else k_coarsen_edge<2><<<cfg3(cb).g, cfg3(cb).b, 0, s>>>(Lf, Lc, e, fine, coarse, cb, total);
+  if (dim == 3) launch_k(k_coarsen_edge<3>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, e, fine, coarse, cb, total);
+  else launch_k(k_coarsen_edge<2>, cfg3(cb).g, cfg3(cb).b, 0, s, Lf, Lc, e, fine, coarse, cb, total);
 }
 
 void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag,
@@ -2292,7 +2502,7 @@ void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, do
   Box b = cell_box(L);
   if (L.bclo[A] != BC_PER) b.hi[A] = L.n[A];
   const unsigned total = box_count(b);
-  k_beta<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, rho, beta, flag, cflag, ref, b, total);
+  launch_k(k_beta, cfg3(b).g, cfg3(b).b, 0, s, L, A, rho, beta, flag, cflag, ref, b, total);
 }
 
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags) {
@@ -2301,28 +2511,31 @@ void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
   ++g_kernel_launches;
-    if (dim == 3) k_check_diag<3, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
-    else k_check_diag<2, FM><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flags, b, total);
+    if (dim == 3) launch_k(k_check_diag<3, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
+    else launch_k(k_check_diag<2, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
   });
 }
 
 void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag) {
   ++g_kernel_launches;
-  const Box b = cell_box(L);
-  if (dim == 3) k_check_mue<3><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flag, b);
-  else k_check_mue<2><<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, flag, b);
+  Box b = cell_box(L);
+  for (int a = 0; a < 3; ++a)
+    if (L.bclo[a] != BC_PER) b.hi[a] += 1;
+  if (dim == 2) b.hi[0] = 0;
+  if (dim == 3) launch_k(k_check_mue<3>, cfg3(b).g, cfg3(b).b, 0, s, L, flag, b);
+  else launch_k(k_check_mue<2>, cfg3(b).g, cfg3(b).b, 0, s, L, flag, b);
 }
 
 void launch_box_fill(cudaStream_t s, const LevelDev& L, Box b, double* x, double v) {
   const unsigned total = box_count(b);
-  k_box_fill<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, v, b, total);
+  launch_k(k_box_fill, cfg3(b).g, cfg3(b).b, 0, s, L, x, v, b, total);
 }
 
 void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, const double* sum,
                            double inv_count) {
   ++g_kernel_launches;
   const unsigned total = box_count(b);
-  k_box_sub_mean<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, x, sum, inv_count, b, total);
+  launch_k(k_box_sub_mean, cfg3(b).g, cfg3(b).b, 0, s, L, x, sum, inv_count, b, total);
 }
 
 void launch_wall_tangent(cudaStream_t s, const LevelDev& L, int A, int B, int side, const double* plane,
@@ -2339,22 +2552,22 @@ void launch_wall_tangent(cudaStream_t s, const LevelDev& L, int A, int B, int si
   ext[B] = 1;
   const unsigned total = box_count(b);
   (void)total;
-  k_wall_tangent<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, A, B, side, plane, out, b, ext[1], ext[2]);
+  launch_k(k_wall_tangent, cfg3(b).g, cfg3(b).b, 0, s, L, A, B, side, plane, out, b, ext[1], ext[2]);
 }
 
 void launch_sum_abs_partial(cudaStream_t s, const double* x, long long n, double* partials) {
   ++g_kernel_launches;
-  k_sum_abs_partial<<<kRedBlocks, kThreads, 0, s>>>(x, n, partials, kRedBlocks);
+  launch_k(k_sum_abs_partial, kRedBlocks, kThreads, 0, s, x, n, partials, kRedBlocks);
 }
 
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x) {
   ++g_kernel_launches;
-  k_add_scalar<<<1, 1, 0, s>>>(y, x);
+  launch_k(k_add_scalar, 1, 1, 0, s, y, x);
 }
 
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x) {
   const unsigned total = box_count(b);
-  k_box_axpy<<<cfg3(b).g, cfg3(b).b, 0, s>>>(L, y, x, b, total);
+  launch_k(k_box_axpy, cfg3(b).g, cfg3(b).b, 0, s, L, y, x, b, total);
 }
 
 void launch_multi_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* w,
@@ -2362,7 +2575,7 @@ void launch_multi_dot(cudaStream_t s, const double* V, long long vstride, int nv
   ++g_kernel_launches;
   static const int grid = wave_grid(k_multi_dot);
   g_red_blocks_used = grid;
-  k_multi_dot<<<grid, kThreads, 0, s>>>(V, vstride, nv, w, n / 2, partials);
+  launch_k(k_multi_dot, grid, kThreads, 0, s, V, vstride, nv, w, n / 2, partials);
 }
 
 void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int nv, const double* h,
@@ -2370,13 +2583,13 @@ void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int n
   ++g_kernel_launches;
   static const int grid = wave_grid(k_update_dot);
   g_red_blocks_used = grid;
-  k_update_dot<<<grid, kThreads, 0, s>>>(V, vstride, nv, h, w, n / 2, partials, mode);
+  launch_k(k_update_dot, grid, kThreads, 0, s, V, vstride, nv, h, w, n / 2, partials, mode);
 }
 
 void launch_dcgs_a(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                    const double* w, long long n, double* partials) {
   ++g_kernel_launches;
-  k_dcgs_a<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+  launch_k(k_dcgs_a, kRedBlocks, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials);
 }
 
 void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
@@ -2394,32 +2607,44 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
       configured = true;
     }
     if (stash <= 160 * 1024) {
-      k_dcgs_b_stash<<<kRedBlocks, kStashThreads, stash, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+      launch_k(k_dcgs_b_stash, kRedBlocks, kStashThreads, stash, s, Q, vstride, nv, d, w, out, n / 2, partials);
       return;
     }
   }
   if (variant == 2) {
-    k_dcgs_b_l2<<<kL2Blocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+    launch_k(k_dcgs_b_l2, kL2Blocks, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials);
     g_red_blocks_used = kL2Blocks;
     return;
   }
-  k_dcgs_b<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials);
+  launch_k(k_dcgs_b, kRedBlocks, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials);
 }
 
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                      const double* w, long long n, double* partials) {
   ++g_kernel_launches;
-  static const bool chunked = [] {
-    const char* e = std::getenv("SB_DCGS_A");
-    return !(e && e[0] == '0');
-  }();
-  if (chunked) {
-    static const int grid_a = wave_grid(k_dcgs_a_g2<4>);
-    g_red_blocks_used = grid_a;
-    k_dcgs_a_g2<4><<<grid_a, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
-  } else {
-    k_dcgs_a_g<<<kRedBlocks, kThreads, 0, s>>>(Q, vstride, k, c, inv_gamma, w, n / 2, partials);
+  // SB_DCGS_A: 0 un-chunked, 2 register-chunked (CH 4), 32 / 34 / 24 (default)
+  // / 323 / 343 grouped
+  // basis reads (CH 2 or 4 double2 per thread, G 2 or 4 vectors per group;
+  // a trailing 3: three resident CTAs per SM)
+  // read per launch (not cached) so tests can switch variants in-process
+  const char* ev = std::getenv("SB_DCGS_A");
+  const int variant = ev ? std::atoi(ev) : 24;
+#define SB_DCGS_A_LAUNCH(KER)                                                        \
+  {                                                                                 \
+    static const int grid_a = wave_grid(KER);                                       \
+    g_red_blocks_used = grid_a;                                                     \
+    launch_k(KER, grid_a, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials); \
   }
+  switch (variant) {
+    case 0: launch_k(k_dcgs_a_g, kRedBlocks, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials); break;
+    case 32: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<2, 2>)); break;
+    case 34: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<2, 4>)); break;
+    case 343: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<2, 4, 3>)); break;
+    case 323: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<2, 2, 3>)); break;
+    case 2: SB_DCGS_A_LAUNCH(k_dcgs_a_g2<4>); break;
+    default: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<4, 2>)); break;
+  }
+#undef SB_DCGS_A_LAUNCH
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
@@ -2427,10 +2652,11 @@ void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv,
   ++g_kernel_launches;
   static const int grid_b = wave_grid(k_dcgs_b_g);
   g_red_blocks_used = grid_b;
-  k_dcgs_b_g<<<grid_b, kThreads, 0, s>>>(Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2);
+  launch_k(k_dcgs_b_g, grid_b, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2);
 }
 
 __global__ void k_block_means(const double* __restrict__ sums, int4 slot, double inv_count, double* __restrict__ means) {
+  pdl_enter();
   if (threadIdx.x == 0) {
     means[0] = slot.x >= 0 ? sums[slot.x] * inv_count : 0.0;
     means[1] = slot.y >= 0 ? sums[slot.y] * inv_count : 0.0;
@@ -2441,11 +2667,11 @@ __global__ void k_block_means(const double* __restrict__ sums, int4 slot, double
 
 void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* means) {
   ++g_kernel_launches;
-  k_block_means<<<1, 32, 0, s>>>(sums, make_int4(slot[0], slot[1], slot[2], slot[3]), inv_count, means);
+  launch_k(k_block_means, 1, 32, 0, s, sums, make_int4(slot[0], slot[1], slot[2], slot[3]), inv_count, means);
 }
 
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out) {
-  k_finalize<<<nv, kThreads, 0, s>>>(partials, out, g_red_blocks_used);
+  launch_k(k_finalize, nv, kThreads, 0, s, partials, out, g_red_blocks_used);
   g_red_blocks_used = kRedBlocks;
 }
 
@@ -2453,31 +2679,31 @@ void launch_sum_partial(cudaStream_t s, const double* x, long long n, double* pa
   ++g_kernel_launches;
   static const int grid = wave_grid(k_sum_partial);
   g_red_blocks_used = grid;
-  k_sum_partial<<<grid, kThreads, 0, s>>>(x, n, partials);
+  launch_k(k_sum_partial, grid, kThreads, 0, s, x, n, partials);
 }
 
 void launch_sub_norm(cudaStream_t s, const double* a, const double* b, long long n, double* partials) {
   ++g_kernel_launches;
   static const int grid = wave_grid(k_sub_norm);
   g_red_blocks_used = grid;
-  k_sub_norm<<<grid, kThreads, 0, s>>>(a, b, n, partials);
+  launch_k(k_sub_norm, grid, kThreads, 0, s, a, b, n, partials);
 }
 
 void launch_scale_div(cudaStream_t s, const double* w, double d, double* out, long long n) {
   ++g_kernel_launches;
-  k_scale_div<<<grid_for(n / 2), kThreads, 0, s>>>(reinterpret_cast<const double2*>(w), d,
+  launch_k(k_scale_div, grid_for(n / 2), kThreads, 0, s, reinterpret_cast<const double2*>(w), d,
                                                     reinterpret_cast<double2*>(out), n / 2);
 }
 
 void launch_combo(cudaStream_t s, double* out, const double* x, const double* V, long long vstride, int nv,
                   const double* y, long long n) {
   ++g_kernel_launches;
-  k_combo<<<grid_for(n / 2), kThreads, 0, s>>>(reinterpret_cast<double2*>(out),
+  launch_k(k_combo, grid_for(n / 2), kThreads, 0, s, reinterpret_cast<double2*>(out),
                                                 reinterpret_cast<const double2*>(x), V, vstride, nv, y, n / 2);
 }
 
 void launch_sub(cudaStream_t s, const double* a, const double* b, double* out, long long n) {
-  k_sub<<<grid_for(n / 2), kThreads, 0, s>>>(reinterpret_cast<const double2*>(a),
+  launch_k(k_sub, grid_for(n / 2), kThreads, 0, s, reinterpret_cast<const double2*>(a),
                                              reinterpret_cast<const double2*>(b),
                                              reinterpret_cast<double2*>(out), n / 2);
 }

@@ -6,6 +6,24 @@
 
 namespace sb {
 
+// Kernel launch with programmatic stream serialization (see pdl_enter);
+// SB_PDL=0 falls back to plain stream order.
+bool pdl_enabled();
+template <typename... KA, typename... AA>
+inline void launch_k(void (*k)(KA...), dim3 g, dim3 b, size_t smem, cudaStream_t s, AA&&... a) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<AA&&>(a)...);
+}
+
 struct Ptr3 { double* p[3]; };
 struct CPtr3 { const double* p[3]; };
 

@@ -366,6 +366,7 @@ constexpr Need NONE{0, 0, 0};
 template <int FORM, int A, bool DE, int MINB>
 __global__ void __launch_bounds__(RT, MINB)
 k_face_colour_rv(LevelDev L, Ptr3 u, const double* __restrict__ rhs, int parity, double omega, int nseg) {
+  pdl_enter();
   // a CTA = 8 warps on 8 consecutive rows j of one segment: the +-1 rows
   // along axis 1 are shared through L1
   const int t = threadIdx.x & 31;
@@ -426,6 +427,7 @@ template <int FORM, bool DE, bool MODE_M, int MINB>
 __global__ void __launch_bounds__(RT, MINB)
 k_face_all_rv(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3 out, double* __restrict__ out_p,
               int nseg) {
+  pdl_enter();
   const int t = threadIdx.x & 31;
   const int nj = (L.n[1] + 7) >> 3;
   const int seg = (int)blockIdx.x % nseg, rest = (int)blockIdx.x / nseg;
@@ -518,8 +520,8 @@ template <int FM, int A>
 void colour_rv_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, int parity, double omega) {
   const int nseg = L.n[2] / 64;
   const int nb = blocks_for(L, 64);
-  if (L.mue_derived) k_face_colour_rv<FM, A, true, 3><<<nb, RT, 0, s>>>(L, u, rhs, parity, omega, nseg);
-  else k_face_colour_rv<FM, A, false, 3><<<nb, RT, 0, s>>>(L, u, rhs, parity, omega, nseg);
+  if (L.mue_derived) launch_k(k_face_colour_rv<FM, A, true, 3>, nb, RT, 0, s, L, u, rhs, parity, omega, nseg);
+  else launch_k(k_face_colour_rv<FM, A, false, 3>, nb, RT, 0, s, L, u, rhs, parity, omega, nseg);
 }
 
 }  // namespace
@@ -565,11 +567,11 @@ static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 r
   const int nb = blocks_for(L, 32);
   const bool de = L.mue_derived != 0;
   if (form == F_LAP) {
-    if (de) k_face_all_rv<F_LAP, true, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
-    else k_face_all_rv<F_LAP, false, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+    if (de) launch_k(k_face_all_rv<F_LAP, true, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    else launch_k(k_face_all_rv<F_LAP, false, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
   } else {
-    if (de) k_face_all_rv<F_STRESS, true, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
-    else k_face_all_rv<F_STRESS, false, MODE_M, 3><<<nb, RT, 0, s>>>(L, x, rhs, p, out, out_p, nseg);
+    if (de) launch_k(k_face_all_rv<F_STRESS, true, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    else launch_k(k_face_all_rv<F_STRESS, false, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
   }
 }
 

@@ -1302,13 +1302,17 @@ void build_from_level0(sb_ctx* c) {
     }
     for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
     // levels whose edge viscosities are the four-cell mean of mu_c: the face
-    // rows derive them instead of streaming mu_e (SB_MUE_DERIVED=0: never)
-    const bool derive_on = [] {  // read per upload: tests compare both paths in one process
+    // rows derive them instead of streaming mu_e.  SB_MUE_DERIVED: 1 (default)
+    // all-periodic levels, 2 also wall-bounded levels (two-cell boundary
+    // means; bit-compatible but measured no faster on C4: 200 -> 204 us per
+    // finest colour pass, the walled row turns L1/issue-bound), 0 never
+    const int derive_mode = [] {  // read per upload: tests compare the paths in one process
       const char* e = std::getenv("SB_MUE_DERIVED");
-      return !(e && e[0] == '0');
+      return e ? std::atoi(e) : 1;
     }();
     const bool per_all = c->bc[0][0] == BC_PER && c->bc[1][0] == BC_PER && c->bc[2][0] == BC_PER;
-    if (derive_on && per_all)
+    const bool derive_on = derive_mode == 2 || (derive_mode == 1 && per_all);
+    if (derive_on)
       for (int l = 0; l < nl; ++l) launch_check_mue(c->st, c->lv[l].d, c->dim, c->dflags + 16 + l);
     int hm[kFlagInts - 16];
     CK(cudaMemcpyAsync(hf, c->dflags, 16, cudaMemcpyDeviceToHost, c->st));
@@ -1321,7 +1325,7 @@ void build_from_level0(sb_ctx* c) {
     bool changed = false;
     for (int l = 0; l < nl; ++l) {
       LevelDev& d = c->lv[l].d;
-      const int de = (derive_on && per_all && hm[l] == 0) ? 1 : 0;
+      const int de = (derive_on && hm[l] == 0) ? 1 : 0;
       const int bc = (const_on && hm[kMaxLevels + l] == 0 && href[l] > 0.0) ? 1 : 0;
       const double bv = bc ? 1.0 / href[l] : 0.0;  // k_beta's expression
       changed |= de != d.mue_derived || bc != d.beta_const || bv != d.beta_val;

@@ -26,7 +26,7 @@ def _setup(name, n, derive, monkeypatch, edit=None):
     cs, rs, spec = PR.prepare(case)
     if edit is not None:
         cs = edit(cs)
-    monkeypatch.setenv("SB_MUE_DERIVED", "1" if derive else "0")
+    monkeypatch.setenv("SB_MUE_DERIVED", "2" if derive else "0")  # 2: walled levels too
     P = Preconditioner(cs, PrecondConfig(kind=P1))
     monkeypatch.delenv("SB_MUE_DERIVED")
     return case, cs, rs, P
@@ -41,7 +41,7 @@ def _pack(x):
     return pack_stokes(x)
 
 
-@pytest.mark.parametrize("name,n", [("C5", 32), ("C3", 64), ("C1", 64)])
+@pytest.mark.parametrize("name,n", [("C5", 32), ("C3", 64), ("C1", 64), ("C4", 32), ("C2", 64)])
 def test_derived_matches_stored(name, n, monkeypatch):
     from paper_1308_4605_b200 import operators as OPS
     from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
@@ -74,10 +74,17 @@ def test_walls_and_foreign_edges_keep_stored_path(monkeypatch):
     from dataclasses import replace
     from paper_1308_4605_b200 import operators as OPS
     from paper_1308_4605_b200.grid import NodeEdgeField
-    # a wall-bounded level never derives
+    # a wall-bounded finest level derives when asked (SB_MUE_DERIVED=2, two-cell
+    # boundary means); its coarse levels inject mu_e and keep the stored path.
+    # By default (1) only all-periodic levels derive.
     _, _, _, P = _setup("C4", 16, True, monkeypatch)
-    assert not P.ctx.mue_derived(0)
+    assert P.ctx.mue_derived(0) and not P.ctx.mue_derived(1)
     del P
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case = PR.make_case("C4", 16)
+    cs4, _, _ = PR.prepare(case)
+    assert not Preconditioner(cs4, PrecondConfig(kind=P1)).ctx.mue_derived(0)
 
     # harmonic edge means: not the arithmetic cell mean -> stored path, and the
     # operator is the one of the given mu_edge (oracle)
@@ -106,6 +113,46 @@ def test_walls_and_foreign_edges_keep_stored_path(monkeypatch):
 
     _, _, _, P2 = _setup("C5", 16, True, monkeypatch, edit=one_off)
     assert not P2.ctx.mue_derived(0)
+
+
+@pytest.mark.parametrize("cells,bc", [((16, 24, 32), "nn pp pp"), ((24, 16, 16), "pp nn ff"),
+                                      ((16, 32, 40), "fn nf nn"), ((32, 48), "pp nn"), ((24, 16), "fn nf")])
+@pytest.mark.parametrize("form,theta", [("stress", 0.0), ("laplacian", 0.4), ("stress_bulk", 1.0)])
+def test_walled_levels_derive_vs_oracle(cells, bc, form, theta, monkeypatch):
+    """Derived edge viscosities on wall-bounded levels (no-slip, free-slip and
+    mixed walls, 2D and 3D, every viscous form): apply_M and one face V-cycle
+    equal the oracle's with the stored mu_edge."""
+    from oracle import stokes_oracle as O
+    from paper_1308_4605_b200 import multigrid as MG
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200.grid import (BoundaryCondition, CellField, FaceField, GridSpec,
+                                           StokesVector)
+    from paper_1308_4605_b200.operators import ViscousForm, make_coefficients
+    names = {"p": "periodic", "n": "no_slip", "f": "free_slip"}
+    pairs = [(names[x[0]], names[x[1]]) for x in bc.split()]
+    g = GridSpec(cells, 1.0 / cells[0], tuple((BoundaryCondition(a), BoundaryCondition(b)) for a, b in pairs))
+    geo = O.Geo(cells, g.h, tuple(pairs))
+    rng = np.random.default_rng(sum(cells) + len(form))
+    rho, mu, gam = 0.5 + rng.random(cells), 0.5 + rng.random(cells), rng.random(cells)
+    c = make_coefficients(g, theta, CellField(g, rho), CellField(g, mu), CellField(g, gam), ViscousForm(form))
+    oc = O.make_coef(geo, theta, rho, mu, gam, form)
+    x = [rng.standard_normal(g.face_shape(a)) for a in range(g.dim)]
+    for a in range(g.dim):
+        if not g.periodic(a):
+            x[a][(slice(None),) * a + (0,)] = 0.0
+            x[a][(slice(None),) * a + (-1,)] = 0.0
+    p = rng.standard_normal(cells)
+    monkeypatch.setenv("SB_MUE_DERIVED", "2")
+    h = MG.build_hierarchy(g, c)
+    assert h.ctx.mue_derived(0)
+    m = OPS.apply_M(StokesVector(FaceField(g, tuple(x)), CellField(g, p)), c, ctx=h.ctx)
+    mu_, mp_ = O.apply_M(geo, oc, [a.copy() for a in x], p)
+    for a in range(g.dim):
+        assert _rel(m.u.components[a], mu_[a]) <= 1e-13, a
+    vf = MG.vcycle(FaceField(g, tuple(x)), h, MG.SmootherParams(), "face")
+    want = O.vcycle(O.Hierarchy(geo, oc), [a.copy() for a in x], "face")
+    for a in range(g.dim):
+        assert _rel(np.asarray(vf.components[a]), want[a]) <= 1e-12, a
 
 
 # ---- constant density: one 1/rho for the cell rows (LevelDev::beta_const) ------
