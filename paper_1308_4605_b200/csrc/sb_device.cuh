@@ -152,7 +152,10 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // levels whose mu_e matched that derivation at setup (LevelDev::mue_derived,
 // k_check_mue); mu_c's neighbours come from L1/L2, so the face row streams
 // one coefficient array instead of three.
-template <int DIM, int A, int PA = false, bool NC = true, bool DE = false>
+// ZM: bit B set = component B is known to be identically zero (the first
+// sweep of a V-cycle level starts from x = 0, multigrid.py:409-439), so its
+// loads are replaced by the value they would return.
+template <int DIM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
@@ -211,6 +214,7 @@ struct GAcc {
   }
   template <int B>
   __device__ __forceinline__ double ub(bool hi, bool lowA) const {
+    if (ZM & (1 << B)) return 0.0;
     const int e = hi ? f + eB<B>() : f;
     return NC ? ld(u[B], lowA ? e + dmA : e) : u[B][lowA ? e + dmA : e];
   }
@@ -312,10 +316,10 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool DE = false>
+template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
-  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE>(L, u, f, ci), ci, diag);
+  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE, ZM>(L, u, f, ci), ci, diag);
 }
 
 template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool CG = false, bool DE = false>

@@ -109,7 +109,17 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 // same-colour faces couple through the wrap): phase 0 stores the new values in
 // tmp, phase 1 copies them in -- exactly the reference's compute-all-then-
 // update-masked order.
-template <int DIM, int FORM, int A, int PHASE, int PA, bool DE = false>
+//
+// Z (first sweep of a V-cycle level, x = 0 on entry): 1 = the components after
+// A are still zero (their loads are skipped); 2 = also u_A itself (first colour
+// of A: no u loads at all); 3 = as 2 and the pass also stores the zero of the
+// other-colour partner face (k ^ 1), which replaces the level's zero fill on
+// all-periodic pad-free levels (every block entry is then written).  Same
+// arithmetic on the same values as the plain pass: bit-identical.
+template <int A>
+__host__ __device__ constexpr int later_mask() { return A == 0 ? 6 : (A == 1 ? 4 : 0); }
+
+template <int DIM, int FORM, int A, int PHASE, int PA, bool DE = false, int Z = 0>
 __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -131,7 +141,21 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
     }
     const double* uc[3] = {u.p[0], u.p[1], u.p[2]};
     double dg;
-    const double au = face_row<DIM, FORM, A, PA, true, false, DE>(L, uc, f, ci, dg);
+    if (Z >= 2) {
+      constexpr int ZM = later_mask<A>() | (1 << A);
+      UA7 s0;
+      s0.c = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) s0.p[q] = s0.m[q] = 0.0;
+      const double au = face_row_core<DIM, FORM, A, PA, true, DE, ZM>(L, s0, uc, f, ci, dg);
+      const double res = __ldg(rhs + f) - au;
+      u.p[A][f] = s0.c + omega * (res / dg);
+      if (Z == 3) u.p[A][(k & 1) ? f - 1 : f + 1] = 0.0;
+      return;
+    }
+    constexpr int ZM = Z == 1 ? later_mask<A>() : 0;
+    const double au =
+        face_row_core<DIM, FORM, A, PA, true, DE, ZM>(L, gather_ua<DIM, A, PA>(L, uc[A], f, ci), uc, f, ci, dg);
     const double res = __ldg(rhs + f) - au;
     const double nv = uc[A][f] + omega * (res / dg);
     if (PHASE == 2) tmp[f] = nv;
@@ -139,7 +163,7 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
   }
 }
 
-template <int DIM, int PHASE, int PA>
+template <int DIM, int PHASE, int PA, int Z = 0>
 __global__ void __launch_bounds__(kThreads)
 k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -159,6 +183,17 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
       return;
     }
     double dg;
+    if (Z >= 2) {  // first colour of a V-cycle level from phi = 0 (see k_face_colour)
+      UA7 s0;
+      s0.c = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) s0.p[q] = s0.m[q] = 0.0;
+      const double lp = cell_row_core<DIM, PA>(L, s0, c, ci, dg);
+      const double res = __ldg(rhs + c) - lp;
+      phi[c] = s0.c + omega * res / dg;
+      if (Z == 3) phi[(k & 1) ? c - 1 : c + 1] = 0.0;
+      return;
+    }
     const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
     const double res = __ldg(rhs + c) - lp;
     const double nv = phi[c] + omega * res / dg;
@@ -2102,18 +2137,30 @@ static bool odd_periodic(const LevelDev& L, int dim) {
 
 template <int DIM, int FM, int A>
 static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, double* tmp,
-                          int parity, double omega) {
+                          int parity, double omega, int z = 0) {
   Box b = face_box(L, DIM, A);
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
   const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
   const dim3 g = c3.g, kb = c3.b;
-  if (tmp == nullptr) {
-    SB_DISPATCH_PA(L, {
-      if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, PAT, true>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
-      else launch_k(k_face_colour<DIM, FM, A, 0, PAT>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
-    });
+  if (tmp == nullptr && z == 3) {  // all-periodic pad-free level (zero_fill_free)
+    if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, 1, true, 3>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
+    else launch_k(k_face_colour<DIM, FM, A, 0, 1, false, 3>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
+  } else if (tmp == nullptr) {
+#define SB_FC_Z(ZZ)                                                                                                          \
+  SB_DISPATCH_PA(L, {                                                                                                        \
+    if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, PAT, true, ZZ>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total); \
+    else launch_k(k_face_colour<DIM, FM, A, 0, PAT, false, ZZ>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);            \
+  })
+    if (z == 2) {
+      SB_FC_Z(2);
+    } else if (z == 1) {
+      SB_FC_Z(1);
+    } else {
+      SB_FC_Z(0);
+    }
+#undef SB_FC_Z
   } else {
     ++g_kernel_launches;
     launch_k(k_face_colour<DIM, FM, A, 2, false>, g, kb, 0, s, L, u, rhs, tmp, parity, omega, b, half2, total);
@@ -2122,23 +2169,23 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
 }
 
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega) {
+                        const double* rhsA, int parity, double omega, int z) {
   ++g_kernel_launches;
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
   // the solver routes those levels through launch_face_colour_tmp below.
-  if (rowv_colour_supported(L, dim, form)) {
+  if (z == 0 && rowv_colour_supported(L, dim, form)) {
     launch_face_colour_rv(s, L, form, A, u, rhsA, parity, omega);
     return;
   }
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega);
-      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega);
-      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega);
+      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z);
+      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z);
+      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z);
     } else {
-      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega);
-      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega);
+      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z);
+      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z);
     }
   });
 }
@@ -2160,14 +2207,18 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 
 template <int DIM>
 static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double* tmp,
-                          int parity, double omega) {
+                          int parity, double omega, int z = 0) {
   Box b = cell_box(L);
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
   const L3 c3 = cfg3(L.n[0], L.n[1], (int)half2);
   const dim3 g = c3.g, kb = c3.b;
-  if (tmp == nullptr) {
+  if (tmp == nullptr && z == 3) {
+    launch_k(k_cell_colour<DIM, 0, 1, 3>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total);
+  } else if (tmp == nullptr && z == 2) {
+    SB_DISPATCH_PA(L, launch_k(k_cell_colour<DIM, 0, PAT, 2>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total));
+  } else if (tmp == nullptr) {
     SB_DISPATCH_PA(L, launch_k(k_cell_colour<DIM, 0, PAT>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total));
   } else {
     ++g_kernel_launches;
@@ -2177,10 +2228,10 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
 }
 
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega) {
+                        int parity, double omega, int z) {
   ++g_kernel_launches;
-  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega);
-  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega);
+  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z);
+  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z);
 }
 
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,

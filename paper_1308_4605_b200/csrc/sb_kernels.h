@@ -50,10 +50,13 @@ struct CoarseChain {
 };
 
 // colour passes (multigrid.py:318-340)
+// z: first-sweep-from-zero variants (k_face_colour): 0 plain, 1 later
+// components zero, 2 also the relaxed array zero, 3 as 2 + store the partner's
+// zero (replaces the zero fill; all-periodic pad-free levels only)
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega);
+                        const double* rhsA, int parity, double omega, int z = 0);
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega);
+                        int parity, double omega, int z = 0);
 // two-phase variants for levels with an odd periodic extent (same-colour
 // cells couple through the wrap): compute all, then update (reference order)
 void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,

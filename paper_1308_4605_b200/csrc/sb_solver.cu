@@ -429,7 +429,10 @@ double cell_pass_bytes(const sb_ctx* c, const Level& L) {
 
 // One smoother sweep on level l.  cur[] holds the iterate; fused levels
 // sweep out of place into alt[] and swap the pointers (ping-pong).
-void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* const* rhs, double omega) {
+// zs (first sweep of a V-cycle level, x = 0 on entry): 0 plain, 1 the level
+// was zero-filled, 2 the level was not (zero_fill_free: the first colour pass
+// stores both colours).  Only the per-colour kernels take the zero variants.
+void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* const* rhs, double omega, int zs = 0) {
   Level& L = c->lv[l];
   if (L.wave) {
     for (int A = 3 - c->dim; A < 3; ++A) {
@@ -456,25 +459,38 @@ void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* cons
         ea = next_event(c);
         CK(cudaEventRecord(ea, c->st));
       }
+      int z = 0;
       if (L.fused) {
         CPtr3 u{{cur[0], cur[1], cur[2]}};
         launch_face_sweep2(c->st, L.d, c->form, A, u, alt[A], rhs[A], omega);
         std::swap(cur[A], alt[A]);
       } else {
         Ptr3 u{{cur[0], cur[1], cur[2]}};
-        if (L.two_phase) launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
-        else launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega);
+        if (L.two_phase) {
+          launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
+        } else {
+          z = zs == 0 ? 0 : (parity == 0 ? (zs == 2 ? 3 : 2) : 1);
+          launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega, z);
+        }
       }
       if (c->profiling) {
         cudaEvent_t eb = next_event(c);
         CK(cudaEventRecord(eb, c->st));
-        c->prof.push_back({ea, eb, 0, l == 0, per_launch * face_pass_bytes(c, L)});
+        // zero-aware passes: 8 B less per skipped component, the partner store
+        // of z = 3 adds 4 B; the roofline (fine) average takes plain passes only
+        double bytes = per_launch * face_pass_bytes(c, L);
+        if (z != 0) {
+          int nz = 0;
+          for (int B = 3 - c->dim; B < 3; ++B) nz += (B > A || (B == A && z >= 2)) ? 1 : 0;
+          bytes -= (8.0 * nz - (z == 3 ? 4.0 : 0.0)) * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+        }
+        c->prof.push_back({ea, eb, 0, l == 0 && z == 0, bytes});
       }
     }
   }
 }
 
-void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs, double omega) {
+void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs, double omega, int zs = 0) {
   Level& L = c->lv[l];
   if (L.wave) {
     cudaEvent_t ea = nullptr;
@@ -497,18 +513,22 @@ void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs,
       ea = next_event(c);
       CK(cudaEventRecord(ea, c->st));
     }
+    int z = 0;
     if (L.fused) {
       launch_cell_sweep2(c->st, L.d, cur, alt, rhs, omega);
       std::swap(cur, alt);
     } else if (L.two_phase) {
       launch_cell_colour_tmp(c->st, L.d, c->dim, cur, rhs, L.tmp, parity, omega);
     } else {
-      launch_cell_colour(c->st, L.d, c->dim, cur, rhs, parity, omega);
+      z = (zs == 0 || parity == 1) ? 0 : (zs == 2 ? 3 : 2);
+      launch_cell_colour(c->st, L.d, c->dim, cur, rhs, parity, omega, z);
     }
     if (c->profiling) {
       cudaEvent_t eb = next_event(c);
       CK(cudaEventRecord(eb, c->st));
-      c->prof.push_back({ea, eb, 1, l == 0, per_launch * cell_pass_bytes(c, L)});
+      const double pts = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
+      const double bytes = per_launch * cell_pass_bytes(c, L) - (z == 0 ? 0.0 : (z == 3 ? 4.0 : 8.0) * pts);
+      c->prof.push_back({ea, eb, 1, l == 0, bytes});
     }
   }
 }
@@ -565,17 +585,38 @@ bool coarse_tail(sb_ctx* c, int l, int kind, const double* const* rhs, double* c
   return true;
 }
 
+// How the first sweep of a V-cycle level treats its x = 0 start: 0 plain
+// passes after the zero fill (streaming / wavefront / row-vector / two-phase
+// levels, SB_ZERO_FIRST=0), 1 zero-aware passes after the zero fill, 2
+// zero-aware passes without it -- all-periodic levels whose block has no pads
+// or ghosts, where the first colour pass stores every entry (bulk-form face
+// rows read the divergence of all components, so they keep the fill).
+static bool zero_first_on() {  // read per call: tests compare both paths in one process
+  const char* e = std::getenv("SB_ZERO_FIRST");
+  return !(e && e[0] == '0');
+}
+int first_sweep_mode(sb_ctx* c, const Level& L, int kind) {
+  if (!zero_first_on() || L.fused || L.wave || L.two_phase) return 0;
+  if (kind == SB_KIND_FACE && rowv_colour_supported(L.d, c->dim, c->form)) return 0;
+  bool pa = L.d.dist0 == 0 && (L.d.n[2] % 4) == 0;
+  for (int a = 3 - c->dim; a < 3; ++a) pa = pa && c->bc[a][0] == BC_PER && L.P[a] == L.d.n[a];
+  if (kind == SB_KIND_FACE && c->form == F_BULK) pa = false;
+  return pa ? 2 : 1;
+}
+
 void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, const sb_smoother& sm) {
   if (coarse_tail(c, l, SB_KIND_FACE, rhs, x, sm)) return;
   Level& L = c->lv[l];
   double* cur[3] = {x[0], x[1], x[2]};
   double* alt[3] = {L.fxa[0], L.fxa[1], L.fxa[2]};
-  for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(cur[A], 0, L.block * 8, c->st));
+  const int zs = first_sweep_mode(c, L, SB_KIND_FACE);
+  if (zs != 2)
+    for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(cur[A], 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
   } else {
-    for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
     Level& Lc = c->lv[l + 1];
     CPtr3 xc{{cur[0], cur[1], cur[2]}};
     if (L.split_rr) {
@@ -605,12 +646,13 @@ void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smooth
   Level& L = c->lv[l];
   double* cur = x;
   double* alt = L.cxa;
-  CK(cudaMemsetAsync(cur, 0, L.block * 8, c->st));
+  const int zs = first_sweep_mode(c, L, SB_KIND_CELL);
+  if (zs != 2) CK(cudaMemsetAsync(cur, 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
   } else {
-    for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
     Level& Lc = c->lv[l + 1];
     if (L.split_rr) {
       launch_cell_res(c->st, L.d, c->dim, cur, rhs, L.cres);
