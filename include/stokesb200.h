@@ -246,7 +246,8 @@ sb_dist* sb_dist_create(const int* cells, double h, const int* bc, int viscous_f
 void sb_dist_destroy(sb_dist* dist);
 /* the CUDA stream the distributed context launches on (cudaStream_t) */
 void* sb_dist_stream(sb_dist* dist);
-/* out[4] = {distributed levels, agglomerated levels, planes per slab, slabs in this process} */
+/* out[6] = {distributed levels, agglomerated levels, planes per slab, slabs in this process,
+ *          bit l: distributed level l derives mu_e from mu_c, bit l: level l has constant 1/rho} */
 int sb_dist_info(sb_dist* dist, int* out);
 int sb_dist_set_coefficients(sb_dist* dist, double theta, const double* const* rho_face, const double* mu_cell,
                              const double* const* mu_edge, const double* gamma_cell);

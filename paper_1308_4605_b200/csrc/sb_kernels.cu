@@ -994,7 +994,8 @@ __device__ double edge_ref(const LevelDev& L, int e, const int* ci) {
   const int ah = DIM == 2 ? 2 : (e == 2 ? 1 : 2);
   const bool pl = L.bclo[al] == BC_PER, ph = L.bclo[ah] == BC_PER;
   const int jl = ci[al], jh = ci[ah], nl = L.n[al], nh = L.n[ah];
-  auto wrap = [](int j, int n) { return j < 0 ? j + n : j; };
+  // a slab-distributed axis 0 reads its ghost plane -1 instead of wrapping
+  auto wrapa = [&](int j, int n, int ax) { return (j < 0 && !(ax == 0 && L.dist0)) ? j + n : j; };
   auto cell = [&](int cl, int ch) {
     int c[3] = {ci[0], ci[1], ci[2]};
     c[al] = cl;
@@ -1004,11 +1005,11 @@ __device__ double edge_ref(const LevelDev& L, int e, const int* ci) {
   auto arr1 = [&](int ch) {
     if (!pl && jl == 0) return cell(0, ch);
     if (!pl && jl == nl) return cell(nl - 1, ch);
-    return 0.5 * (cell(jl, ch) + cell(wrap(jl - 1, nl), ch));
+    return 0.5 * (cell(jl, ch) + cell(wrapa(jl - 1, nl, al), ch));
   };
   if (!ph && jh == 0) return arr1(0);
   if (!ph && jh == nh) return arr1(nh - 1);
-  return 0.5 * (arr1(jh) + arr1(wrap(jh - 1, nh)));
+  return 0.5 * (arr1(jh) + arr1(wrapa(jh - 1, nh, ah)));
 }
 
 // Does every edge (3D) / node (2D) viscosity of a level equal edge_ref to
@@ -1112,6 +1113,15 @@ __global__ void k_box_sub_mean(LevelDev L, double* x, const double* sum, double 
 
 __global__ void k_add_scalar(double* y, const double* x) {
   pdl_enter(); *y += *x; }
+__global__ void k_neg_copy(double* y, const double* x) {
+  pdl_enter();
+  *y = -*x;
+}
+__global__ void k_max_scalar(double* y, const double* x, int neg) {
+  pdl_enter();
+  const double v = neg ? -*x : *x;
+  if (v > *y) *y = v;
+}
 
 __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, Box b, unsigned total) {
   pdl_enter();
@@ -2127,7 +2137,8 @@ static int bc_pattern(const LevelDev& L) {
     default: { constexpr int PAT = 0; __VA_ARGS__; } break;        \
   }
 // level whose edge viscosities are derived from mu_c (DE kernels)
-static bool derive_mue(const LevelDev& L) { return L.mue_derived && !L.dist0; }
+// (slab levels read mu_c's ghost planes along axis 0, exchanged at setup)
+static bool derive_mue(const LevelDev& L) { return L.mue_derived != 0; }
 
 static bool odd_periodic(const LevelDev& L, int dim) {
   for (int a = 3 - dim; a < 3; ++a)
@@ -2137,8 +2148,10 @@ static bool odd_periodic(const LevelDev& L, int dim) {
 
 template <int DIM, int FM, int A>
 static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0) {
+                          int parity, double omega, int z = 0, int ext0 = 0) {
   Box b = face_box(L, DIM, A);
+  b.lo[0] -= ext0;  // slab levels: also relax the ghost planes (sb_dist.inc dsweep_face)
+  b.hi[0] += ext0;
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
@@ -2169,7 +2182,7 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
 }
 
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z) {
+                        const double* rhsA, int parity, double omega, int z, int ext0) {
   ++g_kernel_launches;
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
@@ -2180,12 +2193,12 @@ void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, in
   }
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z);
-      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z);
-      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z);
+      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
     } else {
-      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z);
-      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z);
+      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
     }
   });
 }
@@ -2207,12 +2220,14 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 
 template <int DIM>
 static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0) {
+                          int parity, double omega, int z = 0, int ext0 = 0) {
   Box b = cell_box(L);
+  b.lo[0] -= ext0;
+  b.hi[0] += ext0;
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
-  const L3 c3 = cfg3(L.n[0], L.n[1], (int)half2);
+  const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, L.n[1], (int)half2);
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr && z == 3) {
     launch_k(k_cell_colour<DIM, 0, 1, 3>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total);
@@ -2228,10 +2243,10 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
 }
 
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z) {
+                        int parity, double omega, int z, int ext0) {
   ++g_kernel_launches;
-  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z);
-  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z);
+  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
+  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
 }
 
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
@@ -2614,6 +2629,14 @@ void launch_sum_abs_partial(cudaStream_t s, const double* x, long long n, double
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x) {
   ++g_kernel_launches;
   launch_k(k_add_scalar, 1, 1, 0, s, y, x);
+}
+void launch_max_scalar(cudaStream_t s, double* y, const double* x, bool neg) {
+  ++g_kernel_launches;
+  launch_k(k_max_scalar, 1, 1, 0, s, y, x, neg ? 1 : 0);
+}
+void launch_neg_copy(cudaStream_t s, double* y, const double* x) {
+  ++g_kernel_launches;
+  launch_k(k_neg_copy, 1, 1, 0, s, y, x);
 }
 
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x) {

@@ -52,11 +52,12 @@ struct CoarseChain {
 // colour passes (multigrid.py:318-340)
 // z: first-sweep-from-zero variants (k_face_colour): 0 plain, 1 later
 // components zero, 2 also the relaxed array zero, 3 as 2 + store the partner's
-// zero (replaces the zero fill; all-periodic pad-free levels only)
+// zero (replaces the zero fill; all-periodic pad-free levels only).
+// ext0: also relax ext0 ghost planes on each side of axis 0 (slab levels)
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z = 0);
+                        const double* rhsA, int parity, double omega, int z = 0, int ext0 = 0);
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z = 0);
+                        int parity, double omega, int z = 0, int ext0 = 0);
 // two-phase variants for levels with an odd periodic extent (same-colour
 // cells couple through the wrap): compute all, then update (reference order)
 void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
@@ -143,6 +144,8 @@ void launch_box_add_scalar(cudaStream_t s, const LevelDev& L, Box b, double* x, 
                            double inv_count);  // x -= sum*inv_count
 void launch_axpy_box(cudaStream_t s, const LevelDev& L, Box b, double* y, const double* x);  // y += x
 void launch_axpy_scalar(cudaStream_t s, double* y, const double* x);  // *y += *x (one thread)
+void launch_max_scalar(cudaStream_t s, double* y, const double* x, bool neg);  // *y = max(*y, +-*x)
+void launch_neg_copy(cudaStream_t s, double* y, const double* x);             // *y = -*x
 // inhomogeneous walls (operators.py:267-291, 484-512)
 void launch_wall_tangent(cudaStream_t s, const LevelDev& L, int A, int B, int side, const double* plane,
                          double* out);  // out_A -= 2 mu_e v / h^2 on the rows next to wall (B, side)

@@ -84,10 +84,10 @@ class DistSolver:
         return int(self.lib.sb_dist_stream(self.h) or 0)
 
     def info(self) -> dict:
-        out = (C.c_int * 4)()
+        out = (C.c_int * 6)()
         self.lib.sb_dist_info(self.h, out)
         return {"distributed_levels": out[0], "agglomerated_levels": out[1], "planes_per_slab": out[2],
-                "slabs": out[3]}
+                "slabs": out[3], "mue_derived_levels": out[4], "const_rho_levels": out[5]}
 
     #: arrays passed in already hold only this rank's planes (bench: slab-local generation)
     local_inputs = False

@@ -28,6 +28,12 @@ def test_dist_operator_and_precond_match_single(name, n, nslab):
     D.set_coefficients(cs)
     info = D.info()
     assert info["slabs"] == nslab and info["distributed_levels"] >= 1
+    # slab levels take the same specialisations as the single domain: derived
+    # edge viscosities on all-periodic finest levels, one 1/rho on constant density
+    if name in ("C3", "C5"):
+        assert info["mue_derived_levels"] & 1 and info["const_rho_levels"] & 1
+    else:
+        assert info["mue_derived_levels"] == 0 and info["const_rho_levels"] == 0
     mu, mp = D.apply_M(rs)
     ref = apply_M(rs, cs)
     for a in range(3):
@@ -43,7 +49,7 @@ def test_dist_operator_and_precond_match_single(name, n, nslab):
 
 
 @pytest.mark.parametrize("name,n,nslab,kind", [("C5", 32, 2, "P1"), ("C5", 64, 4, "P1"), ("C4", 32, 2, "P1"),
-                                               ("C3", 64, 4, "P2")])
+                                               ("C3", 64, 4, "P2"), ("C5", 32, 1, "P1"), ("C4", 32, 1, "P1")])
 def test_dist_gmres_matches_single_and_oracle(name, n, nslab, kind):
     from paper_1308_4605_b200.dist import DistSolver
     from paper_1308_4605_b200.grid import pack_stokes, StokesVector, FaceField, CellField
@@ -66,3 +72,50 @@ def test_dist_gmres_matches_single_and_oracle(name, n, nslab, kind):
     r2 = np.array(h2.rows())[:, 2]
     k = min(len(r1), len(r2))
     assert np.allclose(r1[:k], r2[:k], rtol=1e-6)
+
+
+@pytest.mark.parametrize("name,n,nslab", [("C5", 32, 2), ("C4", 32, 4)])
+def test_dist_ghost_plane_red_pass_matches_per_pass_exchange(name, n, nslab, monkeypatch):
+    """The red pass relaxing the ghost planes (one exchange per component sweep)
+    gives the per-colour-pass exchange result: every slab computes exactly the
+    ghost values its neighbour computes, so P^-1 is bit-identical."""
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    case, cs, rs = _case(name, n)
+    out = {}
+    for ext in ("1", "0"):
+        monkeypatch.setenv("SB_DIST_EXT", ext)
+        D = DistSolver(case.grid, cs.viscous_form, nslab=nslab)
+        D.set_coefficients(cs)
+        xu, xp = D.precond_apply(rs, PrecondConfig(kind=P1))
+        out[ext] = [a.copy() for a in xu] + [xp.copy()]
+        del D
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+
+
+def test_dist_graph_kept_across_coefficient_uploads():
+    """The captured P^-1 graph survives a coefficient upload of the same problem
+    class (arrays rewritten in place): a second solve with new coefficients is
+    bit-identical to a fresh context's."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    gcfg = GmresConfig(restart=50, max_iters=500, rtol=1e-9, track_true_residual=False)
+    pc = PrecondConfig(kind=P1)
+    c1, c2 = PR.make_case("C5", 32, seed=11), PR.make_case("C5", 32, seed=12)
+    cs1, rs1, _ = PR.prepare(c1)
+    cs2, rs2, _ = PR.prepare(c2)
+    D = DistSolver(c1.grid, cs1.viscous_form, nslab=2)
+    D.set_coefficients(cs1)
+    D.gmres_solve(rs1, pc, gcfg)
+    D.set_coefficients(cs2)
+    xa, pa, ha = D.gmres_solve(rs2, pc, gcfg)
+    F = DistSolver(c2.grid, cs2.viscous_form, nslab=2)
+    F.set_coefficients(cs2)
+    xb, pb, hb = F.gmres_solve(rs2, pc, gcfg)
+    assert ha.iterations == hb.iterations
+    for a, b in zip(xa, xb):
+        assert np.array_equal(a, b)
+    assert np.array_equal(pa, pb)
