@@ -482,9 +482,13 @@ def run_dist(args, rank, world, local):
     gcfg = GmresConfig(restart=50, max_iters=500, rtol=1e-9, atol=0.0, track_true_residual=False)
     stream = torch.cuda.ExternalStream(D.stream_ptr(), device=dev)
 
+    # solution into HBM-resident tensors (the single-GPU arm's solve_raw contract)
+    dxu = [torch.zeros_like(c) for c in drhs.u.components]
+    dxp = torch.zeros_like(drhs.p.data)
+
     def step():
         D.set_coefficients(dc)
-        return D.gmres_solve(drhs, pc, gcfg)
+        return D.gmres_solve(drhs, pc, gcfg, out=(dxu, dxp))
 
     hist = None
     for _ in range(max(args.warmup, 0)):
@@ -495,17 +499,31 @@ def run_dist(args, rank, world, local):
     clocks = Clocks(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = D.launch_count()
     e0.record(stream)
     for _ in range(args.steps):
         _, _, hist = step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ck = clocks.stop()
+    launches = D.launch_count() - l0
     ms = e0.elapsed_time(e1) / max(args.steps, 1)
     dist.barrier()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # roofline: instrumented solve (untimed, eager launches), finest-level face
+    # colour passes of this rank's slab (plain passes), as the 1-GPU arm
+    D.set_profiling(True)
+    step()
+    D.set_profiling(False)
+    st = D.kernel_stats()
+    peak, peak_src = peaks()
+    fl_bytes = st["fine_face_bytes"] / max(st["fine_face_launches"], 1)
+    fl_ms = st["fine_face_ms"] / max(st["fine_face_launches"], 1)
+    achieved = fl_bytes / (fl_ms * 1e-3) / 1e9 if fl_ms > 0 else None
+    sm_bytes = st["smoother_face_bytes"] + st["smoother_cell_bytes"]
+    sm_ms = st["smoother_face_ms"] + st["smoother_cell_ms"]
     # e2e: the same solve from pinned host arrays (each rank passes its planes)
     def pinned(a):
         tt = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
@@ -547,9 +565,16 @@ def run_dist(args, rank, world, local):
                        "parallelism": f"slab decomposition along axis 0 over {world} GPUs (NCCL)",
                        "distributed_levels": info["distributed_levels"],
                        "agglomerated_levels": info["agglomerated_levels"], "planes_per_gpu": info["planes_per_slab"]},
-            "roofline": None, "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d) * world,
-                                      "d2h_bytes_per_step": int(d2h) * world},
-            "gpu_launches": None, "clocks": ck, "cpu_baseline": None,
+            "roofline": {"bound": "hbm", "kernel": "k_face_colour (finest slab level, rank 0)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "bytes_per_launch": fl_bytes, "ms_per_launch": fl_ms, "peak_source": peak_src},
+            "smoother": {"GBps": sm_bytes / (sm_ms * 1e-3) / 1e9 if sm_ms > 0 else None,
+                         "frac": (sm_bytes / (sm_ms * 1e-3) / 1e9 / peak) if sm_ms > 0 else None,
+                         "face_ms_per_solve": st["smoother_face_ms"], "cell_ms_per_solve": st["smoother_cell_ms"]},
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d) * world,
+                    "d2h_bytes_per_step": int(d2h) * world},
+            "gpu_launches": int(launches), "clocks": ck, "cpu_baseline": None,
         }
         print(json.dumps(out), flush=True)
     D.close()

@@ -246,6 +246,12 @@ sb_dist* sb_dist_create(const int* cells, double h, const int* bc, int viscous_f
 void sb_dist_destroy(sb_dist* dist);
 /* the CUDA stream the distributed context launches on (cudaStream_t) */
 void* sb_dist_stream(sb_dist* dist);
+/* measurement: CUDA events around every slab colour pass of the next solves
+ * (eager launches while enabled; sb_kernel_stats as for sb_ctx), and the
+ * kernels launched by this context (graph nodes counted per replay) */
+void sb_dist_set_profiling(sb_dist* dist, int enabled);
+int sb_dist_get_kernel_stats(sb_dist* dist, sb_kernel_stats* out);
+long long sb_dist_launch_count(sb_dist* dist);
 /* out[6] = {distributed levels, agglomerated levels, planes per slab, slabs in this process,
  *          bit l: distributed level l derives mu_e from mu_c, bit l: level l has constant 1/rho} */
 int sb_dist_info(sb_dist* dist, int* out);

@@ -29,6 +29,7 @@ EXPORTS = (
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
     "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
     "sb_dist_set_coefficients", "sb_dist_apply_M", "sb_dist_precond_apply", "sb_dist_gmres_solve",
+    "sb_dist_set_profiling", "sb_dist_get_kernel_stats", "sb_dist_launch_count",
     "sb_host_alloc", "sb_host_free",
 )
 
@@ -102,6 +103,9 @@ _SIGS = {
     "sb_host_alloc": (_P, [C.c_longlong]),
     "sb_host_free": (None, [_P]),
     "sb_dist_info": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "sb_dist_set_profiling": (None, [_P, C.c_int]),
+    "sb_dist_get_kernel_stats": (C.c_int, [_P, C.POINTER(KernelStats)]),
+    "sb_dist_launch_count": (C.c_longlong, [_P]),
     "sb_dist_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
     "sb_dist_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),
     "sb_dist_precond_apply": (C.c_int, [_P, C.POINTER(Precond), C.POINTER(Smoother), _PP, _P, _PP, _P]),

@@ -83,6 +83,18 @@ class DistSolver:
     def stream_ptr(self) -> int:
         return int(self.lib.sb_dist_stream(self.h) or 0)
 
+    # measurement (bench.py): per-colour-pass CUDA events, launch counting
+    def set_profiling(self, enabled: bool):
+        self.lib.sb_dist_set_profiling(self.h, int(bool(enabled)))
+
+    def kernel_stats(self) -> dict:
+        s = _lib.KernelStats()
+        self.lib.sb_dist_get_kernel_stats(self.h, C.byref(s))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def launch_count(self) -> int:
+        return int(self.lib.sb_dist_launch_count(self.h))
+
     def info(self) -> dict:
         out = (C.c_int * 6)()
         self.lib.sb_dist_info(self.h, out)
@@ -110,16 +122,20 @@ class DistSolver:
         del g
 
     def _out(self):
+        # recycled page-locked buffers (a pageable D2H runs at a third of PCIe speed)
         g = self.grid
         k = g.cells[0] // self.nranks
         shp = lambda s: (k,) + tuple(s[1:])
-        return [np.zeros(shp(g.face_shape(a))) for a in range(3)], np.zeros(shp(g.cells))
+        return [_lib.pinned.array(shp(g.face_shape(a))) for a in range(3)], _lib.pinned.array(shp(g.cells))
 
-    def gmres_solve(self, rhs, pcfg, gcfg, smoother=None):
-        """Solve with the GLOBAL rhs; returns this rank's planes of x and the history."""
+    def gmres_solve(self, rhs, pcfg, gcfg, smoother=None, out=None):
+        """Solve with the GLOBAL rhs; returns this rank's planes of x and the history.
+
+        ``out=(xu, xp)``: write the solution into these arrays (this rank's
+        planes; host arrays or device tensors -- the HBM-resident bench path)."""
         bu = [self._mine(c) for c in rhs.u.components]
         bp = self._mine(rhs.p.data)
-        xu, xp = self._out()
+        xu, xp = self._out() if out is None else (list(out[0]), out[1])
         nrows = int(gcfg.max_iters) + 2
         rows = (_lib.HistoryRow * nrows)()
         n_rows, status = C.c_int(0), C.c_int(0)
