@@ -2187,7 +2187,7 @@ void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, in
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
   // the solver routes those levels through launch_face_colour_tmp below.
-  if (z == 0 && rowv_colour_supported(L, dim, form)) {
+  if (z == 0 && !L.dist0 && rowv_colour_supported(L, dim, form)) {
     launch_face_colour_rv(s, L, form, A, u, rhsA, parity, omega);
     return;
   }

@@ -25,8 +25,9 @@
 // in the same order: results are bit-identical to the per-face kernels
 // (tests/test_gpu_rowv.py).
 //
-// Scope: 3D, all axes periodic, no slab decomposition, LAPLACIAN / STRESS
-// forms, contiguous extent a multiple of 64 (rowv_supported).
+// Scope: 3D, all axes periodic (a slab-distributed axis 0 reads ghost
+// planes), LAPLACIAN / STRESS forms, contiguous extent a multiple of 64
+// (rowv_supported).
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include "sb_kernels.h"
@@ -147,9 +148,10 @@ template <int W>
 __device__ __forceinline__ Seg make_seg(const LevelDev& L, int i, int j, int s, int t, int k0) {
   Seg g;
   g.base = i * L.s0 + j * L.s1 + s;
-  g.di[0] = (i == 0 ? L.n[0] - 1 : -1) * L.s0;
+  // a slab-distributed axis 0 reads its ghost planes instead of wrapping
+  g.di[0] = ((i == 0 && !L.dist0) ? L.n[0] - 1 : -1) * L.s0;
   g.di[1] = 0;
-  g.di[2] = (i == L.n[0] - 1 ? -(L.n[0] - 1) : 1) * L.s0;
+  g.di[2] = ((i == L.n[0] - 1 && !L.dist0) ? -(L.n[0] - 1) : 1) * L.s0;
   g.dj[0] = (j == 0 ? L.n[1] - 1 : -1) * L.s1;
   g.dj[1] = 0;
   g.dj[2] = (j == L.n[1] - 1 ? -(L.n[1] - 1) : 1) * L.s1;
@@ -537,7 +539,7 @@ bool rowv_colour_on() {
 }
 
 bool rowv_supported(const LevelDev& L, int dim, int form) {
-  if (dim != 3 || form == F_BULK || L.dist0 || !rowv_on()) return false;
+  if (dim != 3 || form == F_BULK || !rowv_on()) return false;
   for (int a = 0; a < 3; ++a)
     if (L.bclo[a] != BC_PER || L.n[a] < 2) return false;
   return L.n[2] % 64 == 0;
