@@ -38,6 +38,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int RT = 256;  // threads per CTA
+#ifndef RV_MINB
+#define RV_MINB 3
+#endif
 
 // ---- compile-time operand masks -------------------------------------------
 // A stencil operand at offset (o0, o1, o2) from the thread's face lives in
@@ -569,11 +572,11 @@ static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 r
   const int nb = blocks_for(L, 32);
   const bool de = L.mue_derived != 0;
   if (form == F_LAP) {
-    if (de) launch_k(k_face_all_rv<F_LAP, true, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
-    else launch_k(k_face_all_rv<F_LAP, false, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    if (de) launch_k(k_face_all_rv<F_LAP, true, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    else launch_k(k_face_all_rv<F_LAP, false, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
   } else {
-    if (de) launch_k(k_face_all_rv<F_STRESS, true, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
-    else launch_k(k_face_all_rv<F_STRESS, false, MODE_M, 3>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    if (de) launch_k(k_face_all_rv<F_STRESS, true, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
+    else launch_k(k_face_all_rv<F_STRESS, false, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
   }
 }
 
