@@ -1719,7 +1719,7 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
            const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials,
-           const double* __restrict__ means, long long bb) {
+           const double* __restrict__ means, long long bb, long long gh) {
   pdl_enter();
   __shared__ double acc[kThreads / 32];
   __shared__ double ds[kMaxVec];
@@ -1740,8 +1740,13 @@ k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double
     if (means) {
       const int b0 = (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
       const int b1 = (e1 >= bb) + (e1 >= 2 * bb) + (e1 >= 3 * bb);
-      const double ma = b0 == 0 ? m0 : (b0 == 1 ? m1 : (b0 == 2 ? m2 : m3));
-      const double mb = b1 == 0 ? m0 : (b1 == 1 ? m1 : (b1 == 2 ? m2 : m3));
+      double ma = b0 == 0 ? m0 : (b0 == 1 ? m1 : (b0 == 2 ? m2 : m3));
+      double mb = b1 == 0 ? m0 : (b1 == 1 ? m1 : (b1 == 2 ? m2 : m3));
+      if (gh) {  // slab blocks: the ghost planes at both block ends stay 0
+        const long long la = e - b0 * bb, lb = e1 - b1 * bb;
+        if (la < gh || la >= bb - gh) ma = 0.0;
+        if (lb < gh || lb >= bb - gh) mb = 0.0;
+      }
       if (ok0) {
         w0.x = w0.x - ma;
         w0.y = w0.y - ma;
@@ -2722,11 +2727,13 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
-                     double* out, long long n, double* partials, const double* means, long long block) {
+                     double* out, long long n, double* partials, const double* means, long long block,
+                     long long ghost) {
   ++g_kernel_launches;
   static const int grid_b = wave_grid(k_dcgs_b_g);
   g_red_blocks_used = grid_b;
-  launch_k(k_dcgs_b_g, grid_b, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2);
+  launch_k(k_dcgs_b_g, grid_b, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2,
+           ghost / 2);
 }
 
 __global__ void k_block_means(const double* __restrict__ sums, int4 slot, double inv_count, double* __restrict__ means) {

@@ -165,7 +165,7 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
 // blocks of `block` elements, at most 4)
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,
                      double* out, long long n, double* partials, const double* means = nullptr,
-                     long long block = 0);
+                     long long block = 0, long long ghost = 0);  // ghost: elements kept 0 at each block end
 // means[b] = sums[slot[b]] * inv_count (0 where slot[b] < 0), b < 4
 void launch_block_means(cudaStream_t s, const double* sums, const int* slot, double inv_count, double* means);
 // delayed-reorthogonalisation Arnoldi passes (see sb_solver.cu gmres())
