@@ -1716,6 +1716,10 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
 // (one streaming read of the basis).  means (nullable): the null-space
 // projection of w deferred from P^-1 -- w - means[b] on the b-th block of
 // bb double2 (the k_box_sub_mean expression, so w' is unchanged to the bit).
+// GH (slab blocks): the first and last gh double2 of each block are ghost
+// planes and keep 0 (a separate instantiation: the single-domain kernel's code
+// generation -- 47 registers, 5 CTAs/SM -- is unchanged).
+template <bool GH>
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double* __restrict__ d,
            const double* __restrict__ w, double* __restrict__ out, long long n2, double* __restrict__ partials,
@@ -1742,7 +1746,7 @@ k_dcgs_b_g(const double* __restrict__ Q, long long vstride, int nv, const double
       const int b1 = (e1 >= bb) + (e1 >= 2 * bb) + (e1 >= 3 * bb);
       double ma = b0 == 0 ? m0 : (b0 == 1 ? m1 : (b0 == 2 ? m2 : m3));
       double mb = b1 == 0 ? m0 : (b1 == 1 ? m1 : (b1 == 2 ? m2 : m3));
-      if (gh) {  // slab blocks: the ghost planes at both block ends stay 0
+      if (GH) {  // slab blocks: the ghost planes at both block ends stay 0
         const long long la = e - b0 * bb, lb = e1 - b1 * bb;
         if (la < gh || la >= bb - gh) ma = 0.0;
         if (lb < gh || lb >= bb - gh) mb = 0.0;
@@ -2730,10 +2734,17 @@ void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv,
                      double* out, long long n, double* partials, const double* means, long long block,
                      long long ghost) {
   ++g_kernel_launches;
-  static const int grid_b = wave_grid(k_dcgs_b_g);
-  g_red_blocks_used = grid_b;
-  launch_k(k_dcgs_b_g, grid_b, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means, block / 2,
-           ghost / 2);
+  static const int grid_b = wave_grid(k_dcgs_b_g<false>);
+  static const int grid_bg = wave_grid(k_dcgs_b_g<true>);
+  if (ghost) {
+    g_red_blocks_used = grid_bg;
+    launch_k(k_dcgs_b_g<true>, grid_bg, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means,
+             block / 2, ghost / 2);
+  } else {
+    g_red_blocks_used = grid_b;
+    launch_k(k_dcgs_b_g<false>, grid_b, kThreads, 0, s, Q, vstride, nv, d, w, out, n / 2, partials, means,
+             block / 2, ghost / 2);
+  }
 }
 
 __global__ void k_block_means(const double* __restrict__ sums, int4 slot, double inv_count, double* __restrict__ means) {
