@@ -129,6 +129,14 @@ const char* sb_last_error(void);
 int sb_set_coefficients(sb_ctx* ctx, double theta, const double* const* rho_face,
                         const double* mu_cell, const double* const* mu_edge,
                         const double* gamma_cell);
+/* Device-side make_coefficients (operators.py:107-125; averaging :81-104)
+ * followed by rescale with factor `scale` (operators.py:532-550, applied as
+ * cli.py:340-343 does; scale = 1 for none): only the cell arrays cross the
+ * boundary, the face densities and node/edge viscosities are averaged on the
+ * device, then as sb_set_coefficients.  Equal to the host path to the bit.
+ * gamma_cell may be NULL. */
+int sb_set_cell_coefficients(sb_ctx* ctx, double theta, const double* rho_cell, const double* mu_cell,
+                             const double* gamma_cell, double scale);
 
 /* operators.py:363-365 apply_M:  (A u + G p, -D u). */
 int sb_apply_M(sb_ctx* ctx, const double* const* u, const double* p,

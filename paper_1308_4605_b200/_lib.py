@@ -22,7 +22,7 @@ STATUS = {0: "converged", 1: "breakdown", 2: "maxiter"}
 
 #: every symbol declared in include/stokesb200.h (checked by the CPU tests)
 EXPORTS = (
-    "sb_create", "sb_destroy", "sb_last_error", "sb_set_coefficients", "sb_apply_M",
+    "sb_create", "sb_destroy", "sb_last_error", "sb_set_coefficients", "sb_set_cell_coefficients", "sb_apply_M",
     "sb_apply_A", "sb_apply_A_affine", "sb_homogenize", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
     "sb_num_levels", "sb_level_flags", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
@@ -69,6 +69,7 @@ _SIGS = {
     "sb_create": (_P, [C.c_int, C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_int), C.c_int]),
     "sb_destroy": (None, [_P]),
     "sb_last_error": (C.c_char_p, []),
+    "sb_set_cell_coefficients": (C.c_int, [_P, C.c_double, _P, _P, _P, C.c_double]),
     "sb_set_coefficients": (C.c_int, [_P, C.c_double, _PP, _P, _PP, _P]),
     "sb_apply_M": (C.c_int, [_P, _PP, _P, _PP, _P]),
     "sb_apply_A": (C.c_int, [_P, _PP, _PP]),

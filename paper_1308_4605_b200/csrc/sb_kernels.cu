@@ -1012,6 +1012,46 @@ __device__ double edge_ref(const LevelDev& L, int e, const int* ci) {
   return 0.5 * (arr1(jh) + arr1(wrapa(jh - 1, nh, ah)));
 }
 
+// ---- device-side coefficient averaging (operators.py:81-104, :133-145) ----
+// rho_face[A] = 0.5 (rho[i] + rho[i-1]) along A (periodic wrap), wall
+// boundary faces copy the adjacent cell -- to_stagger_mean's expression.
+__global__ void k_cell_to_face(LevelDev L, int A, const double* __restrict__ cell, double* __restrict__ face, Box b) {
+  pdl_enter();
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  const int f = lin(L, ci);
+  const int sA = A == 0 ? L.s0 : (A == 1 ? L.s1 : 1);
+  double v;
+  if (L.bclo[A] != BC_PER) {
+    if (ci[A] == 0) v = __ldg(cell + f);
+    else if (ci[A] == L.n[A]) v = __ldg(cell + f - sA);
+    else v = 0.5 * (__ldg(cell + f) + __ldg(cell + f - sA));
+  } else {
+    const int lo = ci[A] == 0 ? f + (L.n[A] - 1) * sA : f - sA;
+    v = 0.5 * (__ldg(cell + f) + __ldg(cell + lo));
+  }
+  face[f] = v;
+}
+
+// mu_e (edge with normal axis e; 2D: the node array) = scale * edge_ref:
+// to_stagger_mean along the lower plane axis, then the upper (make_coef), then
+// rescale's multiplication (operators.py:532-550) -- the host's operation order.
+template <int DIM>
+__device__ double edge_ref(const LevelDev& L, int e, const int* ci);
+template <int DIM>
+__global__ void k_cell_to_edge(LevelDev L, int e, double* __restrict__ out, double scale, Box b) {
+  pdl_enter();
+  int ci[3];
+  if (!box_point(b, ci)) return;
+  out[lin(L, ci)] = scale * edge_ref<DIM>(L, e, ci);
+}
+
+__global__ void k_scale(double* __restrict__ x, double scale, long long n) {
+  pdl_enter();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = scale * x[i];
+}
+
 // Does every edge (3D) / node (2D) viscosity of a level equal edge_ref to
 // roundoff?  The reference builds mu_e exactly that way (operators.py:90-104)
 // and rescale multiplies both by c (operators.py:532-550), so on the finest
@@ -2589,6 +2629,29 @@ void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int
     if (dim == 3) launch_k(k_check_diag<3, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
     else launch_k(k_check_diag<2, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
   });
+}
+
+void launch_cell_to_face(cudaStream_t s, const LevelDev& L, int dim, int A, const double* cell, double* face) {
+  ++g_kernel_launches;
+  Box b = cell_box(L);
+  if (L.bclo[A] != BC_PER) b.hi[A] += 1;
+  if (dim == 2) b.hi[0] = 0;
+  launch_k(k_cell_to_face, cfg3(b).g, cfg3(b).b, 0, s, L, A, cell, face, b);
+}
+
+void launch_cell_to_edge(cudaStream_t s, const LevelDev& L, int dim, int e, double* out, double scale) {
+  ++g_kernel_launches;
+  Box b = cell_box(L);
+  for (int a = 0; a < 3; ++a)
+    if (a != e && L.bclo[a] != BC_PER) b.hi[a] += 1;
+  if (dim == 2) b.hi[0] = 0;
+  if (dim == 3) launch_k(k_cell_to_edge<3>, cfg3(b).g, cfg3(b).b, 0, s, L, e, out, scale, b);
+  else launch_k(k_cell_to_edge<2>, cfg3(b).g, cfg3(b).b, 0, s, L, e, out, scale, b);
+}
+
+void launch_scale(cudaStream_t s, double* x, double scale, long long n) {
+  ++g_kernel_launches;
+  launch_k(k_scale, grid_for(n), kThreads, 0, s, x, scale, n);
 }
 
 void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag) {

@@ -136,6 +136,11 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
 void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag,
                  int* cflag = nullptr, const double* ref = nullptr);
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags);
+// device-side make_coefficients + rescale: rho_face[A] from rho_cell, mu_e[e]
+// = scale * edge mean of L.mu_c (unscaled at the call), x *= scale
+void launch_cell_to_face(cudaStream_t s, const LevelDev& L, int dim, int A, const double* cell, double* face);
+void launch_cell_to_edge(cudaStream_t s, const LevelDev& L, int dim, int e, double* out, double scale);
+void launch_scale(cudaStream_t s, double* x, double scale, long long n);
 // all-periodic level: flag |= 1 unless mu_e == edge_mean(mu_c) to roundoff everywhere
 void launch_check_mue(cudaStream_t s, const LevelDev& L, int dim, int* flag);
 // box utilities

@@ -93,6 +93,7 @@ struct sb_ctx {
   // all-periodic level 0 only: the pass subtracts per-block means from every
   // element of a block, pads included)
   bool defer_nulls = false;
+  double* cscratch = nullptr;  // cell-layout scratch (sb_set_cell_coefficients: rho_cell)
   int* dflags = nullptr;
   double* dpart = nullptr;
   double* dsmall = nullptr;   // [h1 kMaxVec][h2 kMaxVec][misc 64][y kMaxVec]
@@ -1502,6 +1503,44 @@ int sb_set_coefficients(sb_ctx* c, double theta, const double* const* rho_face, 
       copy_in(c, L0, 10, mu_edge[2], L0.mu_e[0]);
     } else {
       copy_in(c, L0, 10, mu_edge[0], L0.mu_e[0]);
+    }
+    build_from_level0(c);
+    c->have_coef = true;
+    return SB_OK;
+  });
+}
+
+// Device-side make_coefficients (operators.py:107-125: face densities and
+// node/edge viscosities averaged from the cells, :81-104) followed by rescale
+// (operators.py:532-550 / cli.py:340-343: theta, mu, mu_e, gamma times
+// `scale`; the edge means are formed from the unscaled mu and then scaled, the
+// host's operation order, so every array equals the host path's to the bit).
+// Uploads 2-3 cell arrays instead of 2 + d + (1|3).
+int sb_set_cell_coefficients(sb_ctx* c, double theta, const double* rho_cell, const double* mu_cell,
+                             const double* gamma_cell, double scale) {
+  return guard([&]() -> int {
+    if (!(theta >= 0)) throw ArgErr(SB_EINVAL, "theta must be >= 0");
+    if (!(scale > 0)) throw ArgErr(SB_EINVAL, "scale must be > 0");
+    const double th = scale * theta;
+    if (!c->have_coef || th != c->theta) drop_graph(c);
+    c->theta = th;
+    for (auto& L : c->lv) L.d.theta = th;
+    Level& L0 = c->lv[0];
+    if (!c->cscratch) c->cscratch = dalloc(c, L0.block);
+    copy_in(c, L0, -1, rho_cell, c->cscratch);
+    for (int A = c->off; A < 3; ++A) launch_cell_to_face(c->st, L0.d, c->dim, A, c->cscratch, L0.rho_f[A]);
+    copy_in(c, L0, -1, mu_cell, L0.mu_c);
+    if (c->dim == 3) {
+      for (int e = 0; e < 3; ++e) launch_cell_to_edge(c->st, L0.d, 3, e, L0.mu_e[e], scale);
+    } else {
+      launch_cell_to_edge(c->st, L0.d, 2, 0, L0.mu_e[0], scale);
+    }
+    launch_scale(c->st, L0.mu_c, scale, L0.block);
+    if (gamma_cell) {
+      copy_in(c, L0, -1, gamma_cell, L0.gam_c);
+      launch_scale(c->st, L0.gam_c, scale, L0.block);
+    } else {
+      CK(cudaMemsetAsync(L0.gam_c, 0, L0.block * 8, c->st));
     }
     build_from_level0(c);
     c->have_coef = true;

@@ -224,6 +224,24 @@ class DeviceContext:
         self.theta = float(coeff.theta)
         self._keep = (rho, mu, edges, gam)
 
+    def set_cell_coefficients(self, theta, rho_cell, mu_cell, gamma_cell=None, scale: float = 1.0):
+        """make_coefficients + rescale ON THE DEVICE (sb_set_cell_coefficients):
+        only the cell arrays are uploaded; rho_face and the node/edge viscosities
+        are averaged on the device and (theta, mu, mu_e, gamma) multiplied by
+        ``scale`` -- equal to ``set_coefficients(rescale(make_coefficients(...)))``
+        to the bit (operators.py:107-125, :532-550)."""
+        g = self.grid
+        rho = _f64(getattr(rho_cell, "data", rho_cell))
+        mu = _f64(getattr(mu_cell, "data", mu_cell))
+        gam = None if gamma_cell is None else _f64(getattr(gamma_cell, "data", gamma_cell))
+        for a in (rho, mu) + ((gam,) if gam is not None else ()):
+            if tuple(a.shape) != tuple(g.cells):
+                raise ValueError("cell array layout does not match the grid")
+        _lib.check(self.lib.sb_set_cell_coefficients(self.h, float(theta), _lib.ptr(rho), _lib.ptr(mu),
+                                                      _lib.ptr(gam) if gam is not None else None, float(scale)))
+        self.theta = float(scale) * float(theta)
+        self._keep = (rho, mu, gam)
+
     def num_levels(self) -> int:
         return self.lib.sb_num_levels(self.h)
 
