@@ -2204,7 +2204,19 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
-  const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
+  L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, b.hi[1] - b.lo[1] + 1, (int)half2);
+  // threads along the row: two warps per row segment (64 same-colour faces,
+  // 4 rows per CTA) on rows of >= 128 faces -- measured 164 vs 166-168 us per
+  // finest pass against one warp x 8 rows (C5 256^3); SB_FC_BX overrides
+  static const int bx_env = [] {
+    const char* e = std::getenv("SB_FC_BX");
+    return e ? std::atoi(e) : 64;
+  }();
+  if (bx_env > 0 && (int)half2 >= bx_env && c3.b.x == 32) {
+    const int by = kThreads / bx_env;
+    c3.b = dim3(bx_env, by, 1);
+    c3.g = dim3((half2 + bx_env - 1) / bx_env, (b.hi[1] - b.lo[1] + 1 + by - 1) / by, b.hi[0] - b.lo[0] + 1);
+  }
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr && z == 3) {  // all-periodic pad-free level (zero_fill_free)
     if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, 1, true, 3>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
