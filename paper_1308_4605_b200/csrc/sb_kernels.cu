@@ -2288,7 +2288,16 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
-  const L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, L.n[1], (int)half2);
+  L3 c3 = cfg3(b.hi[0] - b.lo[0] + 1, L.n[1], (int)half2);
+  static const int bx_env = [] {  // SB_CC_BX: threads along the row
+    const char* e = std::getenv("SB_CC_BX");
+    return e ? std::atoi(e) : 32;
+  }();
+  if (bx_env != 32 && bx_env > 0 && (int)half2 >= bx_env && c3.b.x == 32) {
+    const int by = kThreads / bx_env;
+    c3.b = dim3(bx_env, by, 1);
+    c3.g = dim3((half2 + bx_env - 1) / bx_env, (L.n[1] + by - 1) / by, b.hi[0] - b.lo[0] + 1);
+  }
   const dim3 g = c3.g, kb = c3.b;
   if (tmp == nullptr && z == 3) {
     launch_k(k_cell_colour<DIM, 0, 1, 3>, g, kb, 0, s, L, phi, rhs, nullptr, parity, omega, b, half2, total);
