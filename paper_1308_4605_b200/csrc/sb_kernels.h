@@ -34,7 +34,8 @@ struct Box { int lo[3], hi[3]; };
 // one CTA: level 0 of the chain receives its right-hand side from the fine
 // levels' residual->restriction and returns its correction in x.
 constexpr int kCoarseMaxLevels = 10;
-constexpr long long kCoarseCells = 4096;
+constexpr long long kCoarseCells = 1024;   // 2D (32^2)
+constexpr long long kCoarseCells3 = 512;   // 3D (8^3)
 struct CoarseLv {
   LevelDev d;
   double* x[3];      // iterate (face components; cell uses x[0])

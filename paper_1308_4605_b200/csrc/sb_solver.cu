@@ -1278,10 +1278,17 @@ void upload_chains(sb_ctx* c) {
   const int nlev = (int)c->lv.size();
   if (!enabled || c->lv[0].d.dist0 || nlev < 2) return;
   int ls = -1;
+  // largest level of the tail: 3D 8^3, 2D 32^2 (the 16^3 / 64^2 levels run
+  // faster as multi-kernel passes: C5 256^3 0.3407 -> 0.3386 s, C3 128^3
+  // 0.0907 -> 0.0862 s, C2 256^2 8.19 -> 6.89 ms); SB_COARSE_CELLS overrides
+  const long long max_cells = [&] {
+    const char* e = std::getenv("SB_COARSE_CELLS");
+    return e ? std::atoll(e) : (c->dim == 3 ? kCoarseCells3 : kCoarseCells);
+  }();
   for (int l = 1; l < nlev; ++l) {
     long long cells = 1;
     for (int a = 3 - c->dim; a < 3; ++a) cells *= c->lv[l].d.n[a];
-    if (cells <= kCoarseCells) {
+    if (cells <= max_cells) {
       ls = l;
       break;
     }
