@@ -148,3 +148,39 @@ def test_dist_solution_into_device_tensors_and_stats():
     assert np.array_equal(dp.cpu().numpy(), xp)
     st = D.kernel_stats()
     assert st["fine_face_launches"] > 0 and st["fine_face_ms"] > 0 and st["smoother_cell_launches"] > 0
+
+
+@pytest.mark.parametrize("name,n,nslab", [("C5", 64, 2), ("C5", 64, 4), ("C4", 64, 2), ("C3", 64, 4)])
+def test_dist_split_residual_restriction(name, n, nslab, monkeypatch):
+    """Slab levels with the split residual -> restriction (residual field,
+    ghost-plane exchange of component 0, light restriction; the default on
+    slab levels >= 64^3 cells), forced onto every slab level here: the same
+    P1 application as the single domain and the fused slab path, and GMRES
+    with the single-domain iteration count."""
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case, cs, rs = _case(name, n)
+    pc = PrecondConfig(kind=P1)
+    monkeypatch.setenv("SB_DIST_RR_SPLIT", "0")
+    F = DistSolver(case.grid, cs.viscous_form, nslab=nslab)
+    F.set_coefficients(cs)
+    fu, fp = F.precond_apply(rs, pc)
+    monkeypatch.setenv("SB_DIST_RR_SPLIT", "1")
+    D = DistSolver(case.grid, cs.viscous_form, nslab=nslab)
+    D.set_coefficients(cs)
+    xu, xp = D.precond_apply(rs, pc)
+    want = Preconditioner(cs, pc).apply(rs)
+    for a in range(3):
+        s = np.abs(want.u.components[a]).max()
+        assert np.abs(xu[a] - want.u.components[a]).max() <= 1e-11 * s, a
+        assert np.abs(xu[a] - fu[a]).max() <= 1e-11 * s, a
+    assert np.abs(xp - want.p.data).max() <= 1e-11 * np.abs(want.p.data).max()
+    assert np.abs(xp - fp).max() <= 1e-11 * np.abs(want.p.data).max()
+    gcfg = GmresConfig(restart=case.restart, max_iters=500, rtol=1e-9, track_true_residual=False)
+    xd_u, xd_p, hd = D.gmres_solve(rs, pc, gcfg)
+    x1, h1 = gmres_solve(rs, cs, pc, gcfg)
+    assert hd.status == "converged" and abs(hd.iterations - h1.iterations) <= 1
+    num = sum(np.sum((xd_u[a] - x1.u.components[a]) ** 2) for a in range(3)) + np.sum((xd_p - x1.p.data) ** 2)
+    den = sum(np.sum(x1.u.components[a] ** 2) for a in range(3)) + np.sum(x1.p.data ** 2)
+    assert np.sqrt(num / den) <= 1e-8
