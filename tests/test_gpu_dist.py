@@ -184,3 +184,23 @@ def test_dist_split_residual_restriction(name, n, nslab, monkeypatch):
     num = sum(np.sum((xd_u[a] - x1.u.components[a]) ** 2) for a in range(3)) + np.sum((xd_p - x1.p.data) ** 2)
     den = sum(np.sum(x1.u.components[a] ** 2) for a in range(3)) + np.sum(x1.p.data ** 2)
     assert np.sqrt(num / den) <= 1e-8
+
+
+def test_dist_default_split_at_128():
+    """C5 recipe at 128^3 in 2 slabs: the slab levels of >= 64^3 cells take
+    the split residual -> restriction by default; GMRES matches the single
+    domain (iteration count +-1, solution <= 1e-8)."""
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    case, cs, rs = _case("C5", 128)
+    pc = PrecondConfig(kind=P1)
+    gcfg = GmresConfig(restart=case.restart, max_iters=500, rtol=1e-9, track_true_residual=False)
+    D = DistSolver(case.grid, cs.viscous_form, nslab=2)
+    D.set_coefficients(cs)
+    xu, xp, hd = D.gmres_solve(rs, pc, gcfg)
+    x1, h1 = gmres_solve(rs, cs, pc, gcfg)
+    assert hd.status == h1.status == "converged" and abs(hd.iterations - h1.iterations) <= 1
+    num = sum(np.sum((xu[a] - x1.u.components[a]) ** 2) for a in range(3)) + np.sum((xp - x1.p.data) ** 2)
+    den = sum(np.sum(x1.u.components[a] ** 2) for a in range(3)) + np.sum(x1.p.data ** 2)
+    assert np.sqrt(num / den) <= 1e-8
