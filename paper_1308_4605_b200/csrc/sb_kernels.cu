@@ -2212,7 +2212,11 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
     const char* e = std::getenv("SB_FC_BX");
     return e ? std::atoi(e) : 64;
   }();
-  if (bx_env > 0 && (int)half2 >= bx_env && c3.b.x == 32) {
+  static const int bx_min = [] {  // SB_FC_BX_MIN: shortest same-colour row taking it
+    const char* e = std::getenv("SB_FC_BX_MIN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (bx_env > 0 && (int)half2 >= std::max(bx_env, bx_min) && c3.b.x == 32) {
     const int by = kThreads / bx_env;
     c3.b = dim3(bx_env, by, 1);
     c3.g = dim3((half2 + bx_env - 1) / bx_env, (b.hi[1] - b.lo[1] + 1 + by - 1) / by, b.hi[0] - b.lo[0] + 1);
