@@ -241,7 +241,11 @@ void sb_host_free(void* ptr);
  * nranks x nslab slabs; a process owns nslab consecutive slabs.  nranks > 1:
  * one slab per process, one GPU per process, NCCL halo exchange / allreduce /
  * allgather (communicator from sb_nccl_unique_id on rank 0, broadcast by the
- * caller).  nranks == 1 with nslab > 1 runs the same decomposition on one GPU.
+ * caller).  nranks == 1 with nslab > 1 runs the same decomposition on one GPU
+ * (exchanges are device copies).  nranks == 1, nslab == 1 with a non-NULL
+ * nccl_id creates a 1-rank communicator: every exchange / reduction / gather
+ * takes the NCCL branch (self send/recv), i.e. exactly the code each rank runs
+ * at N > 1.  nranks > 1 with nccl_id == NULL is SB_EINVAL.
  * Array arguments hold THIS RANK's planes [rank*n0r, (rank+1)*n0r) of the
  * reference layouts (n0r = N0 / nranks).  Replaces the same seams as
  * sb_set_coefficients / sb_apply_M / sb_precond_apply / sb_gmres_solve
@@ -254,6 +258,12 @@ sb_dist* sb_dist_create(const int* cells, double h, const int* bc, int viscous_f
 void sb_dist_destroy(sb_dist* dist);
 /* the CUDA stream the distributed context launches on (cudaStream_t) */
 void* sb_dist_stream(sb_dist* dist);
+/* order the context after the caller's stream on entry to every public call
+ * (set_coefficients / apply_M / precond_apply / gmres_solve) and the caller's
+ * stream after the context on exit; NULL = no join (the default) */
+void sb_dist_set_stream(sb_dist* dist, void* stream);
+/* 1 when the context routes its exchanges through an NCCL communicator */
+int sb_dist_uses_nccl(sb_dist* dist);
 /* measurement: CUDA events around every slab colour pass of the next solves
  * (eager launches while enabled; sb_kernel_stats as for sb_ctx), and the
  * kernels launched by this context (graph nodes counted per replay) */

@@ -29,7 +29,8 @@ EXPORTS = (
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
     "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
     "sb_dist_set_coefficients", "sb_dist_apply_M", "sb_dist_precond_apply", "sb_dist_gmres_solve",
-    "sb_dist_set_profiling", "sb_dist_get_kernel_stats", "sb_dist_launch_count",
+    "sb_dist_set_profiling", "sb_dist_get_kernel_stats", "sb_dist_launch_count", "sb_dist_set_stream",
+    "sb_dist_uses_nccl",
     "sb_host_alloc", "sb_host_free",
 )
 
@@ -101,6 +102,8 @@ _SIGS = {
                             C.c_int, C.c_char_p]),
     "sb_dist_destroy": (None, [_P]),
     "sb_dist_stream": (_P, [_P]),
+    "sb_dist_set_stream": (None, [_P, _P]),
+    "sb_dist_uses_nccl": (C.c_int, [_P]),
     "sb_host_alloc": (_P, [C.c_longlong]),
     "sb_host_free": (None, [_P]),
     "sb_dist_info": (C.c_int, [_P, C.POINTER(C.c_int)]),

@@ -979,7 +979,7 @@ __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
     if (in_cell(L, ci)) {
       double dg;
       (void)cell_row<DIM>(L, L.mu_c, lin(L, ci), ci, dg);
-      if (dg == 0.0) atomicOr(flags, 2);
+      if (dg == 0.0) atomicOr(flags + 1, 1);  // cell diagonal: its own int (ranks max-reduce the flags)
     }
   }
 }

@@ -121,6 +121,7 @@ struct sb_ctx {
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   long long launches_base = 0;  // g_kernel_launches at creation
+  long long direct_norms = 0;   // GMRES steps that took the direct subdiagonal norm (near breakdown)
   long long graph_launches = 0; // kernel nodes replayed through graphs
   sb_kernel_stats stats{};
 };
@@ -1174,8 +1175,22 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
           ww = hh2(c)[j + 1];
         }
         for (int i = 0; i <= j; ++i) cc += hh2(c)[i] * hh2(c)[i];
-        const double g2 = std::max(ww - cc, 0.0);
-        const double gnext = std::sqrt(g2);
+        // ||w'||^2 - ||c'||^2 cancels as w' approaches span(Q) (near a
+        // breakdown): then materialise s_{j+1} = w' - Q_{j+1} c' in slot j+1
+        // and take its norm directly, as the reference's ||w|| (krylov.py:114);
+        // nothing stays pending for the next pass A
+        const bool direct = cc > 0.5 * ww;
+        double gnext;
+        if (direct) {
+          for (int i = 0; i <= j; ++i) hy(c)[i] = hh2(c)[i];
+          CK(cudaMemcpyAsync(dy(c), hy(c), (j + 1) * 8, cudaMemcpyHostToDevice, c->st));
+          launch_update_dot(c->st, V, vl, j + 1, dy(c), V + (long long)(j + 1) * vl, vl, c->dpart, 1);
+          launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
+          gnext = std::sqrt(fetch_misc(c, 1));
+          ++c->direct_norms;
+        } else {
+          gnext = std::sqrt(std::max(ww - cc, 0.0));
+        }
         for (int i = 0; i <= j; ++i) {
           double e = 0.0;
           for (int t = 0; t < j; ++t) e += Horig[i * m + t] * cpend[t];
@@ -1184,7 +1199,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         hn = gnext / gam;
         for (int i = 0; i <= j; ++i) Horig[i * m + j] = H[i * m + j];
         Horig[(j + 1) * m + j] = hn;
-        for (int i = 0; i <= j; ++i) cpend[i] = hh2(c)[i];
+        for (int i = 0; i <= j; ++i) cpend[i] = direct ? 0.0 : hh2(c)[i];
         gam = gnext;
       }
       H[(j + 1) * m + j] = hn;
@@ -1387,7 +1402,7 @@ void build_from_level0(sb_ctx* c) {
     if (changed) drop_graph(c);
     upload_chains(c);
     c->flag_face = hf[0] & 1;
-    c->flag_cell = (hf[0] >> 1) & 1;
+    c->flag_cell = hf[1] & 1;
     c->flag_rho = hf[2] & 1;
     // operators.py:368-388 velocity_null_components
     c->null_comps.clear();

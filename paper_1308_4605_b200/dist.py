@@ -14,6 +14,7 @@ layouts: ``rank_planes(x, nranks, rank)``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -64,12 +65,23 @@ class DistSolver:
     """One process's part of the slab-decomposed solve (3D, periodic axis 0)."""
 
     def __init__(self, grid, viscous_form, nranks: int = 1, rank: int = 0, nslab: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, nccl_self: bool | None = None):
+        """``nccl_id``: the communicator id every rank shares (``bootstrap_nccl_id``);
+        required when ``nranks > 1``.  ``nccl_self`` (default: environment
+        ``SB_DIST_NCCL_SELF=1``): with one rank and one slab, create a 1-rank
+        communicator anyway so every exchange / reduction / gather runs through
+        the NCCL branches each rank takes at N > 1 (self send/recv)."""
         self.lib = _lib.load()
         self.grid = as_grid(grid)
         g = self.grid
         if g.dim != 3:
             raise ValueError("the distributed path is 3D")
+        if nranks > 1 and nccl_id is None:
+            raise ValueError("nccl_id is required for a multi-rank solver (bootstrap_nccl_id)")
+        if nccl_self is None:
+            nccl_self = os.environ.get("SB_DIST_NCCL_SELF", "0") == "1"
+        if nranks == 1 and nslab == 1 and nccl_self and nccl_id is None:
+            nccl_id = nccl_unique_id()
         self.nranks, self.rank, self.nslab = nranks, rank, nslab
         cells = (C.c_int * 3)(*g.cells)
         bcs = (C.c_int * 6)(*[BC_CODE[x] for pair in g.bc for x in pair])
@@ -82,6 +94,15 @@ class DistSolver:
 
     def stream_ptr(self) -> int:
         return int(self.lib.sb_dist_stream(self.h) or 0)
+
+    def set_stream(self, stream_ptr: int | None):
+        """Join the caller's CUDA stream (e.g. ``torch.cuda.current_stream().cuda_stream``)
+        on entry to / exit from every call; None: no join."""
+        self.lib.sb_dist_set_stream(self.h, stream_ptr or None)
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(self.lib.sb_dist_uses_nccl(self.h))
 
     # measurement (bench.py): per-colour-pass CUDA events, launch counting
     def set_profiling(self, enabled: bool):

@@ -204,3 +204,118 @@ def test_dist_default_split_at_128():
     num = sum(np.sum((xu[a] - x1.u.components[a]) ** 2) for a in range(3)) + np.sum((xp - x1.p.data) ** 2)
     den = sum(np.sum(x1.u.components[a] ** 2) for a in range(3)) + np.sum(x1.p.data ** 2)
     assert np.sqrt(num / den) <= 1e-8
+
+
+# ---- the NCCL transport on one GPU (1-rank communicator, self send/recv) -------------
+
+
+@pytest.mark.parametrize("name,n,kind", [("C5", 32, "P1"), ("C4", 32, "P1"), ("C3", 64, "P2"), ("C5", 128, "P1")])
+def test_dist_nccl_self_matches_single(name, n, kind):
+    """One rank, one slab, routed through NCCL: every halo exchange is a grouped
+    ncclSend/ncclRecv to itself, every reduction an ncclAllReduce, the coarse
+    gather an ncclAllGather, and the P^-1 graph captures those NCCL nodes --
+    the branches each rank takes at N > 1.  The solve matches the single
+    domain (iterations +-1, solution <= 1e-8, r_P history 1e-6) and the
+    device-copy transport of the same one-slab layout."""
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.precond import PrecondConfig, PrecondKind
+    case, cs, rs = _case(name, n)
+    gcfg = GmresConfig(restart=case.restart, max_iters=500, rtol=1e-9, track_true_residual=False)
+    pc = PrecondConfig(kind=PrecondKind(kind))
+    x1, h1 = gmres_solve(rs, cs, pc, gcfg)
+    D = DistSolver(case.grid, cs.viscous_form, nslab=1, nccl_self=True)
+    assert D.uses_nccl
+    D.set_coefficients(cs)
+    xu, xp, hd = D.gmres_solve(rs, pc, gcfg)
+    assert hd.status == h1.status == "converged"
+    assert abs(hd.iterations - h1.iterations) <= 1
+    num = sum(np.sum((xu[a] - x1.u.components[a]) ** 2) for a in range(3)) + np.sum((xp - x1.p.data) ** 2)
+    den = sum(np.sum(x1.u.components[a] ** 2) for a in range(3)) + np.sum(x1.p.data ** 2)
+    assert np.sqrt(num / den) <= 1e-8
+    r1, r2 = np.array(h1.rows())[:, 2], np.array(hd.rows())[:, 2]
+    k = min(len(r1), len(r2))
+    assert np.allclose(r1[:k], r2[:k], rtol=1e-6)
+    # the device-copy transport of the same layout: the same arithmetic, so the
+    # same iterates (exchanges only move bytes; 1-rank reductions are copies)
+    F = DistSolver(case.grid, cs.viscous_form, nslab=1, nccl_self=False)
+    assert not F.uses_nccl
+    F.set_coefficients(cs)
+    fu, fp, hf = F.gmres_solve(rs, pc, gcfg)
+    assert hf.iterations == hd.iterations
+    for a in range(3):
+        assert np.array_equal(fu[a], xu[a])
+    assert np.array_equal(fp, xp)
+
+
+def test_dist_nccl_self_operator_precond_and_graph():
+    """apply_M, P^-1 (eager and graph-captured with NCCL nodes) through the
+    NCCL branches equal the single-domain operators; a second coefficient
+    upload keeps the captured graph and stays bit-identical to a fresh solver."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig
+    from paper_1308_4605_b200.operators import apply_M
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case, cs, rs = _case("C4", 64)
+    D = DistSolver(case.grid, cs.viscous_form, nslab=1, nccl_self=True)
+    D.set_coefficients(cs)
+    mu, mp = D.apply_M(rs)
+    ref = apply_M(rs, cs)
+    for a in range(3):
+        assert np.allclose(mu[a], ref.u.components[a], rtol=0, atol=1e-12 * np.abs(ref.u.components[a]).max())
+    assert np.allclose(mp, ref.p.data, rtol=0, atol=1e-12 * np.abs(ref.p.data).max())
+    want = Preconditioner(cs, PrecondConfig(kind=P1)).apply(rs)
+    xu, xp = D.precond_apply(rs, PrecondConfig(kind=P1))
+    for a in range(3):
+        assert np.abs(xu[a] - want.u.components[a]).max() <= 1e-11 * np.abs(want.u.components[a]).max()
+    assert np.abs(xp - want.p.data).max() <= 1e-11 * np.abs(want.p.data).max()
+    gcfg = GmresConfig(restart=50, max_iters=500, rtol=1e-9, track_true_residual=False)
+    c1, c2 = PR.make_case("C5", 32, seed=11), PR.make_case("C5", 32, seed=12)
+    cs1, rs1, _ = PR.prepare(c1)
+    cs2, rs2, _ = PR.prepare(c2)
+    E = DistSolver(c1.grid, cs1.viscous_form, nslab=1, nccl_self=True)
+    E.set_coefficients(cs1)
+    E.gmres_solve(rs1, PrecondConfig(kind=P1), gcfg)
+    E.set_coefficients(cs2)
+    xa, pa, ha = E.gmres_solve(rs2, PrecondConfig(kind=P1), gcfg)
+    F = DistSolver(c2.grid, cs2.viscous_form, nslab=1, nccl_self=True)
+    F.set_coefficients(cs2)
+    xb, pb, hb = F.gmres_solve(rs2, PrecondConfig(kind=P1), gcfg)
+    assert ha.iterations == hb.iterations
+    for a, b in zip(xa, xb):
+        assert np.array_equal(a, b)
+    assert np.array_equal(pa, pb)
+
+
+@pytest.mark.parametrize("nccl_self,nslab", [(True, 1), (False, 2), (False, 4)])
+@pytest.mark.parametrize("which", ["face", "cell"])
+def test_dist_zero_diagonal_raises(nccl_self, nslab, which):
+    """A zero smoother diagonal (mu = 0 rows with theta = 0 for the velocity
+    operator; for the pressure operator an infinite rho, i.e. 1/rho = 0) is
+    reported as
+    ZeroDivisionError (multigrid.py:74-75, 84-88) through every transport:
+    the per-slab flags are max-reduced, so each condition survives any number
+    of flagging slabs / ranks."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.grid import CellField
+    from paper_1308_4605_b200.krylov import GmresConfig
+    from paper_1308_4605_b200.operators import make_coefficients
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    case = PR.make_case("C5", 32)
+    g = case.grid
+    if which == "face":  # steady region of zero viscosity (tests/test_multigrid.py:75-83)
+        mu = np.zeros(g.cells)
+        mu[0, 0, 0] = 1.0
+        coeff = make_coefficients(g, 0.0, CellField.full(g, 1.0), CellField(g, mu))
+    else:
+        coeff = make_coefficients(g, 0.0, CellField.full(g, np.inf), CellField.full(g, 1.0))
+    D = DistSolver(g, coeff.viscous_form, nslab=nslab, nccl_self=nccl_self)
+    try:
+        D.set_coefficients(coeff)
+    except (ZeroDivisionError, ValueError):
+        return
+    gcfg = GmresConfig(restart=10, max_iters=5, rtol=1e-9, track_true_residual=False)
+    with pytest.raises((ZeroDivisionError, ValueError)):
+        D.gmres_solve(case.rhs, PrecondConfig(kind=P1), gcfg)
