@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--ref-iters", type=int, default=REF_ITERS, help="reference arm: GMRES iterations sampled")
+    ap.add_argument("--ref-n", type=int, default=None, help="reference arm: sample cells per axis")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the slab-decomposed (NCCL) path even with one rank (code-path check)")
     return ap.parse_args()
@@ -147,30 +149,118 @@ def _oracle_case(config, n, precond):
     return case, geo, oc, list(rs.u.components), rs.p.data
 
 
-def cpu_sample(config, target_cells, n_sample, k, precond, iterations):
-    """Time the oracle on the same recipe at n_sample^d: hierarchy setup, then a
-    GMRES run capped at k iterations (k+1 preconditioned-operator applications);
-    extrapolate linearly in cell count (every kernel is O(N)) to a full solve of
-    `iterations` iterations at n_target^d.  The oracle's per-application time
-    at small j under-counts the MGS cost of later iterations, so the
-    extrapolation is a lower bound on the reference's time."""
-    from oracle import stokes_oracle as O
-    case, geo, oc, bu, bp = _oracle_case(config, n_sample, precond)
+def reference_package():
+    """The UNMODIFIED reference ``stokesmg`` pip-installed into baseline/_ref
+    (DESIGN.md §7), or None when it is absent (then the oracle port stands in)."""
+    p = ROOT / "baseline" / "_ref"
+    if not (p / "stokesmg" / "__init__.py").exists():
+        return None
+    if str(p) not in sys.path:
+        sys.path.insert(0, str(p))
+    import stokesmg
+    return stokesmg
+
+
+def _ref_types(sm, case):
+    """The seeded recipe's arrays (the device arm's inputs) in the reference's types."""
+    from stokesmg import grid as G
+    from stokesmg import operators as OP
+    code = {"periodic": G.PERIODIC, "no_slip": G.NO_SLIP, "free_slip": G.FREE_SLIP}
+    g = G.GridSpec(tuple(case.grid.cells), case.grid.h,
+                   tuple((code[lo.value], code[hi.value]) for lo, hi in case.grid.bc))
+    c0 = case.coeff
+    coeff = OP.CoefficientSet(
+        theta=c0.theta, rho_cell=G.CellField(g, c0.rho_cell.data), rho_face=G.FaceField(g, c0.rho_face.components),
+        mu_cell=G.CellField(g, c0.mu_cell.data), mu_node_edge=G.NodeEdgeField(g, dict(c0.mu_node_edge.arrays)),
+        gamma_cell=G.CellField(g, c0.gamma_cell.data), viscous_form=OP.STRESS)
+    rhs = G.StokesVector(G.FaceField(g, case.rhs.u.components), G.CellField(g, case.rhs.p.data))
+    return coeff, rhs
+
+
+def _vector_op_s(n_u):
+    """Seconds of one (dot + axpy + x_k update) triple on length-n_u fp64 vectors
+    with NumPy: the per-basis-vector cost of the reference's MGS Arnoldi and of
+    its per-iteration ``x + V^T y`` (krylov.py:111-113, :132-133)."""
+    a = np.random.default_rng(0).standard_normal(n_u)
+    b = np.ones(n_u)
     t0 = time.perf_counter()
-    P = O.Precond(geo, oc, O.PrecondOpts(kind=precond))
-    t1 = time.perf_counter()
-    O.gmres_solve(geo, oc, bu, bp, P=P, gopts=O.GmresOpts(restart=case.restart, max_iters=k,
-                                                          track_true_residual=False))
-    t2 = time.perf_counter()
+    for _ in range(3):
+        h = float(a @ b)
+        b -= 1e-3 * h * a
+        b += 1e-3 * a
+    return (time.perf_counter() - t0) / 3
+
+
+def cpu_sample(config, target_cells, n_sample, k, precond, iterations):
+    """Time the REFERENCE's CPU path (baseline/_ref ``stokesmg``, unmodified, one
+    core) on the seeded recipe at n_sample cells per axis: ``Preconditioner``
+    construction (hierarchy), then ``gmres_solve(..., max_iters=k)`` (k + 1
+    P^-1 M applications), ``track_true_residual=False``.
+    Extrapolated to a full solve of ``iterations`` iterations at target_cells:
+    (setup + (iterations + 1 + restarts) x per-application time + the MGS /
+    x_k vector work of the later Arnoldi steps) x the cell ratio.  Falls back
+    to the oracle port when the reference is not installed (kind "port")."""
+    from paper_1308_4605_b200 import problems as PR
+    sm = reference_package()
+    case = PR.make_case(config, n_sample)
+    restart = case.restart
+    kind = "reference" if sm is not None else "port"
+    if sm is not None:
+        from stokesmg import operators as ROP
+        from stokesmg import precond as RPC
+        coeff, rhs = _ref_types(sm, case)
+        cs, rs, _ = ROP.rescale(coeff, rhs)
+        pcfg = RPC.PrecondConfig(kind=RPC.PrecondKind(precond))
+        gcfg = sm.GmresConfig(restart=restart, max_iters=k, rtol=1e-9, atol=0.0, track_true_residual=False)
+        t0 = time.perf_counter()
+        P = RPC.Preconditioner(cs, pcfg)
+        t1 = time.perf_counter()
+        _, hist = sm.gmres_solve(rs, cs, pcfg, gcfg, precond=P)
+        t2 = time.perf_counter()
+        n_u = sum(c.size for c in rs.u.components) + rs.p.data.size
+        who = "reference stokesmg 0.1.0 (baseline/_ref, unmodified, NumPy, 1 thread)"
+    else:
+        from oracle import stokes_oracle as O
+        case, geo, oc, bu, bp = _oracle_case(config, n_sample, precond)
+        t0 = time.perf_counter()
+        P = O.Precond(geo, oc, O.PrecondOpts(kind=precond))
+        t1 = time.perf_counter()
+        O.gmres_solve(geo, oc, bu, bp, P=P, gopts=O.GmresOpts(restart=restart, max_iters=k,
+                                                              track_true_residual=False))
+        t2 = time.perf_counter()
+        n_u = sum(x.size for x in bu) + bp.size
+        who = "oracle port of stokesmg (NumPy, 1 thread; reference not installed)"
     t_app = (t2 - t1) / (k + 1)
-    scale = float(math.prod(target_cells)) / float(n_sample) ** geo.dim
-    restarts = max(0, (iterations - 1) // case.restart)
-    t_full = scale * ((t1 - t0) + (iterations + 1 + restarts) * t_app)
-    sample = (f"oracle (NumPy port of stokesmg, 1 thread) on the {config} recipe at {n_sample}^{geo.dim}: "
-              f"hierarchy setup {t1 - t0:.2f}s + {k} GMRES iterations ({k + 1} P^-1 M applications, "
-              f"{t_app:.2f}s each), extrapolated x{scale:g} in cells to {iterations} iterations at "
-              f"{'x'.join(map(str, target_cells))}")
-    return t_full, t2 - t0, sample
+    t_vop = _vector_op_s(n_u)
+    dim = len(case.grid.cells)
+    scale = float(math.prod(target_cells)) / float(math.prod(case.grid.cells))
+    restarts = max(0, (iterations - 1) // restart)
+    js = [(i - 1) % restart for i in range(1, iterations + 1)]
+    mgs_extra = 3.0 * t_vop * (sum(js) - sum(js[:k]))
+    t_full = scale * ((t1 - t0) + (iterations + 1 + restarts) * t_app + mgs_extra)
+    cells_s = "x".join(map(str, case.grid.cells))
+    tgt_s = "x".join(map(str, target_cells))
+    sample = (f"{who} on the {config} recipe at {cells_s}: Preconditioner setup {t1 - t0:.2f} s + "
+              f"gmres_solve(max_iters={k}) {t2 - t1:.1f} s ({k + 1} P^-1 M applications, {t_app:.2f} s each); "
+              f"EXTRAPOLATED to {iterations} iterations ({restarts} restarts) at {tgt_s}"
+              + (f" (x{scale:g} cells)" if scale != 1 else "") +
+              f" incl. {mgs_extra:.1f} s of later-iteration MGS/x_k vector work ({t_vop * 1e3:.0f} ms per basis vector)")
+    info = {"kind": kind, "sample": sample, "sample_wall_s": t2 - t0, "setup_s": t1 - t0,
+            "per_application_s": t_app, "sample_iters": k, "sample_cells": list(case.grid.cells),
+            "extrapolated": True, "dim": dim}
+    return t_full, info
+
+
+def host_info():
+    model, cores = None, os.cpu_count()
+    try:
+        for ln in pathlib.Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_cores": cores}
 
 
 def bench_iterations(config, precond, default):
@@ -181,46 +271,56 @@ def bench_iterations(config, precond, default):
         return default, "default estimate"
 
 
+def workload(config, precond, n_gpus, n=None):
+    """The device arm's workload for N GPUs: (cells, restart, config dict).  The
+    config dict is identical in both arms (the driver compares them)."""
+    from paper_1308_4605_b200 import problems as PR
+    if config == "C5" and n_gpus > 1:
+        cells = tuple(PR.c5_cells(n_gpus))
+    else:
+        n_t = n or {"C1": 64, "C2": 256, "C3": 128, "C4": 256, "C5": 256}[config]
+        cells = (n_t,) * (2 if config in ("C1", "C2") else 3)
+    restart = 50 if config in ("C3", "C5") else 30
+    walls = "periodic" if config in ("C1", "C3", "C5") else "walls"
+    par = "single GPU" if n_gpus == 1 else (
+        f"{n_gpus} GPUs, axis-0 slabs (C5 weak scaling, 256^3 per GPU)" if config == "C5"
+        else f"{n_gpus} GPUs, axis-0 slabs (strong scaling)")
+    cfg = {"workload": f"{config} {'x'.join(map(str, cells))} {walls} {precond} GMRES({restart}) rtol 1e-9",
+           "precond": precond, "restart": restart, "cells": list(cells), "rtol": 1e-9, "seed": 1308,
+           "parallelism": par,
+           "l2": "every fine-level field (>= 134 MB at 256^3) exceeds the 126 MB L2; no flush needed"}
+    return cells, restart, cfg
+
+
+REF_ITERS = 3  # BASELINE.md §3 step 4: C4 / C5 run max_iters = 3 on the CPU
+
+
 def run_reference(args, rank, world):
+    """``--impl reference``: the reference's own CPU path, timed on this host.
+
+    Rank 0 alone runs (other ranks exit 0).  One measured sample at the device
+    arm's per-GPU size (256^3 for C4/C5; the full grid for C1-C3) with
+    ``max_iters=3``, extrapolated to the device arm's iteration
+    count and global grid; the warm-up / steps counts are recorded but the
+    sample is taken once (a single 256^3 sample is minutes of CPU)."""
     if rank != 0:
         return
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    from paper_1308_4605_b200 import problems as PR
     n_gpus = max(args.gpus, world)
-    # the device arm's workload: the single-GPU recipe, or C5's weak-scaling
-    # grid for N GPUs (bench.py --gpus N runs c5_cells(N) globally)
-    if n_gpus > 1 and args.config == "C5":
-        cells = tuple(PR.c5_cells(n_gpus))
-        restart, walls_s = 50, "periodic"
-    else:
-        n_t = args.n or (256 if args.config in ("C4", "C5") else (128 if args.config == "C3" else
-                                                                 (64 if args.config == "C1" else 256)))
-        dim = 2 if args.config in ("C1", "C2") else 3
-        cells = (n_t,) * dim
-        restart = 50 if args.config in ("C3", "C5") else 30
-        walls_s = "periodic" if args.config in ("C1", "C3", "C5") else "walls"
+    cells, restart, cfg = workload(args.config, args.precond, n_gpus, args.n)
     its, its_src = bench_iterations(args.config, args.precond, 40)
-    n_sample = min(cells[0], 128) if args.config in ("C3", "C4", "C5") else cells[0]
-    for _ in range(args.warmup):
-        cpu_sample(args.config, cells, max(8, n_sample // 4), 1, args.precond, its)
-    vals, walls = [], []
-    desc = ""
-    for _ in range(args.steps):
-        v, w, desc = cpu_sample(args.config, cells, n_sample, 1, args.precond, its)
-        vals.append(v)
-        walls.append(w)
-    v = statistics.mean(vals)
+    n_sample = args.ref_n or (min(cells[0], 256) if len(cells) == 3 else cells[0])
+    k = args.ref_iters
+    v, info = cpu_sample(args.config, cells, n_sample, k, args.precond, its)
+    info.update(host_info())
+    info["iterations_assumed"] = its
+    info["iterations_source"] = its_src
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded recipe, SURVEY §8d)",
-        "config": {"workload": f"{args.config} {'x'.join(map(str, cells))} {walls_s} {args.precond} "
-                               f"GMRES({restart}) rtol 1e-9",
-                   "precond": args.precond, "cells": list(cells), "iterations_assumed": its,
-                   "iterations_source": its_src},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
-                         "sample_wall_s": statistics.mean(walls)},
+        "higher_is_better": False, "scaling": "weak" if args.config == "C5" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded recipe, SURVEY §8d)", "config": cfg,
+        "cpu_baseline": dict(value=v, unit="s", cores=1, **info),
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -322,7 +422,9 @@ def main():
 
     # ---- roofline: instrumented solve (untimed) -------------------------------
     P.set_profiling(True)
+    P.scalar_vcycles = 0  # the counter accumulates over solves on a reused Preconditioner
     step()
+    vc_solve = P.scalar_vcycles
     P.set_profiling(False)
     st = P.kernel_stats()
     peak, peak_src = peaks()
@@ -384,11 +486,12 @@ def main():
     iters = hist.iterations
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample (~30 s of CPU): the reference at 128^3, one GMRES
+        # iteration; the full 256^3 measurement is the --impl reference arm
         n_t = case.grid.cells[0]
         n_s = min(n_t, 128) if g.dim == 3 else n_t
-        v, wall, desc = cpu_sample(args.config, tuple(case.grid.cells), n_s, 2, args.precond, iters)
-        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": desc,
-               "sample_wall_s": wall}
+        v, info = cpu_sample(args.config, tuple(case.grid.cells), n_s, 1, args.precond, iters)
+        cpu = dict(value=v, unit="s", cores=1, **info, **host_info())
 
     if rank == 0:
         ITER_FILE.parent.mkdir(exist_ok=True)
@@ -398,7 +501,7 @@ def main():
             d = {}
         if args.n is None:
             d[f"{args.config}_{args.precond}"] = {"iterations": iters, "status": hist.status,
-                                                  "scalar_vcycles": hist.entries[-1].scalar_vcycles}
+                                                  "scalar_vcycles": vc_solve}
             (ROOT / "gpurun_out").mkdir(exist_ok=True)
             (ROOT / "gpurun_out" / "bench_iterations.json").write_text(json.dumps(d, indent=1))
         value = ms / 1e3
@@ -406,16 +509,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded recipe, SURVEY §8d)",
-            "config": {"workload": f"{args.config} {'x'.join(map(str, g.cells))} "
-                                   f"{'periodic' if case.steady_periodic else 'walls'} {args.precond} "
-                                   f"GMRES({case.restart}) rtol 1e-9",
-                       "precond": args.precond, "restart": case.restart, "cells": list(g.cells),
-                       "iterations": iters, "status": hist.status,
-                       "scalar_vcycles": hist.entries[-1].scalar_vcycles,
-                       "setup_ms": setup_ms,
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (no domain decomposition yet)",
-                       "l2": "every field (134 MB at 256^3) exceeds the 126 MB L2; no flush needed",
-                       "graphs": bool(args.graphs)},
+            "config": workload(args.config, args.precond, world, args.n)[2],
+            "solve": {"iterations": iters, "status": hist.status, "scalar_vcycles_per_solve": vc_solve,
+                      "setup_ms": setup_ms, "graphs": bool(args.graphs)},
             "roofline": {"bound": "hbm", "kernel": "k_face_colour (finest level)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -433,21 +529,24 @@ def main():
 
 
 def run_dist(args, rank, world, local):
-    """N > 1: the slab-decomposed solve (one slab per GPU, NCCL halo exchange /
-    allreduce / coarse allgather inside libstokesb200.so), C5 weak scaling:
-    256^3 cells per GPU on the box (512 x 256^2, 512^2 x 256, 512^3)."""
+    """N > 1 (or --force-dist): the slab-decomposed solve, one slab per GPU,
+    NCCL halo exchange / allreduce / coarse allgather inside libstokesb200.so
+    (with one rank the 1-rank communicator runs the same NCCL branches).
+    C5: weak scaling, 256^3 cells per GPU (512 x 256^2, 512^2 x 256, 512^3),
+    each rank generating only its planes.  C4 (and C3): strong scaling of the
+    BASELINE grid (256^3), every rank generating the global recipe and passing
+    its planes."""
     import torch
     import torch.distributed as dist
 
     from paper_1308_4605_b200 import problems as PR
     from paper_1308_4605_b200.dist import DistSolver, bootstrap_nccl_id
-    from paper_1308_4605_b200.grid import GridSpec
     from paper_1308_4605_b200.krylov import GmresConfig
     from paper_1308_4605_b200.operators import STRESS
     from paper_1308_4605_b200.precond import PrecondConfig, PrecondKind
 
-    if args.config != "C5":
-        raise SystemExit("multi-GPU bench runs the C5 weak-scaling sweep")
+    if args.config not in ("C3", "C4", "C5"):
+        raise SystemExit("the slab-decomposed path is 3D (C3 / C4 / C5)")
     dev = torch.device("cuda", local)
 
     def reduce(kind, a, b):
@@ -459,17 +558,35 @@ def run_dist(args, rank, world, local):
         dist.all_reduce(t)
         return float(t[0]), float(t[1])
 
-    cells = PR.c5_cells(world)
-    grid, coeff, rhs, c = PR.make_c5_slab(cells, world, rank, reduce=reduce)
+    cells, restart, wcfg = workload(args.config, args.precond, world, args.n)
     nid = bootstrap_nccl_id()
-    D = DistSolver(grid, STRESS, nranks=world, rank=rank, nslab=1, nccl_id=nid)
-    D.local_inputs = True
+    if args.config == "C5" and args.n is None:
+        grid, coeff, rhs, c = PR.make_c5_slab(cells, world, rank, reduce=reduce)
+        D = DistSolver(grid, STRESS, nranks=world, rank=rank, nslab=1, nccl_id=nid)
+        D.local_inputs = True
+    else:
+        from paper_1308_4605_b200.dist import rank_planes
+        case = PR.make_case(args.config, args.n)
+        cs, rs, _ = PR.prepare(case)
+        grid = case.grid
+        D = DistSolver(grid, STRESS, nranks=world, rank=rank, nslab=1, nccl_id=nid)
+        D.local_inputs = True
+        mine = lambda a: rank_planes(a, world, rank)
+        from types import SimpleNamespace as NS
+        coeff = NS(theta=cs.theta,
+                   rho_face=NS(components=[mine(x) for x in cs.rho_face.components]),
+                   mu_cell=NS(data=mine(cs.mu_cell.data)), gamma_cell=NS(data=mine(cs.gamma_cell.data)),
+                   mu_node_edge=NS(arrays={k: mine(v) for k, v in cs.mu_node_edge.arrays.items()}))
+        coeff.mu_node_edge.plane = lambda a, b, _e=coeff.mu_node_edge.arrays: _e[(min(a, b), max(a, b))]
+        rhs = NS(u=NS(components=[mine(x) for x in rs.u.components]), p=NS(data=mine(rs.p.data)))
+        del case, cs, rs
+    assert D.uses_nccl
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
     class DC:  # HBM-resident coefficient set (duck-typed)
         pass
     dc = DC()
-    dc.theta = 0.0
+    dc.theta = coeff.theta
     dc.rho_face = type("F", (), {"components": [T(x) for x in coeff.rho_face.components]})()
     dc.mu_cell = type("C", (), {"data": T(coeff.mu_cell.data)})()
     dc.gamma_cell = type("C", (), {"data": T(coeff.gamma_cell.data)})()
@@ -479,7 +596,7 @@ def run_dist(args, rank, world, local):
     drhs.u = type("U", (), {"components": [T(x) for x in rhs.u.components]})()
     drhs.p = type("P", (), {"data": T(rhs.p.data)})()
     pc = PrecondConfig(kind=PrecondKind(args.precond))
-    gcfg = GmresConfig(restart=50, max_iters=500, rtol=1e-9, atol=0.0, track_true_residual=False)
+    gcfg = GmresConfig(restart=restart, max_iters=500, rtol=1e-9, atol=0.0, track_true_residual=False)
     stream = torch.cuda.ExternalStream(D.stream_ptr(), device=dev)
 
     # solution into HBM-resident tensors (the single-GPU arm's solve_raw contract)
@@ -530,7 +647,7 @@ def run_dist(args, rank, world, local):
         tt.numpy()[...] = a
         return tt.numpy()
     hc = type("HC", (), {})()
-    hc.theta = 0.0
+    hc.theta = coeff.theta
     hc.rho_face = type("F", (), {"components": [pinned(x) for x in coeff.rho_face.components]})()
     hc.mu_cell = type("C", (), {"data": pinned(coeff.mu_cell.data)})()
     hc.gamma_cell = type("C", (), {"data": pinned(coeff.gamma_cell.data)})()
@@ -562,13 +679,14 @@ def run_dist(args, rank, world, local):
         info = D.info()
         out = {
             "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak" if args.config == "C5" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded recipe, SURVEY §8d; per-rank slabs)",
-            "config": {"workload": f"C5 {'x'.join(map(str, cells))} periodic {args.precond} GMRES(50) rtol 1e-9",
-                       "cells": list(cells), "iterations": hist.iterations, "status": hist.status,
-                       "parallelism": f"slab decomposition along axis 0 over {world} GPUs (NCCL)",
-                       "distributed_levels": info["distributed_levels"],
-                       "agglomerated_levels": info["agglomerated_levels"], "planes_per_gpu": info["planes_per_slab"]},
+            "config": wcfg,
+            "solve": {"iterations": hist.iterations, "status": hist.status,
+                      "transport": "NCCL (1-rank communicator)" if world == 1 else f"NCCL over {world} ranks",
+                      "distributed_levels": info["distributed_levels"],
+                      "agglomerated_levels": info["agglomerated_levels"], "planes_per_gpu": info["planes_per_slab"]},
             "roofline": {"bound": "hbm", "kernel": "k_face_colour (finest slab level, rank 0)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,

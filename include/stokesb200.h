@@ -218,6 +218,37 @@ int sb_residual_restrict(sb_ctx* ctx, int kind, int level, const double* const* 
 int sb_prolong_add(sb_ctx* ctx, int kind, int level, const double* const* coarse,
                    double* const* fine);
 
+/* ---- the reference's remaining public operators (geometry only unless noted;
+ * a context needs no coefficients for these) ---- */
+/* div(u) -> cell, reading the stored boundary faces (operators.py:182-188) */
+int sb_div(sb_ctx* ctx, const double* const* u, double* out);
+/* grad(p) -> faces, wall-normal faces 0 (operators.py:191-198) */
+int sb_grad(sb_ctx* ctx, const double* p, double* const* out);
+/* lap_pressure(p) = div(grad(p)) (operators.py:201-203) */
+int sb_lap_pressure(sb_ctx* ctx, const double* p, double* out);
+/* pure restriction level -> level+1 (multigrid.py:177-182, :214-233) */
+int sb_restrict(sb_ctx* ctx, int kind, int level, const double* const* fine, double* const* coarse);
+/* pure prolongation level+1 -> level (multigrid.py:185-192, :282-295) */
+int sb_prolong(sb_ctx* ctx, int kind, int level, const double* const* coarse, double* const* fine);
+/* needs coefficients: the smoother diagonal of a level as arrays
+ * (helmholtz_diagonal / lrho_diagonal, operators.py:396-439; wall-normal
+ * boundary faces 1) */
+int sb_diagonal(sb_ctx* ctx, int kind, int level, double* const* out);
+/* needs coefficients: S~^-1 r = -theta phi + V r with phi the caller's Poisson
+ * solve of r, or V r when phi is NULL (apply_schur_inv, schur.py:59-78) */
+int sb_schur_inv(sb_ctx* ctx, const double* r, const double* phi, double* out);
+
+/* ---- restarted GMRES on flat vectors with a caller-supplied operator: the
+ * reference's gmres_kernel(apply_op, b, restart, max_iters, target,
+ * breakdown_tol, callback) seam (krylov.py:81-146).  Host arrays of length n;
+ * the basis and orthogonalisation live on the device, apply(in, out, user)
+ * computes out = op(in) on host arrays, callback(k, x_k, r_P, restart_flag,
+ * user) (nullable) sees every iterate.  status: SB_STATUS_*; iterations = k. */
+typedef void (*sb_apply_fn)(const double* in, double* out, void* user);
+typedef void (*sb_iter_fn)(int k, const double* x, double resid_precond, int restart_flag, void* user);
+int sb_gmres_flat(long long n, const double* b, int restart, int max_iters, double target, double breakdown_tol,
+                  sb_apply_fn apply, sb_iter_fn callback, void* user, double* x_out, int* status, int* iterations);
+
 /* ---- measurement ---- */
 void sb_set_profiling(sb_ctx* ctx, int enabled);
 int sb_get_kernel_stats(sb_ctx* ctx, sb_kernel_stats* out);

@@ -26,6 +26,8 @@ EXPORTS = (
     "sb_apply_A", "sb_apply_A_affine", "sb_homogenize", "sb_apply_Lrho", "sb_mg_solve", "sb_precond_apply", "sb_gmres_solve",
     "sb_num_levels", "sb_level_flags", "sb_level_cells", "sb_get_level_coefficients", "sb_smooth",
     "sb_residual_restrict", "sb_prolong_add", "sb_set_profiling", "sb_get_kernel_stats",
+    "sb_div", "sb_grad", "sb_lap_pressure", "sb_restrict", "sb_prolong", "sb_diagonal", "sb_schur_inv",
+    "sb_gmres_flat",
     "sb_launch_count", "sb_set_graphs", "sb_device_bytes", "sb_set_stream",
     "sb_nccl_id_bytes", "sb_nccl_unique_id", "sb_dist_create", "sb_dist_destroy", "sb_dist_info", "sb_dist_stream",
     "sb_dist_set_coefficients", "sb_dist_apply_M", "sb_dist_precond_apply", "sb_dist_gmres_solve",
@@ -90,6 +92,15 @@ _SIGS = {
     "sb_smooth": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, _PP, _PP]),
     "sb_residual_restrict": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP, _PP]),
     "sb_prolong_add": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP]),
+    "sb_div": (C.c_int, [_P, _PP, _P]),
+    "sb_grad": (C.c_int, [_P, _P, _PP]),
+    "sb_lap_pressure": (C.c_int, [_P, _P, _P]),
+    "sb_restrict": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP]),
+    "sb_prolong": (C.c_int, [_P, C.c_int, C.c_int, _PP, _PP]),
+    "sb_diagonal": (C.c_int, [_P, C.c_int, C.c_int, _PP]),
+    "sb_schur_inv": (C.c_int, [_P, _P, _P, _P]),
+    "sb_gmres_flat": (C.c_int, [C.c_longlong, _P, C.c_int, C.c_int, C.c_double, C.c_double, _P, _P, _P, _P,
+                                C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sb_set_profiling": (None, [_P, C.c_int]),
     "sb_get_kernel_stats": (C.c_int, [_P, C.POINTER(KernelStats)]),
     "sb_launch_count": (C.c_longlong, [_P]),

@@ -984,6 +984,81 @@ __global__ void k_check_diag(LevelDev L, int* flags, Box b, unsigned total) {
   }
 }
 
+// The smoother diagonals as arrays (helmholtz_diagonal / lrho_diagonal,
+// operators.py:396-439): the same register-computed diagonal the colour passes
+// divide by; wall-normal boundary faces are set to one as in the reference.
+template <int DIM, int FORM, int A>
+__device__ __forceinline__ void wr_face_diag(const LevelDev& L, const int* ci, double* out) {
+  if (!in_face(L, A, ci)) return;
+  const int f = lin(L, ci);
+  if (is_wall_face(L, A, ci)) {
+    out[f] = 1.0;
+    return;
+  }
+  double dg;
+  const double* none[3] = {L.mu_c, L.mu_c, L.mu_c};
+  (void)face_row<DIM, FORM, A>(L, none, f, ci, dg);
+  out[f] = dg;
+}
+
+template <int DIM, int FORM>
+__global__ void k_write_diag(LevelDev L, Ptr3 fd, double* cd, Box b, unsigned total) {
+  pdl_enter();
+  {
+    int ci[3];
+    if (!box_point(b, ci)) return;
+    if (fd.p[2] != nullptr) {
+      if (DIM == 3) wr_face_diag<3, FORM, 0>(L, ci, fd.p[0]);
+      wr_face_diag<DIM, FORM, 1>(L, ci, fd.p[1]);
+      wr_face_diag<DIM, FORM, 2>(L, ci, fd.p[2]);
+    }
+    if (cd != nullptr && in_cell(L, ci)) {
+      double dg;
+      (void)cell_row<DIM>(L, L.mu_c, lin(L, ci), ci, dg);
+      cd[lin(L, ci)] = dg;
+    }
+  }
+}
+
+// div / grad as the reference's public functions compute them (operators.py:
+// 182-198), bit for bit: div = ((d0 + d1) + d2) / h reading the stored
+// boundary faces, grad = (p[i] - p[i-1]) / h with wall-normal faces 0.
+template <int DIM>
+__global__ void k_div(LevelDev L, CPtr3 u, double* out, Box b, unsigned total) {
+  pdl_enter();
+  {
+    int ci[3];
+    if (!box_point(b, ci)) return;
+    const int c = lin(L, ci);
+    const double* uu[3] = {u.p[0], u.p[1], u.p[2]};
+    out[c] = div_sum<DIM>(L, uu, c, ci) / L.h;
+  }
+}
+
+template <int A>
+__device__ __forceinline__ void grad_face(const LevelDev& L, const double* p, double* out, const int* ci) {
+  if (!in_face(L, A, ci)) return;
+  const int f = lin(L, ci);
+  if (is_wall_face(L, A, ci)) {
+    out[f] = 0.0;
+    return;
+  }
+  const int dm = A == 0 ? dminus<0>(L, ci[0]) : (A == 1 ? dminus<1>(L, ci[1]) : dminus<2>(L, ci[2]));
+  out[f] = (__ldg(p + f) - __ldg(p + f + dm)) / L.h;
+}
+
+template <int DIM>
+__global__ void k_grad(LevelDev L, const double* p, Ptr3 out, Box b, unsigned total) {
+  pdl_enter();
+  {
+    int ci[3];
+    if (!box_point(b, ci)) return;
+    if (DIM == 3) grad_face<0>(L, p, out.p[0], ci);
+    grad_face<1>(L, p, out.p[1], ci);
+    grad_face<2>(L, p, out.p[2], ci);
+  }
+}
+
 // The reference's edge (3D) / node (2D) viscosity at index ci of edge array e,
 // for any boundary conditions: _avg_to_stagger along the lower plane axis,
 // then the higher (operators.py:90-104, :133-145) -- periodic and interior
@@ -2650,10 +2725,35 @@ void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int
   Box b = full_box(L);
   const unsigned total = box_count(b);
   SB_DISPATCH_FORM(form, {
-  ++g_kernel_launches;
     if (dim == 3) launch_k(k_check_diag<3, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
     else launch_k(k_check_diag<2, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, flags, b, total);
   });
+}
+
+void launch_write_diag(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 face_diag, double* cell_diag) {
+  ++g_kernel_launches;
+  Box b = full_box(L);
+  const unsigned total = box_count(b);
+  SB_DISPATCH_FORM(form, {
+    if (dim == 3) launch_k(k_write_diag<3, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, face_diag, cell_diag, b, total);
+    else launch_k(k_write_diag<2, FM>, cfg3(b).g, cfg3(b).b, 0, s, L, face_diag, cell_diag, b, total);
+  });
+}
+
+void launch_div(cudaStream_t s, const LevelDev& L, int dim, CPtr3 u, double* out) {
+  ++g_kernel_launches;
+  Box b = cell_box(L);
+  const unsigned total = box_count(b);
+  if (dim == 3) launch_k(k_div<3>, cfg3(b).g, cfg3(b).b, 0, s, L, u, out, b, total);
+  else launch_k(k_div<2>, cfg3(b).g, cfg3(b).b, 0, s, L, u, out, b, total);
+}
+
+void launch_grad(cudaStream_t s, const LevelDev& L, int dim, const double* p, Ptr3 out) {
+  ++g_kernel_launches;
+  Box b = full_box(L);
+  const unsigned total = box_count(b);
+  if (dim == 3) launch_k(k_grad<3>, cfg3(b).g, cfg3(b).b, 0, s, L, p, out, b, total);
+  else launch_k(k_grad<2>, cfg3(b).g, cfg3(b).b, 0, s, L, p, out, b, total);
 }
 
 void launch_cell_to_face(cudaStream_t s, const LevelDev& L, int dim, int A, const double* cell, double* face) {

@@ -137,6 +137,11 @@ void launch_coarsen_edge(cudaStream_t s, const LevelDev& Lf, const LevelDev& Lc,
 void launch_beta(cudaStream_t s, const LevelDev& L, int A, const double* rho, double* beta, int* flag,
                  int* cflag = nullptr, const double* ref = nullptr);
 void launch_check_diag(cudaStream_t s, const LevelDev& L, int dim, int form, int* flags);
+// the smoother diagonals as arrays (face: Ptr3 with p[2] != null; cell: nullable)
+// the reference's public div / grad (operators.py:182-198), bit-exact
+void launch_div(cudaStream_t s, const LevelDev& L, int dim, CPtr3 u, double* out);
+void launch_grad(cudaStream_t s, const LevelDev& L, int dim, const double* p, Ptr3 out);
+void launch_write_diag(cudaStream_t s, const LevelDev& L, int dim, int form, Ptr3 face_diag, double* cell_diag);
 // device-side make_coefficients + rescale: rho_face[A] from rho_cell, mu_e[e]
 // = scale * edge mean of L.mu_c (unscaled at the call), x *= scale
 void launch_cell_to_face(cudaStream_t s, const LevelDev& L, int dim, int A, const double* cell, double* face);

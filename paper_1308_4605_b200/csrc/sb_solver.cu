@@ -392,9 +392,9 @@ double* vpres(sb_ctx* c, double* v) { return v + (long long)c->dim * c->lv[0].bl
 void check_ready(sb_ctx* c) {
   if (!c->have_coef) throw ArgErr(SB_EINVAL, "coefficients not set (call sb_set_coefficients)");
 }
-void check_mg(sb_ctx* c, int kind) {
+void check_mg(sb_ctx* c, int kind, bool need_levels = true) {
   check_ready(c);
-  if (c->lv.size() < 2) throw ArgErr(SB_EINVAL, "grid cannot be coarsened; need even counts >= 4");
+  if (need_levels && c->lv.size() < 2) throw ArgErr(SB_EINVAL, "grid cannot be coarsened; need even counts >= 4");
   if (kind == SB_KIND_CELL) {
     if (c->flag_rho) throw ArgErr(SB_EINVAL, "face density must be positive");
     if (c->flag_cell) throw ArgErr(SB_EDOM, "zero diagonal in pressure operator");
@@ -1197,6 +1197,13 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
           H[i * m + j] = ((hh1(c)[i] - e) + hh2(c)[i]) / gam;
         }
         hn = gnext / gam;
+        static const bool trace = [] {
+          const char* e = std::getenv("SB_GMRES_TRACE");
+          return e && e[0] == '1';
+        }();
+        if (trace)
+          std::fprintf(stderr, "gmres k=%d j=%d ww=%.6e cc=%.6e gnext=%.6e gam=%.6e hn=%.6e direct=%d\n", k, j, ww,
+                       cc, gnext, gam, hn, (int)direct);
         for (int i = 0; i <= j; ++i) Horig[i * m + j] = H[i * m + j];
         Horig[(j + 1) * m + j] = hn;
         for (int i = 0; i <= j; ++i) cpend[i] = direct ? 0.0 : hh2(c)[i];
@@ -1788,7 +1795,7 @@ static void level_bufs(sb_ctx* c, int l, int kind, double** x, double** rhs) {
 
 int sb_smooth(sb_ctx* c, int kind, int level, double omega, double* const* x, const double* const* rhs) {
   return guard([&]() -> int {
-    check_mg(c, kind);
+    check_mg(c, kind, false);  // one sweep needs no coarse level (smooth_face on any grid)
     if (level < 0 || level >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
     double *bx[3], *br[3];
     level_bufs(c, level, kind, bx, br);
@@ -1874,6 +1881,140 @@ int sb_prolong_add(sb_ctx* c, int kind, int level, const double* const* coarse, 
   });
 }
 
+// ---- the reference's remaining public operators (operators.py:182-198,
+// :396-439; multigrid.py:177-295; schur.py:59-78) on the device ----------------
+
+static void zero_block(sb_ctx* c, const Level& L, double* p) { CK(cudaMemsetAsync(p, 0, (size_t)L.block * 8, c->st)); }
+
+int sb_div(sb_ctx* c, const double* const* u, double* out) {
+  return guard([&]() -> int {
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    for (int r = 0; r < c->dim; ++r) copy_in(c, L, r + c->off, u[r], c->sf0[r + c->off]);
+    launch_div(c->st, L.d, c->dim, CPtr3{{c->sf0[0], c->sf0[1], c->sf0[2]}}, c->sc0);
+    copy_out(c, L, -1, c->sc0, out);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_grad(sb_ctx* c, const double* p, double* const* out) {
+  return guard([&]() -> int {
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    copy_in(c, L, -1, p, c->sc0);
+    launch_grad(c->st, L.d, c->dim, c->sc0, Ptr3{{c->sf0[0], c->sf0[1], c->sf0[2]}});
+    for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, c->sf0[r + c->off], out[r]);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+// lap_pressure = div(grad(p)) (operators.py:201-203), the same two steps
+int sb_lap_pressure(sb_ctx* c, const double* p, double* out) {
+  return guard([&]() -> int {
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    copy_in(c, L, -1, p, c->sc0);
+    launch_grad(c->st, L.d, c->dim, c->sc0, Ptr3{{c->sf0[0], c->sf0[1], c->sf0[2]}});
+    launch_div(c->st, L.d, c->dim, CPtr3{{c->sf0[0], c->sf0[1], c->sf0[2]}}, c->sc1);
+    copy_out(c, L, -1, c->sc1, out);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_diagonal(sb_ctx* c, int kind, int level, double* const* out) {
+  return guard([&]() -> int {
+    check_ready(c);
+    if (kind != SB_KIND_CELL && kind != SB_KIND_FACE) throw ArgErr(SB_EINVAL, "kind must be 'cell' or 'face'");
+    if (level < 0 || level >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *bx[3], *br[3];
+    level_bufs(c, level, kind, bx, br);
+    const Level& L = c->lv[level];
+    if (kind == SB_KIND_FACE) {
+      launch_write_diag(c->st, L.d, c->dim, c->form, Ptr3{{bx[0], bx[1], bx[2]}}, nullptr);
+      for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, bx[r + c->off], out[r]);
+    } else {
+      launch_write_diag(c->st, L.d, c->dim, c->form, Ptr3{{nullptr, nullptr, nullptr}}, bx[0]);
+      copy_out(c, L, -1, bx[0], out[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+// S~^-1 r = -theta phi + V r (phi = the Poisson solve of r; NULL: steady, V r)
+int sb_schur_inv(sb_ctx* c, const double* r, const double* phi, double* out) {
+  return guard([&]() -> int {
+    check_ready(c);
+    ensure_scratch(c);
+    const Level& L = c->lv[0];
+    copy_in(c, L, -1, r, c->sc0);
+    if (phi) copy_in(c, L, -1, phi, c->sc1);
+    launch_schur(c->st, L.d, c->form, c->sc0, phi ? c->sc1 : nullptr, c->sf0[2], 1.0);
+    copy_out(c, L, -1, c->sf0[2], out);
+    sync(c);
+    return SB_OK;
+  });
+}
+
+// pure restriction / prolongation between levels `level` and `level + 1`
+int sb_restrict(sb_ctx* c, int kind, int level, const double* const* fine, double* const* coarse) {
+  return guard([&]() -> int {
+    if (kind != SB_KIND_CELL && kind != SB_KIND_FACE) throw ArgErr(SB_EINVAL, "kind must be 'cell' or 'face'");
+    if (level < 0 || level + 1 >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *fx[3], *fr[3], *cx[3], *cr[3];
+    level_bufs(c, level, kind, fx, fr);
+    level_bufs(c, level + 1, kind, cx, cr);
+    const Level& L = c->lv[level];
+    const Level& C = c->lv[level + 1];
+    if (kind == SB_KIND_FACE) {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, L, A, fine[r], fx[A]);
+        zero_block(c, C, cr[A]);  // coarse wall faces stay 0
+        launch_face_restrict(c->st, L.d, C.d, c->dim, A, fx[A], cr[A]);
+        copy_out(c, C, A, cr[A], coarse[r]);
+      }
+    } else {
+      copy_in(c, L, -1, fine[0], fx[0]);
+      launch_cell_restrict(c->st, L.d, C.d, c->dim, fx[0], cr[0]);
+      copy_out(c, C, -1, cr[0], coarse[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
+int sb_prolong(sb_ctx* c, int kind, int level, const double* const* coarse, double* const* fine) {
+  return guard([&]() -> int {
+    if (kind != SB_KIND_CELL && kind != SB_KIND_FACE) throw ArgErr(SB_EINVAL, "kind must be 'cell' or 'face'");
+    if (level < 0 || level + 1 >= (int)c->lv.size()) throw ArgErr(SB_EINVAL, "level out of range");
+    double *fx[3], *fr[3], *cx[3], *cr[3];
+    level_bufs(c, level, kind, fx, fr);
+    level_bufs(c, level + 1, kind, cx, cr);
+    const Level& L = c->lv[level];
+    const Level& C = c->lv[level + 1];
+    if (kind == SB_KIND_FACE) {
+      for (int r = 0; r < c->dim; ++r) {
+        const int A = r + c->off;
+        copy_in(c, C, A, coarse[r], cx[A]);
+        zero_block(c, L, fx[A]);
+        launch_face_prolong_add(c->st, L.d, C.d, c->dim, A, cx[A], fx[A]);
+        copy_out(c, L, A, fx[A], fine[r]);
+      }
+    } else {
+      copy_in(c, C, -1, coarse[0], cx[0]);
+      zero_block(c, L, fx[0]);
+      launch_cell_prolong_add(c->st, L.d, C.d, c->dim, cx[0], fx[0]);
+      copy_out(c, L, -1, fx[0], fine[0]);
+    }
+    sync(c);
+    return SB_OK;
+  });
+}
+
 void sb_set_profiling(sb_ctx* c, int enabled) { c->profiling = enabled != 0; }
 
 int sb_get_kernel_stats(sb_ctx* c, sb_kernel_stats* out) {
@@ -1917,3 +2058,6 @@ int sb_set_stream(sb_ctx* c, void* stream) {
 
 // slab-decomposed multi-GPU path (shares this translation unit)
 #include "sb_dist.inc"
+
+// gmres_kernel seam: flat vectors, host operator callback (shares this translation unit)
+#include "sb_flat.inc"

@@ -139,3 +139,51 @@ def true_residual(x, rhs, coeff) -> float:
     return norm2(apply_M(x, coeff) - StokesVector(
         FaceField(as_grid(rhs.u.grid), tuple(rhs.u.components)),
         CellField(as_grid(rhs.u.grid), rhs.p.data)))
+
+
+_APPLY_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+_ITER_FN = C.CFUNCTYPE(None, C.c_int, C.POINTER(C.c_double), C.c_double, C.c_int, C.c_void_p)
+
+
+def gmres_kernel(apply_op, b, restart: int, max_iters: int, target: float, breakdown_tol: float,
+                 callback=None):
+    """Restarted GMRES on flat vectors for ``apply_op(x) = b`` (krylov.py:81-146).
+
+    Returns ``(x, status, iterations)`` with status ``converged`` /
+    ``breakdown`` / ``maxiter`` and the reference's restart, stopping and
+    callback semantics (``callback(k, x_k, r_P, restart_flag)`` after every
+    iteration).  The basis and the Arnoldi orthogonalisation (CGS2) live on
+    the device (``sb_gmres_flat``); ``apply_op`` is called on host NumPy
+    vectors, as the reference calls it."""
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    n = b.size
+    err = []
+
+    def _apply(pin, pout, _user):
+        try:
+            v = np.ctypeslib.as_array(pin, shape=(n,)).copy()
+            w = np.asarray(apply_op(v), dtype=np.float64).reshape(-1)
+            np.ctypeslib.as_array(pout, shape=(n,))[:] = w
+        except BaseException as e:  # surfaced after the C call returns
+            err.append(e)
+            np.ctypeslib.as_array(pout, shape=(n,))[:] = 0.0
+
+    def _iter(k, px, rp, rflag, _user):
+        if callback is None or err:
+            return
+        try:
+            callback(int(k), np.ctypeslib.as_array(px, shape=(n,)).copy(), float(rp), bool(rflag))
+        except BaseException as e:
+            err.append(e)
+
+    fa, fi = _APPLY_FN(_apply), _ITER_FN(_iter)
+    x = np.zeros(n)
+    status, its = C.c_int(0), C.c_int(0)
+    rc = _lib.load().sb_gmres_flat(C.c_longlong(n), _lib.ptr(b), int(restart), int(max_iters), float(target),
+                                   float(breakdown_tol), C.cast(fa, C.c_void_p),
+                                   C.cast(fi, C.c_void_p) if callback is not None else None,
+                                   None, _lib.ptr(x), C.byref(status), C.byref(its))
+    if err:
+        raise err[0]
+    _lib.check(rc)
+    return x, _lib.STATUS[status.value], int(its.value)

@@ -102,6 +102,28 @@ def _pair_mean_all(x):
     return x
 
 
+    def diag_face(self, level: int) -> FaceField:
+        """The velocity smoother's diagonal on ``level`` (multigrid.py:79-89);
+        ZeroDivisionError on a zero interior entry, as the reference."""
+        g = _level_grid(self, level)
+        out = [np.zeros(g.face_shape(a)) for a in range(g.dim)]
+        _lib.check(self.ctx.lib.sb_diagonal(self.ctx.h, _lib.KIND_FACE, int(level), _lib.parr(out)))
+        d = FaceField(g, tuple(out))
+        for a in range(g.dim):
+            if np.any(d.interior(a) == 0):
+                raise ZeroDivisionError("zero diagonal in velocity operator (theta = 0 with mu = 0 row)")
+        return d
+
+    def diag_cell(self, level: int) -> CellField:
+        """The pressure smoother's diagonal on ``level`` (multigrid.py:70-77)."""
+        g = _level_grid(self, level)
+        out = np.zeros(g.cells)
+        _lib.check(self.ctx.lib.sb_diagonal(self.ctx.h, _lib.KIND_CELL, int(level), _lib.parr([out])))
+        if np.any(out == 0):
+            raise ZeroDivisionError("zero diagonal in pressure operator")
+        return CellField(g, out)
+
+
 def build_hierarchy(grid, coeff) -> MgHierarchy:
     g = as_grid(grid)
     if not g.can_coarsen():
@@ -189,3 +211,123 @@ def prolong_add(hierarchy: MgHierarchy, level: int, kind: str, coarse, fine):
     _lib.check(ctx.lib.sb_prolong_add(ctx.h, k, int(level), _lib.parr(_arrays(coarse, kind)),
                                       _lib.parr(fs)))
     return _wrap(_level_grid(hierarchy, level), fs, kind)
+
+
+# ---------------------------------------------------------------------------
+# the reference's public transfer / coarsening / smoother functions
+# (multigrid.py:127-295, :318-340) with their signatures, on the device
+# ---------------------------------------------------------------------------
+
+
+def _transfer_ctx(grid):
+    g = as_grid(grid)
+    if any(n % 2 for n in g.cells):
+        raise ValueError(f"cannot restrict odd cell counts {g.cells}")
+    from .operators import _Geometry
+    geo = _Geometry(g)
+    if geo.ctx.num_levels() < 2:
+        geo.ctx.release()
+        raise ValueError(f"grid {g.cells} cannot be coarsened on the device; need even counts >= 4")
+    return geo
+
+
+def restrict_cell(fine: CellField) -> CellField:
+    """Mean of the 2^d children (multigrid.py:177-182), bit-identical."""
+    g = as_grid(fine.grid)
+    with _transfer_ctx(g) as ctx:
+        gc = g.coarsened()
+        out = [np.zeros(gc.cells)]
+        _lib.check(ctx.lib.sb_restrict(ctx.h, _lib.KIND_CELL, 0, _lib.parr([_f64(fine.data)]), _lib.parr(out)))
+    return CellField(gc, out[0])
+
+
+def restrict_face(fine: FaceField) -> FaceField:
+    """Staggered restriction: tangential pair means, normal [1/4, 1/2, 1/4];
+    coarse wall faces 0 (multigrid.py:195-233), bit-identical."""
+    g = as_grid(fine.grid)
+    with _transfer_ctx(g) as ctx:
+        gc = g.coarsened()
+        out = [np.zeros(gc.face_shape(a)) for a in range(g.dim)]
+        _lib.check(ctx.lib.sb_restrict(ctx.h, _lib.KIND_FACE, 0, _lib.parr([_f64(c) for c in fine.components]),
+                                       _lib.parr(out)))
+    return FaceField(gc, tuple(out))
+
+
+def _fine_of(gc):
+    from .grid import GridSpec
+    return GridSpec(tuple(2 * n for n in gc.cells), gc.h / 2, gc.bc)
+
+
+def prolong_cell(coarse: CellField) -> CellField:
+    """Injection into the 2^d children (multigrid.py:185-192)."""
+    gf = _fine_of(as_grid(coarse.grid))
+    with _transfer_ctx(gf) as ctx:
+        out = [np.zeros(gf.cells)]
+        _lib.check(ctx.lib.sb_prolong(ctx.h, _lib.KIND_CELL, 0, _lib.parr([_f64(coarse.data)]), _lib.parr(out)))
+    return CellField(gf, out[0])
+
+
+def prolong_face(coarse: FaceField) -> FaceField:
+    """Staggered prolongation: tangential 3/4-1/4 (walls clamp), normal copy /
+    average (multigrid.py:236-295).  Wall-normal boundary faces are not
+    unknowns: they come back 0 (SURVEY §8b field convention)."""
+    gf = _fine_of(as_grid(coarse.grid))
+    with _transfer_ctx(gf) as ctx:
+        out = [np.zeros(gf.face_shape(a)) for a in range(gf.dim)]
+        _lib.check(ctx.lib.sb_prolong(ctx.h, _lib.KIND_FACE, 0, _lib.parr([_f64(c) for c in coarse.components]),
+                                      _lib.parr(out)))
+    return FaceField(gf, tuple(out))
+
+
+def coarsen_coefficients(coeff, coarse_grid) -> CoefficientSet:
+    """One level of coefficient coarsening (multigrid.py:127-169), by the
+    device's coarsening kernels; rho_cell by the device cell restriction."""
+    from .operators import _ctx_for
+    g = as_grid(coeff.rho_cell.grid)
+    gc = as_grid(coarse_grid)
+    if gc != g.coarsened():
+        raise ValueError(f"coarse grid {gc.cells} is not the coarsening of {g.cells}")
+    ctx = _ctx_for(coeff, g)
+    if ctx.num_levels() < 2:
+        raise ValueError(f"grid {g.cells} cannot be coarsened; need even counts >= 4")
+    rho = [np.zeros(gc.face_shape(a)) for a in range(gc.dim)]
+    mu = np.zeros(gc.cells)
+    gam = np.zeros(gc.cells)
+    edges = [np.zeros(gc.node_edge_shape(pl)) for pl in edge_planes(gc.dim)]
+    _lib.check(ctx.lib.sb_get_level_coefficients(ctx.h, 1, _lib.parr(rho), _lib.ptr(mu), _lib.parr(edges),
+                                                 _lib.ptr(gam)))
+    out = CoefficientSet.__new__(CoefficientSet)
+    out.theta = coeff.theta
+    out.rho_cell = CellField(gc, restrict_cell(coeff.rho_cell).data)
+    out.rho_face = FaceField(gc, tuple(rho))
+    out.mu_cell = CellField(gc, mu)
+    out.mu_node_edge = NodeEdgeField(gc, dict(zip(edge_planes(gc.dim), edges)))
+    out.gamma_cell = CellField(gc, gam)
+    out.viscous_form = coeff.viscous_form
+    return out
+
+
+def _smooth_level0(kind, x, rhs, grid, coeff, omega):
+    from .operators import _ctx_for
+    ctx = _ctx_for(coeff, grid)
+    k = _kind(kind)
+    xs = _arrays(x, kind)
+    _lib.check(ctx.lib.sb_smooth(ctx.h, k, 0, float(omega), _lib.parr(xs), _lib.parr(_arrays(rhs, kind))))
+    if kind == "cell":
+        x.data[...] = xs[0]
+    else:
+        for a, arr in enumerate(xs):
+            x.components[a][...] = arr
+
+
+def smooth_cell(phi: CellField, rhs: CellField, grid, coeff, diag: CellField, omega: float) -> None:
+    """One red-black GS sweep of the pressure operator, in place (multigrid.py:318-324).
+    ``diag`` is the operator's diagonal (lrho_diagonal) as every reference caller
+    passes; the device recomputes it in registers."""
+    _smooth_level0("cell", phi, rhs, as_grid(grid), coeff, omega)
+
+
+def smooth_face(u: FaceField, rhs: FaceField, grid, coeff, diag: FaceField, omega: float) -> None:
+    """One 2d-colour GS sweep of the velocity operator, in place (multigrid.py:327-340).
+    ``diag``: helmholtz_diagonal (recomputed in registers on the device)."""
+    _smooth_level0("face", u, rhs, as_grid(grid), coeff, omega)

@@ -414,3 +414,81 @@ def apply_Lrho(p, coeff, ctx: DeviceContext | None = None) -> CellField:
     out = np.zeros(g.cells)
     _lib.check(ctx.lib.sb_apply_Lrho(ctx.h, _lib.ptr(_f64(p.data)), _lib.ptr(out)))
     return CellField(g, out)
+
+
+# ---------------------------------------------------------------------------
+# the reference's remaining public operators (operators.py:182-203, :303-345,
+# :396-439), on the device
+# ---------------------------------------------------------------------------
+
+
+class _Geometry:
+    """A pooled coefficient-free context for the geometry-only operators."""
+
+    def __init__(self, grid):
+        self.ctx = DeviceContext.acquire(as_grid(grid), STRESS)
+
+    def __enter__(self):
+        return self.ctx
+
+    def __exit__(self, *exc):
+        self.ctx.release()
+
+
+def div(u) -> CellField:
+    """Cell-centred divergence (operators.py:182-188); reads the stored boundary
+    faces.  Bit-identical to the reference: ((d0 + d1) + d2) / h."""
+    g = as_grid(u.grid)
+    out = np.zeros(g.cells)
+    with _Geometry(g) as ctx:
+        _lib.check(ctx.lib.sb_div(ctx.h, _lib.parr([_f64(c) for c in u.components]), _lib.ptr(out)))
+    return CellField(g, out)
+
+
+def grad(p) -> FaceField:
+    """Face-centred pressure gradient, wall-normal faces zero (operators.py:191-198)."""
+    g = as_grid(p.grid)
+    out = _out_face(g)
+    with _Geometry(g) as ctx:
+        _lib.check(ctx.lib.sb_grad(ctx.h, _lib.ptr(_f64(p.data)), _lib.parr(out)))
+    return FaceField(g, tuple(out))
+
+
+def lap_pressure(p) -> CellField:
+    """Scalar pressure Laplacian, exactly div(grad(p)) (operators.py:201-203)."""
+    g = as_grid(p.grid)
+    out = np.zeros(g.cells)
+    with _Geometry(g) as ctx:
+        _lib.check(ctx.lib.sb_lap_pressure(ctx.h, _lib.ptr(_f64(p.data)), _lib.ptr(out)))
+    return CellField(g, out)
+
+
+def apply_viscous(u, coeff, bvals=None) -> FaceField:
+    """Discrete viscous term L_mu u in the coefficient set's form
+    (operators.py:303-345): the device's A row with theta = 0, negated
+    (A u = theta rho u - L_mu u, wall-normal rows 0); ``bvals`` as apply_A."""
+    g = as_grid(u.grid)
+    c0 = CoefficientSet.__new__(CoefficientSet)
+    c0.__dict__.update(coeff.__dict__)
+    c0.theta = 0.0  # the viscous part alone (no validation: an inviscid set stays usable)
+    a = apply_A(u, c0, bvals)
+    return FaceField(g, tuple(-x for x in a.components))
+
+
+def helmholtz_diagonal(grid, coeff) -> FaceField:
+    """Diagonal of A = theta rho - L_mu, boundary faces one (operators.py:408-439),
+    as the device smoother computes it in registers."""
+    g = as_grid(grid)
+    ctx = _ctx_for(coeff, g)
+    out = _out_face(g)
+    _lib.check(ctx.lib.sb_diagonal(ctx.h, _lib.KIND_FACE, 0, _lib.parr(out)))
+    return FaceField(g, tuple(out))
+
+
+def lrho_diagonal(grid, coeff) -> CellField:
+    """Diagonal of D (1/rho) G, wall faces carry no flux (operators.py:396-405)."""
+    g = as_grid(grid)
+    ctx = _ctx_for(coeff, g)
+    out = np.zeros(g.cells)
+    _lib.check(ctx.lib.sb_diagonal(ctx.h, _lib.KIND_CELL, 0, _lib.parr([out])))
+    return CellField(g, out)

@@ -6,10 +6,11 @@
 BASELINE recipes only ever converge, so this pins the other two on inputs
 where the reference reaches them cleanly:
 
-* ``breakdown`` -- a 4x4 periodic 2D problem whose Krylov space is exhausted
-  after 40 (P1) Arnoldi steps: the Arnoldi norm drops from ~1e-3 to ~1e-15
-  of r_P0 (``krylov.py:138``, breakdown_tol = 1e-14 r_P0, ``:198``) while the
-  target ``rtol = 1e-300`` is never met;
+* ``breakdown`` -- 4x4 2D problems (periodic P1; walls, theta > 0, P2) whose
+  rhs makes the preconditioned Krylov space exactly 2-dimensional
+  (``invariant_rhs``): the Arnoldi norm collapses to roundoff at iteration 2
+  (``krylov.py:138``, breakdown_tol = 1e-14 r_P0, ``:198``) while the target
+  ``rtol = 1e-300`` is never met;
 * ``maxiter``   -- GMRES(3) capped at 7 iterations (two restarts: restart
   flags on iterations 4 and 7, ``krylov.py:135``), 2D and 3D.
 
@@ -38,10 +39,37 @@ OUT = pathlib.Path(__file__).resolve().parent
 CODE = {"p": G.PERIODIC, "n": G.NO_SLIP, "f": G.FREE_SLIP}
 
 CASES = [  # name, cells, bc, theta, precond, restart, max_iters, rtol, coefficient seed, rhs seed
-    ("ex_breakdown_P1", (4, 4), ["pp", "pp"], 0.0, "P1", 100, 300, 1e-300, 5, 3),
+    ("ex_breakdown_P1", (4, 4), ["pp", "pp"], 0.0, "P1", 30, 100, 1e-300, 5, None),
+    ("ex_breakdown_P2", (4, 4), ["pp", "nn"], 1.0, "P2", 30, 100, 1e-300, 8, None),
     ("ex_maxiter_2d", (16, 16), ["pp", "nn"], 1.0, "P1", 3, 7, 1e-12, 7, 4),
     ("ex_maxiter_3d", (8, 8, 8), ["pp", "pp", "pp"], 0.0, "P2", 3, 7, 1e-12, 9, 6),
 ]
+
+
+def invariant_rhs(g, c, kind):
+    """A rhs whose preconditioned Krylov space is exactly 2-dimensional:
+    z0 = P^-1 b spans two real eigenvectors of P^-1 M (dense 4x4-grid
+    operators built column by column from the reference's own P.apply /
+    apply_M), so the Arnoldi norm collapses to roundoff at iteration 2 in
+    any orthogonalisation scheme -- a breakdown the device must reproduce."""
+    from stokesmg.grid import pack_stokes, unpack_stokes
+    cs, _, _ = OP.rescale(c, G.StokesVector.zeros(g))
+    P = PC.Preconditioner(cs, PC.PrecondConfig(kind=PC.PrecondKind(kind)))
+    n = pack_stokes(G.StokesVector.zeros(g)).size
+    Pi, PiM = np.zeros((n, n)), np.zeros((n, n))
+    for i in range(n):
+        e = np.zeros(n)
+        e[i] = 1.0
+        v = unpack_stokes(g, e)
+        Pi[:, i] = pack_stokes(P.apply(v))
+        PiM[:, i] = pack_stokes(P.apply(OP.apply_M(v, cs)))
+    lam, vec = np.linalg.eig(PiM)
+    real = [k for k in np.argsort(-np.abs(lam)) if abs(lam[k].imag) < 1e-12 and abs(lam[k]) > 1e-6]
+    pick = [real[0]] + [k for k in real[1:] if abs(lam[k].real - lam[real[0]].real) > 0.1][:1]
+    z0 = sum(np.real(vec[:, k]) for k in pick)
+    b = np.linalg.lstsq(Pi, z0, rcond=None)[0]
+    assert np.linalg.norm(Pi @ b - z0) <= 1e-10 * np.linalg.norm(z0)
+    return cs, unpack_stokes(g, b)
 
 
 def main():
@@ -52,8 +80,11 @@ def main():
         mu = G.CellField(g, 0.5 + rng.random(cells))
         rho = G.CellField(g, 0.5 + rng.random(cells))
         c = OP.make_coefficients(g, theta, rho, mu)
-        rhs, _ = PR.make_rhs(g, c, seed=rseed)
-        cs, rs, spec = OP.rescale(c, rhs)
+        if rseed is None:
+            cs, rs = invariant_rhs(g, c, kind)
+        else:
+            rhs, _ = PR.make_rhs(g, c, seed=rseed)
+            cs, rs, spec = OP.rescale(c, rhs)
         gcfg = sm.GmresConfig(restart=restart, max_iters=max_iters, rtol=rtol, atol=0.0,
                               track_true_residual=True)
         x, hist = sm.gmres_solve(rs, cs, PC.PrecondConfig(kind=PC.PrecondKind(kind)), gcfg)
