@@ -47,7 +47,10 @@ struct ArgErr : std::runtime_error {
 
 constexpr int kMaxVec = 128;
 constexpr int kMaxLevels = 24;
-constexpr int kFlagInts = 16 + 2 * kMaxLevels;  // dflags: 16 setup-check slots + mu_e / constant-rho flags per level
+constexpr int kFlagInts = 16 + 2 * kMaxLevels;
+// GMRES: ||w'||^2 below this fraction of ||w||^2 (or ||c'||^2 > ||w'||^2 / 2)
+// finishes the Arnoldi step explicitly (direct second pass, sb_solver.cu gmres)
+constexpr double kDirectRel = 1e-10;  // dflags: 16 setup-check slots + mu_e / constant-rho flags per level
 
 struct Level {
   LevelDev d{};
@@ -1174,19 +1177,33 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
           sync(c);
           ww = hh2(c)[j + 1];
         }
-        for (int i = 0; i <= j; ++i) cc += hh2(c)[i] * hh2(c)[i];
-        // ||w'||^2 - ||c'||^2 cancels as w' approaches span(Q) (near a
-        // breakdown): then materialise s_{j+1} = w' - Q_{j+1} c' in slot j+1
-        // and take its norm directly, as the reference's ||w|| (krylov.py:114);
-        // nothing stays pending for the next pass A
-        const bool direct = cc > 0.5 * ww;
+        double dd = 0.0;
+        for (int i = 0; i <= j; ++i) {
+          cc += hh2(c)[i] * hh2(c)[i];
+          dd += hh1(c)[i] * hh1(c)[i];
+        }
+        // Near a breakdown (w nearly in span(Q)) the delayed scheme loses its
+        // accuracy: ||w'||^2 - ||c'||^2 cancels, and the Gram c' = d - G d
+        // carries an absolute error ~eps ||d|| that can exceed ||w'|| itself.
+        // Then finish the step explicitly: c' = Q^T w' re-read from the basis
+        // (gram) and s_{j+1} = w' - Q c' with its norm taken directly, as the
+        // reference's ||w|| (krylov.py:114).  Nothing stays pending.
+        const bool direct = cc > 0.5 * ww || ww < kDirectRel * (dd + ww);
         double gnext;
         if (direct) {
-          for (int i = 0; i <= j; ++i) hy(c)[i] = hh2(c)[i];
-          CK(cudaMemcpyAsync(dy(c), hy(c), (j + 1) * 8, cudaMemcpyHostToDevice, c->st));
-          launch_update_dot(c->st, V, vl, j + 1, dy(c), V + (long long)(j + 1) * vl, vl, c->dpart, 1);
+          double* sj = V + (long long)(j + 1) * vl;
+          if (gram) {
+            launch_multi_dot(c->st, V, vl, j + 1, sj, vl, c->dpart);
+            launch_finalize(c->st, c->dpart, j + 1, dy(c));
+          } else {
+            for (int i = 0; i <= j; ++i) hy(c)[i] = hh2(c)[i];
+            CK(cudaMemcpyAsync(dy(c), hy(c), (j + 1) * 8, cudaMemcpyHostToDevice, c->st));
+          }
+          launch_update_dot(c->st, V, vl, j + 1, dy(c), sj, vl, c->dpart, 1);
           launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
-          gnext = std::sqrt(fetch_misc(c, 1));
+          CK(cudaMemcpyAsync(hy(c), dy(c), (j + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+          gnext = std::sqrt(fetch_misc(c, 1));  // synchronises
+          for (int i = 0; i <= j; ++i) hh2(c)[i] = hy(c)[i];
           ++c->direct_norms;
         } else {
           gnext = std::sqrt(std::max(ww - cc, 0.0));

@@ -41,6 +41,11 @@ CODE = {"p": G.PERIODIC, "n": G.NO_SLIP, "f": G.FREE_SLIP}
 CASES = [  # name, cells, bc, theta, precond, restart, max_iters, rtol, coefficient seed, rhs seed
     ("ex_breakdown_P1", (4, 4), ["pp", "pp"], 0.0, "P1", 30, 100, 1e-300, 5, None),
     ("ex_breakdown_P2", (4, 4), ["pp", "nn"], 1.0, "P2", 30, 100, 1e-300, 8, None),
+    # Krylov space exhausted after ~40 Arnoldi steps (a random rhs on a 4x4
+    # grid): where the Arnoldi norm collapses is roundoff-determined (the
+    # reference's MGS stops at 40, CGS2 variants at 38), so the device test
+    # allows +-3 iterations here
+    ("ex_exhaust_P1", (4, 4), ["pp", "pp"], 0.0, "P1", 100, 300, 1e-300, 5, 3),
     ("ex_maxiter_2d", (16, 16), ["pp", "nn"], 1.0, "P1", 3, 7, 1e-12, 7, 4),
     ("ex_maxiter_3d", (8, 8, 8), ["pp", "pp", "pp"], 0.0, "P2", 3, 7, 1e-12, 9, 6),
 ]
@@ -108,7 +113,8 @@ def main():
         put("hist", np.array(hist.rows(), dtype=np.float64))
         index.append(dict(name=name, kind="gmres_exit", cells=list(cells), h=g.h, bc=bc, theta=cs.theta,
                           form="stress", precond=kind, restart=restart, max_iters=max_iters, rtol=rtol,
-                          status=hist.status, iterations=hist.iterations))
+                          status=hist.status, iterations=hist.iterations,
+                          its_tol=3 if name.startswith("ex_exhaust") else 0))
         print(name, hist.status, hist.iterations)
     np.savez_compressed(OUT / "golden_exit.npz", **store)
     (OUT / "golden_exit.json").write_text(json.dumps(index, indent=1))

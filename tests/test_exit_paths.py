@@ -108,7 +108,7 @@ def test_device_exit_paths(name):
                        track_true_residual=True)
     x, hist = gmres_solve(rs, cs, PrecondConfig(kind=PrecondKind(e["precond"])), gcfg)
     got, ref, k = _check_history(e, hist.rows(), hist.status, hist.iterations,
-                                 1 if e["status"] == "breakdown" else 0)
+                                 e.get("its_tol", 1 if e["status"] == "breakdown" else 0))
     if e["status"] == "maxiter":
         assert got.shape == ref.shape
         assert np.allclose(got[:, 2], ref[:, 2], rtol=1e-6)
@@ -116,6 +116,11 @@ def test_device_exit_paths(name):
     from paper_1308_4605_b200.grid import CellField, FaceField, StokesVector
     xr = pack_stokes(StokesVector(FaceField(g, tuple(_arr(name, f"xu{a}") for a in range(g.dim))),
                                   CellField(g, _arr(name, "xp"))))
+    if e.get("its_tol", 0) > 1:  # roundoff-determined stop: compare through the residual
+        k = min(len(got), len(ref)) - 3
+        assert np.allclose(got[:k, 2], ref[:k, 2], rtol=1e-6, atol=1e-12 * ref[0, 2])
+        assert got[-1, 3] <= 1e-10 * ref[0, 3]
+        return
     assert np.linalg.norm(pack_stokes(x) - xr) <= 1e-8 * np.linalg.norm(xr)
 
 
