@@ -1636,7 +1636,8 @@ k_dcgs_a_g(double* __restrict__ Q, long long vstride, int k, const double* __res
 template <int CH>
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
-            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+            const double* __restrict__ w, long long n2, double* __restrict__ partials,
+            const double* __restrict__ /*means: A/B variant without the deferral*/, long long /*bb*/) {
   pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
@@ -1731,10 +1732,16 @@ __device__ __forceinline__ double warp_sum_many(double* v, int lane) {
 // per thread in flight, and the 2G dot products of a group reduced across the
 // warp by one transpose-reduction (2G-1 + 5-log2(2G) shuffles instead of 10G).
 // q_j = (s - sum_i c_i Q_i) * inv_gamma keeps the ascending-i update order.
-template <int CH, int G, int MB = 2>
+// MEANS: the null-space projection deferred from P^-1 is applied to w on
+// load (w - means[b] on the b-th block of bb double2, pass B's expression), so
+// d = Q^T (projected w) is exactly what pass B subtracts: the Gram identity
+// c' = d - G d then holds to roundoff even when the means dominate w (near a
+// breakdown, where Q^T 1 = O(eps) would otherwise leak into d).
+template <int CH, int G, int MB = 2, bool MEANS = false>
 __global__ void __launch_bounds__(kThreads, MB)
 k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
-            const double* __restrict__ w, long long n2, double* __restrict__ partials) {
+            const double* __restrict__ w, long long n2, double* __restrict__ partials,
+            const double* __restrict__ means = nullptr, long long bb = 0) {
   pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
@@ -1754,6 +1761,12 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
       const long long e = base + t * blockDim.x + threadIdx.x;
       ok[t] = e < n2;
       wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      if (MEANS && ok[t]) {
+        const int bi = (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
+        const double m = __ldg(means + bi);
+        wv[t].x = wv[t].x - m;
+        wv[t].y = wv[t].y - m;
+      }
       sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
       q[t] = sv[t];
     }
@@ -2891,8 +2904,15 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
 }
 
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
-                     const double* w, long long n, double* partials) {
+                     const double* w, long long n, double* partials, const double* means, long long block) {
   ++g_kernel_launches;
+  if (means) {  // deferred null projection: the grouped kernel with the means applied on load
+    static const int grid_m = wave_grid(k_dcgs_a_g3<4, 2, 2, true>);
+    g_red_blocks_used = grid_m;
+    launch_k(k_dcgs_a_g3<4, 2, 2, true>, grid_m, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials,
+             means, block / 2);
+    return;
+  }
   // SB_DCGS_A: 0 un-chunked, 2 register-chunked (CH 4), 32 / 34 / 24 (default)
   // / 323 / 343 grouped
   // basis reads (CH 2 or 4 double2 per thread, G 2 or 4 vectors per group;
@@ -2904,7 +2924,7 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
   {                                                                                 \
     static const int grid_a = wave_grid(KER);                                       \
     g_red_blocks_used = grid_a;                                                     \
-    launch_k(KER, grid_a, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials); \
+    launch_k(KER, grid_a, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials, nullptr, 0LL); \
   }
   switch (variant) {
     case 0: launch_k(k_dcgs_a_g, kRedBlocks, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials); break;

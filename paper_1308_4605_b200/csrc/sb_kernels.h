@@ -170,8 +170,10 @@ void launch_update_dot(cudaStream_t s, const double* V, long long vstride, int n
                        double* w, long long n, double* partials, int mode);  // mode 0: dots, 1: norm
 void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out);
 // Gram-matrix variant of the delayed-reorthogonalisation passes
+// means (nullable): the deferred null projection applied to w on load (as pass B)
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
-                     const double* w, long long n, double* partials);
+                     const double* w, long long n, double* partials, const double* means = nullptr,
+                     long long block = 0);
 // means (nullable): per-block values subtracted from w first (deferred null projection,
 // blocks of `block` elements, at most 4)
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,

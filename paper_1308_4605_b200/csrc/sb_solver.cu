@@ -1140,7 +1140,8 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         if (j > 0) CK(cudaMemcpyAsync(dh2(c), hy(c), j * 8, cudaMemcpyHostToDevice, c->st));
         double cc = 0.0, ww;
         if (gram) {
-          launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart);
+          launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart,
+                          c->defer_nulls ? dmeans(c) : nullptr, c->lv[0].block);
           launch_finalize(c->st, c->dpart, 2 * j + 2, dh1(c));
           launch_dcgs_b_g(c->st, V, vl, j + 1, dh1(c), c->vw, V + (long long)(j + 1) * vl, vl, c->dpart,
                           c->defer_nulls ? dmeans(c) : nullptr, c->lv[0].block);

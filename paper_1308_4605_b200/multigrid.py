@@ -92,16 +92,6 @@ class MgHierarchy:
             self._levels = out
         return self._levels
 
-
-def _pair_mean_all(x):
-    for a in range(x.ndim):
-        sl0 = [slice(None)] * x.ndim
-        sl1 = [slice(None)] * x.ndim
-        sl0[a], sl1[a] = slice(0, None, 2), slice(1, None, 2)
-        x = 0.5 * (x[tuple(sl0)] + x[tuple(sl1)])
-    return x
-
-
     def diag_face(self, level: int) -> FaceField:
         """The velocity smoother's diagonal on ``level`` (multigrid.py:79-89);
         ZeroDivisionError on a zero interior entry, as the reference."""
@@ -122,6 +112,15 @@ def _pair_mean_all(x):
         if np.any(out == 0):
             raise ZeroDivisionError("zero diagonal in pressure operator")
         return CellField(g, out)
+
+
+def _pair_mean_all(x):
+    for a in range(x.ndim):
+        sl0 = [slice(None)] * x.ndim
+        sl1 = [slice(None)] * x.ndim
+        sl0[a], sl1[a] = slice(0, None, 2), slice(1, None, 2)
+        x = 0.5 * (x[tuple(sl0)] + x[tuple(sl1)])
+    return x
 
 
 def build_hierarchy(grid, coeff) -> MgHierarchy:
