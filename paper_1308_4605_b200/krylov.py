@@ -95,9 +95,49 @@ def _history(rows, n, status) -> ConvergenceHistory:
 def _device_precond(coeff, pcfg, smoother, precond):
     if precond is None:
         return Preconditioner(coeff, pcfg, smoother)
-    if not isinstance(precond, Preconditioner):
-        raise TypeError("precond must be a paper_1308_4605_b200 Preconditioner (device path)")
+    if not hasattr(precond, "apply") or not hasattr(precond, "scalar_vcycles"):
+        raise TypeError("precond must provide .apply(StokesVector) and .scalar_vcycles (krylov.py:180-207)")
     return precond
+
+
+def _solve_operator_callback(rhs, coeff, P, gcfg):
+    """gmres_solve (krylov.py:164-214) for preconditioners that are not the
+    fused device P^-1 -- the dense exact-subsolver study path and any
+    duck-typed ``precond=`` object (the reference's seam): the Krylov basis and
+    Arnoldi run on the device (``gmres_kernel`` / ``sb_gmres_flat``), M on the
+    device (one context), and P.apply is called on the host fields as the
+    reference calls it."""
+    from .grid import pack_stokes, unpack_stokes
+    from .operators import _ctx_for
+    g = as_grid(rhs.u.grid)
+    ctx = _ctx_for(coeff, g)
+    history = ConvergenceHistory()
+    b_raw = pack_stokes(rhs)
+    rhs_norm = float(np.linalg.norm(b_raw))
+
+    def apply_op(v):
+        return pack_stokes(P.apply(apply_M(unpack_stokes(g, v), coeff, ctx=ctx)))
+
+    z0 = pack_stokes(P.apply(rhs))
+    rp0 = float(np.linalg.norm(z0))
+    history.add(0, P.scalar_vcycles, rp0, rhs_norm, False)
+    if rp0 <= gcfg.atol or rp0 == 0.0:
+        history.status = "converged"
+        return StokesVector.zeros(g), history
+    target = gcfg.rtol * rp0 + gcfg.atol
+    breakdown_tol = max(gcfg.atol, 1e-14 * rp0)
+
+    def callback(k, xvec, rp, restart_flag):
+        if gcfg.track_true_residual:
+            mx = pack_stokes(apply_M(unpack_stokes(g, xvec), coeff, ctx=ctx))
+            rt = float(np.linalg.norm(b_raw - mx))
+        else:
+            rt = float("nan")
+        history.add(k, P.scalar_vcycles, rp, rt, restart_flag)
+
+    xvec, status, _ = gmres_kernel(apply_op, z0, gcfg.restart, gcfg.max_iters, target, breakdown_tol, callback)
+    history.status = status
+    return unpack_stokes(g, xvec), history
 
 
 def solve_raw(P: Preconditioner, gcfg, bu, bp, xu, xp):
@@ -127,6 +167,8 @@ def gmres_solve(rhs, coeff, pcfg: PrecondConfig, gcfg: GmresConfig,
     """
     g = as_grid(rhs.u.grid)
     P = _device_precond(coeff, pcfg, smoother, precond)
+    if not isinstance(P, Preconditioner) or P.exact:
+        return _solve_operator_callback(rhs, coeff, P, gcfg)
     xu = [_lib.pinned.array(g.face_shape(a)) for a in range(g.dim)]
     xp = _lib.pinned.array(g.cells)
     hist = solve_raw(P, gcfg, [_f64(c) for c in rhs.u.components], _f64(rhs.p.data), xu, xp)

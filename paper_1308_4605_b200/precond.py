@@ -7,8 +7,11 @@ keeps its contract -- ``apply(StokesVector) -> StokesVector`` and the
 (``sb_ctx``): the multigrid hierarchy is built on the B200 at construction and
 each ``apply`` is one ``sb_precond_apply`` call (velocity V-cycle, pressure
 V-cycle, glue kernels and null projection, replayed as a CUDA graph).
-Dense exact subsolvers (``exact_subsolvers=True``, the reference's
-small-grid LU study path ``_exact.py``) are outside the device hot path.
+With dense exact subsolvers (``exact_subsolvers=True``, the reference's
+small-grid LU study path, ``_exact.py``) the same block algebra (:111-168) is
+composed from device operator calls (div, grad, apply_A, apply_schur_inv) and
+the device-factorised dense solves; it runs no V-cycles and leaves the counter
+untouched, as the reference.
 """
 
 from __future__ import annotations
@@ -67,9 +70,10 @@ class Preconditioner:
     """Applies P^{-1}; counts scalar V-cycles (d per velocity solve, 1 per Poisson)."""
 
     def __init__(self, coeff, cfg: PrecondConfig, smoother: SmootherParams | None = None):
-        if getattr(cfg, "exact_subsolvers", False):
-            raise NotImplementedError(
-                "exact (dense LU) subsolvers are a small-grid study path outside the device solve")
+        self.exact = bool(getattr(cfg, "exact_subsolvers", False))
+        if self.exact:
+            self._init_exact(coeff, cfg, smoother)
+            return
         self.coeff = coeff
         self.grid = as_grid(coeff.grid)
         self.cfg = cfg
@@ -85,7 +89,86 @@ class Preconditioner:
         self._pc = precond_c(cfg)
         self._sm = smoother_c(self.smoother)
 
+    # -- dense exact subsolvers (precond.py:73-82, :91-168) ---------------------
+
+    def _init_exact(self, coeff, cfg, smoother):
+        from ._exact import DenseCellSolver, DenseFaceSolver
+        self.coeff = coeff
+        self.grid = as_grid(coeff.grid)
+        self.cfg = cfg
+        self.smoother = smoother if smoother is not None else SmootherParams()
+        self.scalar_vcycles = 0
+        self._null_comps = velocity_null_components(self.grid, coeff)
+        self.ctx = None
+        self._hierarchy = None
+        self._face_solver = self._cell_solver = None
+        if getattr(cfg.kind, "value", cfg.kind) == "identity":
+            return
+        self._face_solver = DenseFaceSolver(self.grid, coeff)
+        if self._needs_poisson():
+            self._cell_solver = DenseCellSolver(self.grid, coeff)
+
+    def _needs_poisson(self) -> bool:
+        return getattr(self.cfg.kind, "value", self.cfg.kind) == "P1" or self.coeff.theta > 0
+
+    def velocity_solve(self, b):
+        if self._face_solver is None:
+            raise RuntimeError("velocity_solve is the exact-subsolver seam (device V-cycles run inside apply)")
+        return self._face_solver.solve(b)
+
+    def pressure_solve(self, b):
+        if self._cell_solver is None:
+            raise RuntimeError("pressure_solve is the exact-subsolver seam (device V-cycles run inside apply)")
+        return self._cell_solver.solve(b)
+
+    def _apply_exact(self, r) -> StokesVector:
+        from .operators import apply_A, div, grad
+        from .schur import apply_schur_inv, schur_diagonal
+        kind = getattr(self.cfg.kind, "value", self.cfg.kind)
+        if kind == "identity":
+            return r.copy()
+        g, coeff = self.grid, self.coeff
+        sign = -1.0 if getattr(self.cfg.schur.sign, "value", self.cfg.schur.sign) == MINUS.value else 1.0
+        schur = lambda b: apply_schur_inv(b, coeff, self.cfg.schur,
+                                          self.pressure_solve if coeff.theta > 0 else None)
+        if kind == "P1":
+            xu_star = self.velocity_solve(r.u)
+            b_c = div(xu_star) + r.p
+            phi = self.pressure_solve(b_c)
+            xu = xu_star.copy()
+            gphi = grad(phi)
+            for a in range(g.dim):
+                xu.components[a][...] -= gphi.components[a] / coeff.rho_face.components[a]
+                if not g.periodic(a):
+                    xu.components[a][(slice(None),) * a + (0,)] = 0.0
+                    xu.components[a][(slice(None),) * a + (-1,)] = 0.0
+            s_inv = CellField(g, schur_diagonal(coeff) * b_c.data - coeff.theta * phi.data)
+            x = StokesVector(xu, s_inv * sign)
+        elif kind == "P2":
+            xu = self.velocity_solve(r.u)
+            x = StokesVector(xu, schur(div(xu) + r.p) * sign)
+        elif kind == "P3":
+            xp = schur(r.p) * sign
+            x = StokesVector(self.velocity_solve(r.u - grad(xp)), xp)
+        elif kind == "P4":
+            x = StokesVector(self.velocity_solve(r.u), schur(r.p) * sign)
+        elif kind == "P5":
+            xu_star = self.velocity_solve(r.u)
+            xp = schur(div(xu_star) + r.p) * sign
+            b2 = r.u - grad(xp) - apply_A(xu_star, coeff)
+            x = StokesVector(xu_star + self.velocity_solve(b2), xp)
+        else:
+            raise ValueError(f"unknown preconditioner kind {kind}")
+        from .grid import subtract_mean
+        x = StokesVector(x.u, subtract_mean(x.p))
+        for a in self._null_comps:
+            view = x.u.interior(a)
+            view -= view.mean()
+        return x
+
     def apply(self, r) -> StokesVector:
+        if self.exact:
+            return self._apply_exact(r)
         g = self.grid
         ru = [_f64(c) for c in r.u.components]
         xu = [np.zeros(g.face_shape(a)) for a in range(g.dim)]

@@ -70,3 +70,13 @@ def apply_schur_inv(r, coeff, cfg: SchurConfig, pressure_solve=None):
     _lib.check(ctx.lib.sb_schur_inv(ctx.h, _lib.ptr(_f64(r.data)), _lib.ptr(phi) if phi is not None else None,
                                     _lib.ptr(out)))
     return CellField(g, out)
+
+
+def exact_schur_apply(p, coeff, face_solver=None):
+    """Reference -D A^-1 G p through the dense exact velocity solve (schur.py:81-92;
+    small grids only): device grad / div and the device-factorised A."""
+    from ._exact import DenseFaceSolver
+    from .operators import div, grad
+    if face_solver is None:
+        face_solver = DenseFaceSolver(p.grid, coeff)
+    return -div(face_solver.solve(grad(p)))
