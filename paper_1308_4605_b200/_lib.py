@@ -166,7 +166,7 @@ def check(rc: int):
     raise RuntimeError(f"stokesb200 CUDA failure: {msg}")
 
 
-def ptr(a) -> int:
+def address(a) -> int:
     """Address of a C-contiguous float64 NumPy array or torch tensor (host or CUDA)."""
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or not a.flags.c_contiguous:
@@ -178,9 +178,24 @@ def ptr(a) -> int:
     return a.data_ptr()
 
 
+def ptr(a):
+    """``c_void_p`` to an array that keeps the array alive while the pointer
+    object lives: ``ptr(_f64(x))`` passed straight into a C call must not let
+    a temporary contiguous copy be freed before the call runs."""
+    out = C.c_void_p(address(a))
+    out._keep = a
+    return out
+
+
 def parr(arrs):
-    vals = [C.c_void_p(ptr(a) if a is not None else 0) for a in arrs]
-    return (C.c_void_p * max(len(vals), 1))(*vals)
+    """Pointer array for a list of arrays.  The returned ctypes array keeps the
+    arrays alive: callers pass temporaries (``[_f64(c) for c in ...]`` copies
+    of non-contiguous views) that must outlive the C call."""
+    arrs = list(arrs)
+    vals = [C.c_void_p(address(a) if a is not None else 0) for a in arrs]
+    out = (C.c_void_p * max(len(vals), 1))(*vals)
+    out._keep = arrs
+    return out
 
 
 class PinnedPool:

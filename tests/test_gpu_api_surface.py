@@ -201,3 +201,31 @@ def test_reference_test_modules_against_the_package():
     log.parent.mkdir(exist_ok=True)
     log.write_text(out.stdout + out.stderr)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+
+
+def test_non_contiguous_inputs():
+    """Arrays that are views (np.real of a complex field, strided slices) are
+    copied to contiguous temporaries at the boundary; the temporaries must
+    outlive the C call (a reference test's Fourier-mode inputs exposed a
+    use-after-free here).  Results equal those of contiguous copies."""
+    from paper_1308_4605_b200 import operators as OPS_
+    from paper_1308_4605_b200.grid import PERIODIC, CellField, FaceField, GridSpec, StokesVector
+    from paper_1308_4605_b200.operators import make_coefficients
+    g = GridSpec((8, 8, 8), 0.5, ((PERIODIC, PERIODIC),) * 3)
+    rng = np.random.default_rng(5)
+    c = make_coefficients(g, 0.3, CellField(g, 1 + rng.random(g.cells)), CellField(g, 1 + rng.random(g.cells)))
+    z = [rng.standard_normal(g.face_shape(a)) + 1j * rng.standard_normal(g.face_shape(a)) for a in range(3)]
+    zp = rng.standard_normal(g.cells) + 1j * rng.standard_normal(g.cells)
+    views = FaceField(g, tuple(np.real(x) for x in z))
+    copies = FaceField(g, tuple(np.ascontiguousarray(np.real(x)) for x in z))
+    assert not views.components[0].flags.c_contiguous
+    for f in (OPS_.apply_A, OPS_.apply_viscous):
+        a, b = f(views, c), f(copies, c)
+        for k in range(3):
+            assert np.array_equal(a.components[k], b.components[k])
+    pv, pc = CellField(g, np.imag(zp)), CellField(g, np.ascontiguousarray(np.imag(zp)))
+    m1 = OPS_.apply_M(StokesVector(views, pv), c)
+    m2 = OPS_.apply_M(StokesVector(copies, pc), c)
+    assert np.array_equal(m1.p.data, m2.p.data)
+    assert np.array_equal(OPS_.div(views).data, OPS_.div(copies).data)
+    assert np.array_equal(OPS_.lap_pressure(pv).data, OPS_.lap_pressure(pc).data)
