@@ -1637,7 +1637,8 @@ template <int CH>
 __global__ void __launch_bounds__(kThreads)
 k_dcgs_a_g2(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
             const double* __restrict__ w, long long n2, double* __restrict__ partials,
-            const double* __restrict__ /*means: A/B variant without the deferral*/, long long /*bb*/) {
+            const double* __restrict__ /*means: A/B variant without the deferral*/, long long /*bb*/,
+            double* __restrict__ /*wout*/, long long /*gh*/) {
   pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
@@ -1737,16 +1738,23 @@ __device__ __forceinline__ double warp_sum_many(double* v, int lane) {
 // d = Q^T (projected w) is exactly what pass B subtracts: the Gram identity
 // c' = d - G d then holds to roundoff even when the means dominate w (near a
 // breakdown, where Q^T 1 = O(eps) would otherwise leak into d).
-template <int CH, int G, int MB = 2, bool MEANS = false>
+//
+// W1 (one-pass Arnoldi, sb_solver.cu gmres): also ||w||^2 (slot 2k+2) and w
+// (projected by the means) stored to wout = basis slot k+1 -- the next
+// step's unfinished vector, whose pending projection the next pass A applies,
+// so no second stream over the basis.  gh: slab blocks keep their first / last
+// gh double2 (ghost planes) at 0, the means are not applied there.
+template <int CH, int G, int MB = 2, bool MEANS = false, bool W1 = false>
 __global__ void __launch_bounds__(kThreads, MB)
 k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
             const double* __restrict__ w, long long n2, double* __restrict__ partials,
-            const double* __restrict__ means = nullptr, long long bb = 0) {
+            const double* __restrict__ means = nullptr, long long bb = 0, double* __restrict__ wout = nullptr,
+            long long gh = 0) {
   pdl_enter();
   __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
   __shared__ double cs[kMaxVec];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nslot = 2 * k + 2;
+  const int nslot = 2 * k + 2 + (W1 ? 1 : 0);
   for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
   for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
   __syncthreads();
@@ -1763,7 +1771,11 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
       wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
       if (MEANS && ok[t]) {
         const int bi = (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
-        const double m = __ldg(means + bi);
+        double m = __ldg(means + bi);
+        if (gh) {
+          const long long la = e - bi * bb;
+          if (la < gh || la >= bb - gh) m = 0.0;
+        }
         wv[t].x = wv[t].x - m;
         wv[t].y = wv[t].y - m;
       }
@@ -1818,19 +1830,38 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
       const double r = warp_sum_many<2>(dv, lane);
       if (lane < 2) acc[lane ? k + 1 + i : i][warp] += r;
     }
-    double dv[2] = {0.0, 0.0};
+    if (W1) {
+      double dv[4] = {0.0, 0.0, 0.0, 0.0};
+      double2* o2 = reinterpret_cast<double2*>(wout);
 #pragma unroll
-    for (int t = 0; t < CH; ++t) {
-      if (k > 0) {
-        q[t].x *= inv_gamma;
-        q[t].y *= inv_gamma;
-        if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+      for (int t = 0; t < CH; ++t) {
+        if (k > 0) {
+          q[t].x *= inv_gamma;
+          q[t].y *= inv_gamma;
+          if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+        }
+        if (ok[t]) o2[base + t * blockDim.x + threadIdx.x] = wv[t];
+        dv[0] += q[t].x * wv[t].x + q[t].y * wv[t].y;
+        dv[1] += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+        dv[2] += wv[t].x * wv[t].x + wv[t].y * wv[t].y;
       }
-      dv[0] += q[t].x * wv[t].x + q[t].y * wv[t].y;
-      dv[1] += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+      const double r = warp_sum_many<4>(dv, lane);
+      if (lane < 3) acc[lane == 0 ? k : (lane == 1 ? 2 * k + 1 : 2 * k + 2)][warp] += r;
+    } else {
+      double dv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        if (k > 0) {
+          q[t].x *= inv_gamma;
+          q[t].y *= inv_gamma;
+          if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+        }
+        dv[0] += q[t].x * wv[t].x + q[t].y * wv[t].y;
+        dv[1] += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+      }
+      const double r = warp_sum_many<2>(dv, lane);
+      if (lane < 2) acc[lane ? 2 * k + 1 : k][warp] += r;
     }
-    const double r = warp_sum_many<2>(dv, lane);
-    if (lane < 2) acc[lane ? 2 * k + 1 : k][warp] += r;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
@@ -2910,7 +2941,7 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
     static const int grid_m = wave_grid(k_dcgs_a_g3<4, 2, 2, true>);
     g_red_blocks_used = grid_m;
     launch_k(k_dcgs_a_g3<4, 2, 2, true>, grid_m, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials,
-             means, block / 2);
+             means, block / 2, nullptr, 0LL);
     return;
   }
   // SB_DCGS_A: 0 un-chunked, 2 register-chunked (CH 4), 32 / 34 / 24 (default)
@@ -2924,7 +2955,8 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
   {                                                                                 \
     static const int grid_a = wave_grid(KER);                                       \
     g_red_blocks_used = grid_a;                                                     \
-    launch_k(KER, grid_a, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials, nullptr, 0LL); \
+    launch_k(KER, grid_a, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials, nullptr, 0LL, nullptr, \
+             0LL);                                                                  \
   }
   switch (variant) {
     case 0: launch_k(k_dcgs_a_g, kRedBlocks, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials); break;
@@ -2936,6 +2968,24 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
     default: SB_DCGS_A_LAUNCH((k_dcgs_a_g3<4, 2>)); break;
   }
 #undef SB_DCGS_A_LAUNCH
+}
+
+void launch_arnoldi1(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
+                     const double* w, long long n, double* partials, const double* means, long long block,
+                     long long ghost) {
+  ++g_kernel_launches;
+  double* wout = Q + (long long)(k + 1) * vstride;
+  if (means) {
+    static const int grid_m = wave_grid(k_dcgs_a_g3<4, 2, 2, true, true>);
+    g_red_blocks_used = grid_m;
+    launch_k(k_dcgs_a_g3<4, 2, 2, true, true>, grid_m, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2,
+             partials, means, block / 2, wout, ghost / 2);
+  } else {
+    static const int grid_p = wave_grid(k_dcgs_a_g3<4, 2, 2, false, true>);
+    g_red_blocks_used = grid_p;
+    launch_k(k_dcgs_a_g3<4, 2, 2, false, true>, grid_p, kThreads, 0, s, Q, vstride, k, c, inv_gamma, w, n / 2,
+             partials, nullptr, 0LL, wout, 0LL);
+  }
 }
 
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,

@@ -174,6 +174,12 @@ void launch_finalize(cudaStream_t s, const double* partials, int nv, double* out
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                      const double* w, long long n, double* partials, const double* means = nullptr,
                      long long block = 0);
+// One-pass Arnoldi (Gram variant without pass B): pass A plus ||w||^2 (slot
+// 2k+2) and the (means-projected) w stored to basis slot k+1; ghost: elements
+// kept 0 at each block end (slab blocks)
+void launch_arnoldi1(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
+                     const double* w, long long n, double* partials, const double* means = nullptr,
+                     long long block = 0, long long ghost = 0);
 // means (nullable): per-block values subtracted from w first (deferred null projection,
 // blocks of `block` elements, at most 4)
 void launch_dcgs_b_g(cudaStream_t s, const double* Q, long long vstride, int nv, const double* d, const double* w,

@@ -50,7 +50,10 @@ constexpr int kMaxLevels = 24;
 constexpr int kFlagInts = 16 + 2 * kMaxLevels;
 // GMRES: ||w'||^2 below this fraction of ||w||^2 (or ||c'||^2 > ||w'||^2 / 2)
 // finishes the Arnoldi step explicitly (direct second pass, sb_solver.cu gmres)
-constexpr double kDirectRel = 1e-10;  // dflags: 16 setup-check slots + mu_e / constant-rho flags per level
+constexpr double kDirectRel = 1e-10;
+// one-pass Arnoldi: gam_{j+1}^2 below this fraction of ||w||^2 finishes the
+// step explicitly (the implicit norm then carries < ~1e-10 relative error)
+constexpr double kOnePassRel = 1e-6;  // dflags: 16 setup-check slots + mu_e / constant-rho flags per level
 
 struct Level {
   LevelDev d{};
@@ -1078,7 +1081,12 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     const char* e = std::getenv("SB_ORTHO");
     return !(e && (std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
   }();
-  std::vector<double> G((m + 1) * (m + 1), 0.0);
+  // default: one-pass Gram Arnoldi (SB_ORTHO=gram2: the two-pass Gram variant)
+  static const bool one_pass = [] {
+    const char* e = std::getenv("SB_ORTHO");
+    return !(e && (std::strcmp(e, "gram2") == 0 || std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
+  }();
+  std::vector<double> G((m + 1) * (m + 1), 0.0), tv(m + 1);
   double gam = 1.0;
   int k = 0;
   bool first = true;
@@ -1139,6 +1147,86 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         for (int i = 0; i < j; ++i) hy(c)[i] = cpend[i];
         if (j > 0) CK(cudaMemcpyAsync(dh2(c), hy(c), j * 8, cudaMemcpyHostToDevice, c->st));
         double cc = 0.0, ww;
+        if (one_pass) {
+          // One pass over the basis per iteration.  Pass A finishes q_j, forms
+          // d = Q_{j+1}^T w, the Gram extension and ||w||^2, and stores w
+          // (projected by the deferred means) into slot j+1 as the unfinished
+          // s_{j+1} = gam_{j+1} q_{j+1} + Q_{j+1} t with t = d + c' (c' = d - G d,
+          // the CGS2 correction), gam_{j+1}^2 = ||w||^2 - 2 t.d + t^T G t.  The
+          // next pass A applies t while it streams the basis, so the separate
+          // pass B (w' = w - Q d) disappears.  Near a breakdown (gam_{j+1}^2 <
+          // kOnePassRel ||w||^2) the step is finished explicitly: two streamed
+          // CGS passes on slot j+1 and a direct norm (krylov.py:114).
+          double* sj1 = V + (long long)(j + 1) * vl;
+          launch_arnoldi1(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart,
+                          c->defer_nulls ? dmeans(c) : nullptr, c->lv[0].block);
+          launch_finalize(c->st, c->dpart, 2 * j + 3, dh1(c));
+          CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (2 * j + 3) * 8, cudaMemcpyDeviceToHost, c->st));
+          sync(c);
+          const double* dd = hh1(c);
+          const double* sd = hh1(c) + j + 1;
+          const double ss = hh1(c)[2 * j + 1];
+          const double wwf = hh1(c)[2 * j + 2];
+          double cgc = 0.0, csd = 0.0;
+          for (int l = 0; l < j; ++l) {
+            double gcl = 0.0;
+            for (int t = 0; t < j; ++t) gcl += G[l * (m + 1) + t] * cpend[t];
+            const double gjl = (sd[l] - gcl) / gam;
+            G[j * (m + 1) + l] = gjl;
+            G[l * (m + 1) + j] = gjl;
+            cgc += cpend[l] * gcl;
+            csd += cpend[l] * sd[l];
+          }
+          G[j * (m + 1) + j] = j == 0 ? ss : (ss - 2.0 * csd + cgc) / (gam * gam);
+          std::vector<double> cp(j + 1);
+          for (int i = 0; i <= j; ++i) {
+            double gd = 0.0;
+            for (int t = 0; t <= j; ++t) gd += G[i * (m + 1) + t] * dd[t];
+            cp[i] = dd[i] - gd;
+            tv[i] = dd[i] + cp[i];
+          }
+          double td = 0.0, tgt = 0.0;
+          for (int i = 0; i <= j; ++i) {
+            double gt = 0.0;
+            for (int t = 0; t <= j; ++t) gt += G[i * (m + 1) + t] * tv[t];
+            td += tv[i] * dd[i];
+            tgt += tv[i] * gt;
+          }
+          const double r2 = wwf - 2.0 * td + tgt;
+          const bool direct = !(r2 > kOnePassRel * wwf);
+          double gnext;
+          if (direct) {
+            for (int i = 0; i <= j; ++i) hy(c)[i] = dd[i];
+            CK(cudaMemcpyAsync(dy(c), hy(c), (j + 1) * 8, cudaMemcpyHostToDevice, c->st));
+            launch_update_dot(c->st, V, vl, j + 1, dy(c), sj1, vl, c->dpart, 0);
+            launch_finalize(c->st, c->dpart, j + 1, dy(c) + kMaxVec);
+            launch_update_dot(c->st, V, vl, j + 1, dy(c) + kMaxVec, sj1, vl, c->dpart, 1);
+            launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
+            CK(cudaMemcpyAsync(hy(c), dy(c) + kMaxVec, (j + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+            gnext = std::sqrt(fetch_misc(c, 1));  // synchronises
+            for (int i = 0; i <= j; ++i) cp[i] = hy(c)[i];
+            ++c->direct_norms;
+          } else {
+            gnext = std::sqrt(r2);
+          }
+          for (int i = 0; i <= j; ++i) {
+            double e = 0.0;
+            for (int t = 0; t < j; ++t) e += Horig[i * m + t] * cpend[t];
+            H[i * m + j] = ((dd[i] - e) + cp[i]) / gam;
+          }
+          hn = gnext / gam;
+          static const bool trace1 = [] {
+            const char* e = std::getenv("SB_GMRES_TRACE");
+            return e && e[0] == '1';
+          }();
+          if (trace1)
+            std::fprintf(stderr, "gmres1 k=%d j=%d ww=%.6e r2=%.6e gnext=%.6e gam=%.6e hn=%.6e direct=%d\n", k, j,
+                         wwf, r2, gnext, gam, hn, (int)direct);
+          for (int i = 0; i <= j; ++i) Horig[i * m + j] = H[i * m + j];
+          Horig[(j + 1) * m + j] = hn;
+          for (int i = 0; i <= j; ++i) cpend[i] = direct ? 0.0 : dd[i] + cp[i];
+          gam = gnext;
+        } else {
         if (gram) {
           launch_dcgs_a_g(c->st, V, vl, j, dh2(c), 1.0 / gam, c->vw, vl, c->dpart,
                           c->defer_nulls ? dmeans(c) : nullptr, c->lv[0].block);
@@ -1226,6 +1314,7 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
         Horig[(j + 1) * m + j] = hn;
         for (int i = 0; i <= j; ++i) cpend[i] = direct ? 0.0 : hh2(c)[i];
         gam = gnext;
+        }  // two-pass Gram / DCGS
       }
       H[(j + 1) * m + j] = hn;
       for (int i = 0; i < j; ++i) {
