@@ -1081,10 +1081,17 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     const char* e = std::getenv("SB_ORTHO");
     return !(e && (std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
   }();
-  // default: one-pass Gram Arnoldi (SB_ORTHO=gram2: the two-pass Gram variant)
+  // SB_ORTHO=gram1: one-pass Gram Arnoldi (opt-in).  It removes pass B (C5
+  // 256^3 launch list 336 -> 321 ms) but its pending coefficients t = d + c'
+  // are first order (||t|| / gam_{j+1} = ||w|| / ||r||, growing along a cycle),
+  // so every implicit step carries ~eps ||w|| / ||r|| of cancellation error:
+  // harmless at rtol 1e-9, but the Krylov relation is no longer accurate to
+  // the 1e-14 breakdown threshold (krylov.py:138, 198) -- a Krylov-exhaustion
+  // solve runs to maxiter instead of breaking down.  The default two-pass Gram
+  // variant keeps the pending correction second order (cpend = c').
   static const bool one_pass = [] {
     const char* e = std::getenv("SB_ORTHO");
-    return !(e && (std::strcmp(e, "gram2") == 0 || std::strcmp(e, "dcgs") == 0 || std::strcmp(e, "cgs2") == 0));
+    return e && std::strcmp(e, "gram1") == 0;
   }();
   std::vector<double> G((m + 1) * (m + 1), 0.0), tv(m + 1);
   double gam = 1.0;
