@@ -1764,15 +1764,26 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
   for (long long base = blockIdx.x * span; base < n2; base += (long long)gridDim.x * span) {
     double2 wv[CH], sv[CH], q[CH];
     bool ok[CH];
+    // the chunk [base, base + span) crosses at most one block boundary
+    // (span << bb): its two candidate means, chosen per element by one compare
+    long long bnd = 0;
+    double m_lo = 0.0, m_hi = 0.0;
+    int b_lo = 0;
+    if (MEANS) {
+      b_lo = (base >= bb) + (base >= 2 * bb) + (base >= 3 * bb);
+      bnd = (long long)(b_lo + 1) * bb;
+      m_lo = __ldg(means + b_lo);
+      m_hi = b_lo < 3 ? __ldg(means + b_lo + 1) : 0.0;
+    }
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
       const long long e = base + t * blockDim.x + threadIdx.x;
       ok[t] = e < n2;
       wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
       if (MEANS && ok[t]) {
-        const int bi = (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
-        double m = __ldg(means + bi);
+        double m = e < bnd ? m_lo : m_hi;
         if (gh) {
+          const int bi = e < bnd ? b_lo : b_lo + 1;
           const long long la = e - bi * bb;
           if (la < gh || la >= bb - gh) m = 0.0;
         }
