@@ -1764,12 +1764,14 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
   for (long long base = blockIdx.x * span; base < n2; base += (long long)gridDim.x * span) {
     double2 wv[CH], sv[CH], q[CH];
     bool ok[CH];
-    // the chunk [base, base + span) crosses at most one block boundary
-    // (span << bb): its two candidate means, chosen per element by one compare
+    // when the chunk [base, base + span) crosses at most one block boundary
+    // (span <= bb, every production size): its two candidate means, chosen per
+    // element by one compare; tiny vectors take the per-element block index
     long long bnd = 0;
     double m_lo = 0.0, m_hi = 0.0;
     int b_lo = 0;
-    if (MEANS) {
+    const bool chunked = span <= bb;
+    if (MEANS && chunked) {
       b_lo = (base >= bb) + (base >= 2 * bb) + (base >= 3 * bb);
       bnd = (long long)(b_lo + 1) * bb;
       m_lo = __ldg(means + b_lo);
@@ -1781,9 +1783,10 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
       ok[t] = e < n2;
       wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
       if (MEANS && ok[t]) {
-        double m = e < bnd ? m_lo : m_hi;
+        const int bf = chunked ? (e < bnd ? b_lo : b_lo + 1) : (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
+        double m = chunked ? (e < bnd ? m_lo : m_hi) : __ldg(means + bf);
         if (gh) {
-          const int bi = e < bnd ? b_lo : b_lo + 1;
+          const int bi = bf;
           const long long la = e - bi * bb;
           if (la < gh || la >= bb - gh) m = 0.0;
         }
