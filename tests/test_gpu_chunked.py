@@ -27,8 +27,8 @@ def test_chunked_sweeps_bit_identical(name, n, kind, monkeypatch):
         P = Preconditioner(cs, pc)
         y = P.apply(rs)
         x, h = gmres_solve(rs, cs, pc, gcfg, precond=P)
-        out[mb] = (P, y, x, h)  # P kept alive: its context must not return to the pool
-    (_, y0, x0, h0), (_, y1, x1, h1) = out["0"], out["0.4"]
+        out[mb] = (y, x, h)
+    (y0, x0, h0), (y1, x1, h1) = out["0"], out["0.4"]
     for a in range(3):
         assert np.array_equal(y0.u.components[a], y1.u.components[a]), a
         assert np.array_equal(x0.u.components[a], x1.u.components[a]), a
