@@ -2330,15 +2330,10 @@ static bool odd_periodic(const LevelDev& L, int dim) {
 
 template <int DIM, int FM, int A>
 static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0, int ext0 = 0, int p0 = -1, int p1 = -1) {
+                          int parity, double omega, int z = 0, int ext0 = 0) {
   Box b = face_box(L, DIM, A);
   b.lo[0] -= ext0;  // slab levels: also relax the ghost planes (sb_dist.inc dsweep_face)
   b.hi[0] += ext0;
-  if (p0 >= 0) {  // a range of axis-0 planes (chunked sweeps, sb_solver.cu sweep_face)
-    b.lo[0] = std::max(b.lo[0], p0);
-    b.hi[0] = std::min(b.hi[0], p1);
-    if (b.lo[0] > b.hi[0]) return;
-  }
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
@@ -2385,23 +2380,23 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
 }
 
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z, int ext0, int p0, int p1) {
+                        const double* rhsA, int parity, double omega, int z, int ext0) {
   ++g_kernel_launches;
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
   // the solver routes those levels through launch_face_colour_tmp below.
-  if (z == 0 && !L.dist0 && p0 < 0 && rowv_colour_supported(L, dim, form)) {
+  if (z == 0 && !L.dist0 && rowv_colour_supported(L, dim, form)) {
     launch_face_colour_rv(s, L, form, A, u, rhsA, parity, omega);
     return;
   }
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, p0, p1);
-      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, p0, p1);
-      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, p0, p1);
+      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
     } else {
-      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, p0, p1);
-      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, p0, p1);
+      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
     }
   });
 }
@@ -2423,15 +2418,10 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 
 template <int DIM>
 static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0, int ext0 = 0, int p0 = -1, int p1 = -1) {
+                          int parity, double omega, int z = 0, int ext0 = 0) {
   Box b = cell_box(L);
   b.lo[0] -= ext0;
   b.hi[0] += ext0;
-  if (p0 >= 0) {
-    b.lo[0] = std::max(b.lo[0], p0);
-    b.hi[0] = std::min(b.hi[0], p1);
-    if (b.lo[0] > b.hi[0]) return;
-  }
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
@@ -2460,10 +2450,10 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
 }
 
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z, int ext0, int p0, int p1) {
+                        int parity, double omega, int z, int ext0) {
   ++g_kernel_launches;
-  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z, ext0, p0, p1);
-  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z, ext0, p0, p1);
+  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
+  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
 }
 
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,

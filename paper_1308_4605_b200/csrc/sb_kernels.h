@@ -56,10 +56,9 @@ struct CoarseChain {
 // zero (replaces the zero fill; all-periodic pad-free levels only).
 // ext0: also relax ext0 ghost planes on each side of axis 0 (slab levels)
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z = 0, int ext0 = 0, int p0 = -1,
-                        int p1 = -1);
+                        const double* rhsA, int parity, double omega, int z = 0, int ext0 = 0);
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z = 0, int ext0 = 0, int p0 = -1, int p1 = -1);
+                        int parity, double omega, int z = 0, int ext0 = 0);
 // two-phase variants for levels with an odd periodic extent (same-colour
 // cells couple through the wrap): compute all, then update (reference order)
 void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,

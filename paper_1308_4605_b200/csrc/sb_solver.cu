@@ -66,7 +66,6 @@ struct Level {
   bool split_rr = false;                      // residual to memory, then restrict (large levels)
   double *fres[3]{}, *cres = nullptr;
   bool wave = false;                          // wavefront red-black sweeps (sb_wave.cu)
-  int chunk = 0;                              // chunked red/black ordering: planes per chunk (0 = off)
   int* wsteps[4]{};                           // step tables: face components 0..2, cells (3)
   int wnsteps[4]{};
   int* wctr = nullptr;                        // work counter + per-plane red counters
@@ -184,24 +183,6 @@ void make_level(sb_ctx* c, const int* n, double h) {
     return e ? std::atoi(e) : 0;
   }();
   L.wave = !L.fused && wave_min > 0 && n[0] >= wave_min && wave_supported(L.d, c->dim, c->form);
-  // Chunked red/black ordering (sweep_face / sweep_cell): each colour pass is
-  // cut into chunks of axis-0 planes whose operands (~SB_CHUNK_MB of face-row
-  // streams) fit the 126 MB L2 twice over, and the launches interleave
-  // R0 R1 B0 R2 B1 ... so a chunk's black pass re-reads what its red pass
-  // loaded one launch earlier from L2 instead of HBM.  Levels whose operands
-  // exceed the budget, axis 0 periodic, 3D, no other sweep scheme.
-  {
-    const double chunk_mb = [] {
-      const char* e = std::getenv("SB_CHUNK_MB");
-      return e ? std::atof(e) : 0.0;
-    }();
-    const double plane_mb = 5.0 * (double)L.P[1] * L.P[2] * 8.0 / 1e6;  // u_A, u_B, u_C, mu_c, rhs
-    const int planes = plane_mb > 0 ? (int)(chunk_mb / plane_mb) : 0;
-    L.chunk = (c->dim == 3 && chunk_mb > 0 && planes >= 2 && n[0] > 2 * planes && !L.two_phase && !L.fused &&
-               !L.wave && c->bc[0][0] == BC_PER)
-                  ? planes
-                  : 0;
-  }
   // split residual / restriction on levels with >= SB_RR_SPLIT cells (default
   // 64^3; 0 = always fused): full-occupancy residual kernel + light restriction
   const long long split_min = [] {
@@ -478,45 +459,6 @@ void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* cons
     }
     return;
   }
-  if (L.chunk > 0) {  // chunked red/black ordering (see make_level): R0 R1 B0 R2 B1 ... B_last, B(plane 0)
-    const int P = L.chunk, n0 = L.d.n[0], nch = (n0 + P - 1) / P;
-    for (int A = 3 - c->dim; A < 3; ++A) {
-      cudaEvent_t ea = nullptr;
-      if (c->profiling) {
-        ea = next_event(c);
-        CK(cudaEventRecord(ea, c->st));
-      }
-      const int zr = zs == 0 ? 0 : (zs == 2 ? 3 : 2), zb = zs == 0 ? 0 : 1;
-      Ptr3 u{{cur[0], cur[1], cur[2]}};
-      auto red = [&](int ch) {
-        launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], 0, omega, zr, 0, ch * P,
-                           std::min(n0, (ch + 1) * P) - 1);
-      };
-      // black of plane 0 needs red of plane n0-1 (periodic wrap): last
-      auto black = [&](int ch) {
-        launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], 1, omega, zb, 0, std::max(1, ch * P),
-                           std::min(n0, (ch + 1) * P) - 1);
-      };
-      red(0);
-      for (int ch = 0; ch < nch; ++ch) {
-        if (ch + 1 < nch) red(ch + 1);
-        black(ch);
-      }
-      launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], 1, omega, zb, 0, 0, 0);
-      if (c->profiling) {
-        cudaEvent_t eb = next_event(c);
-        CK(cudaEventRecord(eb, c->st));
-        double bytes = 2 * face_pass_bytes(c, L);
-        if (zs != 0) {
-          int nz = 0;
-          for (int B = 3 - c->dim; B < 3; ++B) nz += (B > A ? 2 : 0) + (B == A ? 1 : 0);
-          bytes -= (8.0 * nz - (zr == 3 ? 4.0 : 0.0)) * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
-        }
-        c->prof.push_back({ea, eb, 0, l == 0 && zs == 0, bytes});
-      }
-    }
-    return;
-  }
   const int per_launch = L.fused ? 2 : 1;
   for (int A = 3 - c->dim; A < 3; ++A) {
     for (int parity = 0; parity < 2; parity += per_launch) {
@@ -569,36 +511,6 @@ void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs,
       cudaEvent_t eb = next_event(c);
       CK(cudaEventRecord(eb, c->st));
       c->prof.push_back({ea, eb, 1, l == 0, 2 * cell_pass_bytes(c, L)});
-    }
-    return;
-  }
-  if (L.chunk > 0) {  // chunked red/black ordering, as sweep_face
-    const int P = L.chunk, n0 = L.d.n[0], nch = (n0 + P - 1) / P;
-    cudaEvent_t ea = nullptr;
-    if (c->profiling) {
-      ea = next_event(c);
-      CK(cudaEventRecord(ea, c->st));
-    }
-    const int zr = zs == 0 ? 0 : (zs == 2 ? 3 : 2);
-    auto red = [&](int ch) {
-      launch_cell_colour(c->st, L.d, c->dim, cur, rhs, 0, omega, zr, 0, ch * P, std::min(n0, (ch + 1) * P) - 1);
-    };
-    auto black = [&](int ch) {
-      launch_cell_colour(c->st, L.d, c->dim, cur, rhs, 1, omega, 0, 0, std::max(1, ch * P),
-                         std::min(n0, (ch + 1) * P) - 1);
-    };
-    red(0);
-    for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) red(ch + 1);
-      black(ch);
-    }
-    launch_cell_colour(c->st, L.d, c->dim, cur, rhs, 1, omega, 0, 0, 0, 0);
-    if (c->profiling) {
-      cudaEvent_t eb = next_event(c);
-      CK(cudaEventRecord(eb, c->st));
-      const double pts = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
-      const double bytes = 2 * cell_pass_bytes(c, L) - (zr == 0 ? 0.0 : (zr == 3 ? 4.0 : 8.0) * pts);
-      c->prof.push_back({ea, eb, 1, l == 0, bytes});
     }
     return;
   }
