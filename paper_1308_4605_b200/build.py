@@ -8,8 +8,7 @@ import subprocess
 import sys
 
 HERE = pathlib.Path(__file__).resolve().parent
-SRC = [HERE / "csrc" / "sb_kernels.cu", HERE / "csrc" / "sb_sweep.cu", HERE / "csrc" / "sb_wave.cu",
-       HERE / "csrc" / "sb_rowv.cu",
+SRC = [HERE / "csrc" / "sb_kernels.cu", HERE / "csrc" / "sb_rowv.cu",
        HERE / "csrc" / "sb_solver.cu"]
 OUT = HERE / "libstokesb200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

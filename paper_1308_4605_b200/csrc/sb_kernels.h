@@ -66,19 +66,6 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
                             double* tmp, int parity, double omega);
 bool level_needs_two_phase(const LevelDev& L, int dim);
-// fused two-colour sweeps, out of place (sb_sweep.cu); 3D, non-bulk, even periodic extents
-bool sweep2_supported(const LevelDev& L, int dim, int form);
-void launch_face_sweep2(cudaStream_t s, const LevelDev& L, int form, int A, CPtr3 u, double* unew,
-                        const double* rhsA, double omega);
-void launch_cell_sweep2(cudaStream_t s, const LevelDev& L, const double* phi, double* pnew, const double* rhs,
-                        double omega);
-// wavefront red-black sweeps, one launch per component (sb_wave.cu)
-bool wave_supported(const LevelDev& L, int dim, int form);
-std::vector<int> wave_steps(int np, bool per0, int lookahead);  // step order, 2*plane + colour
-void launch_face_wave(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u, const double* rhsA,
-                      double omega, const int* steps, int nsteps, int* ctr);
-void launch_cell_wave(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double omega,
-                      const int* steps, int nsteps, int* ctr);
 // row-vector kernels for large all-periodic 3D levels (sb_rowv.cu; the callers
 // are launch_face_colour / launch_face_res3 / launch_apply_M, which count the launch)
 bool rowv_supported(const LevelDev& L, int dim, int form);         // residual field, apply_M

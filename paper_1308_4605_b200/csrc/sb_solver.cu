@@ -62,14 +62,8 @@ struct Level {
   bool two_phase = false;
   double *mu_c = nullptr, *gam_c = nullptr, *mu_e[3]{}, *rho_f[3]{}, *beta_f[3]{};
   double *fx[3]{}, *frhs[3]{}, *cx = nullptr, *crhs = nullptr, *tmp = nullptr;
-  bool fused = false;                         // two-colour streaming sweeps (sb_sweep.cu)
   bool split_rr = false;                      // residual to memory, then restrict (large levels)
   double *fres[3]{}, *cres = nullptr;
-  bool wave = false;                          // wavefront red-black sweeps (sb_wave.cu)
-  int* wsteps[4]{};                           // step tables: face components 0..2, cells (3)
-  int wnsteps[4]{};
-  int* wctr = nullptr;                        // work counter + per-plane red counters
-  double *fxa[3]{}, *cxa = nullptr;           // ping-pong partners of the iterate
 };
 
 struct ProfEv {
@@ -168,21 +162,6 @@ void make_level(sb_ctx* c, const int* n, double h) {
   L.d.inv_h2 = 1.0 / (h * h);
   L.d.theta = 0.0;
   L.two_phase = level_needs_two_phase(L.d, c->dim);
-  // streaming two-colour sweeps: opt-in (SB_FUSED_SWEEPS=1) until they beat
-  // the per-colour kernels
-  static const bool fused_on = [] {
-    const char* e = std::getenv("SB_FUSED_SWEEPS");
-    return e && e[0] == '1';
-  }();
-  L.fused = fused_on && !L.two_phase && sweep2_supported(L.d, c->dim, c->form);
-  // wavefront sweeps (sb_wave.cu) on levels with >= SB_WAVE_MIN planes; opt-in
-  // (default 0 = off): they halve the sweep's HBM traffic but measured no
-  // faster than the per-colour passes
-  const int wave_min = [] {  // read per context: tests compare both paths in one process
-    const char* e = std::getenv("SB_WAVE_MIN");
-    return e ? std::atoi(e) : 0;
-  }();
-  L.wave = !L.fused && wave_min > 0 && n[0] >= wave_min && wave_supported(L.d, c->dim, c->form);
   // split residual / restriction on levels with >= SB_RR_SPLIT cells (default
   // 64^3; 0 = always fused): full-occupancy residual kernel + light restriction
   const long long split_min = [] {
@@ -222,25 +201,6 @@ void alloc_level(sb_ctx* c, Level& L, bool first) {
   if (L.split_rr) {
     for (int a = 3 - c->dim; a < 3; ++a) L.fres[a] = dalloc(c, B);
     L.cres = dalloc(c, B);
-  }
-  if (L.wave) {
-    const char* ek = std::getenv("SB_WAVE_K");  // red lookahead in planes
-    const int K = std::max(1, ek ? std::atoi(ek) : 8);
-    for (int k = 0; k < 4; ++k) {
-      const bool wallA = k < 3 && k >= 3 - c->dim && L.d.bclo[k] != BC_PER;
-      const int np = L.d.n[0] - (k == 0 && wallA ? 1 : 0);
-      const std::vector<int> st = wave_steps(np, L.d.bclo[0] == BC_PER, K);
-      L.wsteps[k] = reinterpret_cast<int*>(dalloc(c, ((long long)st.size() + 1) / 2));
-      // same stream as dalloc's zero fill, then wait: the host vector dies here
-      CK(cudaMemcpyAsync(L.wsteps[k], st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      L.wnsteps[k] = (int)st.size();
-    }
-    L.wctr = reinterpret_cast<int*>(dalloc(c, (L.d.n[0] + 2) / 2 + 1));
-  }
-  if (L.fused) {
-    for (int a = 3 - c->dim; a < 3; ++a) L.fxa[a] = dalloc(c, B);
-    L.cxa = dalloc(c, B);
   }
   L.d.mu_c = L.mu_c;
   L.d.gam_c = L.gam_c;
@@ -435,58 +395,33 @@ double cell_pass_bytes(const sb_ctx* c, const Level& L) {
 
 // ---- multigrid ---------------------------------------------------------------
 
-// One smoother sweep on level l.  cur[] holds the iterate; fused levels
-// sweep out of place into alt[] and swap the pointers (ping-pong).
+// One smoother sweep on level l, in place on cur[].
 // zs (first sweep of a V-cycle level, x = 0 on entry): 0 plain, 1 the level
 // was zero-filled, 2 the level was not (zero_fill_free: the first colour pass
 // stores both colours).  Only the per-colour kernels take the zero variants.
-void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* const* rhs, double omega, int zs = 0) {
+void sweep_face(sb_ctx* c, int l, double** cur, const double* const* rhs, double omega, int zs = 0) {
   Level& L = c->lv[l];
-  if (L.wave) {
-    for (int A = 3 - c->dim; A < 3; ++A) {
-      cudaEvent_t ea = nullptr;
-      if (c->profiling) {
-        ea = next_event(c);
-        CK(cudaEventRecord(ea, c->st));
-      }
-      Ptr3 u{{cur[0], cur[1], cur[2]}};
-      launch_face_wave(c->st, L.d, c->form, A, u, rhs[A], omega, L.wsteps[A], L.wnsteps[A], L.wctr);
-      if (c->profiling) {
-        cudaEvent_t eb = next_event(c);
-        CK(cudaEventRecord(eb, c->st));
-        c->prof.push_back({ea, eb, 0, l == 0, 2 * face_pass_bytes(c, L)});
-      }
-    }
-    return;
-  }
-  const int per_launch = L.fused ? 2 : 1;
   for (int A = 3 - c->dim; A < 3; ++A) {
-    for (int parity = 0; parity < 2; parity += per_launch) {
+    for (int parity = 0; parity < 2; ++parity) {
       cudaEvent_t ea = nullptr;
       if (c->profiling) {
         ea = next_event(c);
         CK(cudaEventRecord(ea, c->st));
       }
       int z = 0;
-      if (L.fused) {
-        CPtr3 u{{cur[0], cur[1], cur[2]}};
-        launch_face_sweep2(c->st, L.d, c->form, A, u, alt[A], rhs[A], omega);
-        std::swap(cur[A], alt[A]);
+      Ptr3 u{{cur[0], cur[1], cur[2]}};
+      if (L.two_phase) {
+        launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
       } else {
-        Ptr3 u{{cur[0], cur[1], cur[2]}};
-        if (L.two_phase) {
-          launch_face_colour_tmp(c->st, L.d, c->dim, c->form, A, u, rhs[A], L.tmp, parity, omega);
-        } else {
-          z = zs == 0 ? 0 : (parity == 0 ? (zs == 2 ? 3 : 2) : 1);
-          launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega, z);
-        }
+        z = zs == 0 ? 0 : (parity == 0 ? (zs == 2 ? 3 : 2) : 1);
+        launch_face_colour(c->st, L.d, c->dim, c->form, A, u, rhs[A], parity, omega, z);
       }
       if (c->profiling) {
         cudaEvent_t eb = next_event(c);
         CK(cudaEventRecord(eb, c->st));
         // zero-aware passes: 8 B less per skipped component, the partner store
         // of z = 3 adds 4 B; the roofline (fine) average takes plain passes only
-        double bytes = per_launch * face_pass_bytes(c, L);
+        double bytes = face_pass_bytes(c, L);
         if (z != 0) {
           int nz = 0;
           for (int B = 3 - c->dim; B < 3; ++B) nz += (B > A || (B == A && z >= 2)) ? 1 : 0;
@@ -498,34 +433,16 @@ void sweep_face(sb_ctx* c, int l, double** cur, double** alt, const double* cons
   }
 }
 
-void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs, double omega, int zs = 0) {
+void sweep_cell(sb_ctx* c, int l, double*& cur, const double* rhs, double omega, int zs = 0) {
   Level& L = c->lv[l];
-  if (L.wave) {
-    cudaEvent_t ea = nullptr;
-    if (c->profiling) {
-      ea = next_event(c);
-      CK(cudaEventRecord(ea, c->st));
-    }
-    launch_cell_wave(c->st, L.d, cur, rhs, omega, L.wsteps[3], L.wnsteps[3], L.wctr);
-    if (c->profiling) {
-      cudaEvent_t eb = next_event(c);
-      CK(cudaEventRecord(eb, c->st));
-      c->prof.push_back({ea, eb, 1, l == 0, 2 * cell_pass_bytes(c, L)});
-    }
-    return;
-  }
-  const int per_launch = L.fused ? 2 : 1;
-  for (int parity = 0; parity < 2; parity += per_launch) {
+  for (int parity = 0; parity < 2; ++parity) {
     cudaEvent_t ea = nullptr;
     if (c->profiling) {
       ea = next_event(c);
       CK(cudaEventRecord(ea, c->st));
     }
     int z = 0;
-    if (L.fused) {
-      launch_cell_sweep2(c->st, L.d, cur, alt, rhs, omega);
-      std::swap(cur, alt);
-    } else if (L.two_phase) {
+    if (L.two_phase) {
       launch_cell_colour_tmp(c->st, L.d, c->dim, cur, rhs, L.tmp, parity, omega);
     } else {
       z = (zs == 0 || parity == 1) ? 0 : (zs == 2 ? 3 : 2);
@@ -535,7 +452,7 @@ void sweep_cell(sb_ctx* c, int l, double*& cur, double*& alt, const double* rhs,
       cudaEvent_t eb = next_event(c);
       CK(cudaEventRecord(eb, c->st));
       const double pts = (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
-      const double bytes = per_launch * cell_pass_bytes(c, L) - (z == 0 ? 0.0 : (z == 3 ? 4.0 : 8.0) * pts);
+      const double bytes = cell_pass_bytes(c, L) - (z == 0 ? 0.0 : (z == 3 ? 4.0 : 8.0) * pts);
       c->prof.push_back({ea, eb, 1, l == 0, bytes});
     }
   }
@@ -594,7 +511,7 @@ bool coarse_tail(sb_ctx* c, int l, int kind, const double* const* rhs, double* c
 }
 
 // How the first sweep of a V-cycle level treats its x = 0 start: 0 plain
-// passes after the zero fill (streaming / wavefront / row-vector / two-phase
+// passes after the zero fill (row-vector / two-phase
 // levels, SB_ZERO_FIRST=0), 1 zero-aware passes after the zero fill, 2
 // zero-aware passes without it -- all-periodic levels whose block has no pads
 // or ghosts, where the first colour pass stores every entry (bulk-form face
@@ -604,7 +521,7 @@ static bool zero_first_on() {  // read per call: tests compare both paths in one
   return !(e && e[0] == '0');
 }
 int first_sweep_mode(sb_ctx* c, const Level& L, int kind) {
-  if (!zero_first_on() || L.fused || L.wave || L.two_phase) return 0;
+  if (!zero_first_on() || L.two_phase) return 0;
   if (kind == SB_KIND_FACE && rowv_colour_supported(L.d, c->dim, c->form)) return 0;
   bool pa = L.d.dist0 == 0 && (L.d.n[2] % 4) == 0;
   for (int a = 3 - c->dim; a < 3; ++a) pa = pa && c->bc[a][0] == BC_PER && L.P[a] == L.d.n[a];
@@ -616,15 +533,14 @@ void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, c
   if (coarse_tail(c, l, SB_KIND_FACE, rhs, x, sm)) return;
   Level& L = c->lv[l];
   double* cur[3] = {x[0], x[1], x[2]};
-  double* alt[3] = {L.fxa[0], L.fxa[1], L.fxa[2]};
   const int zs = first_sweep_mode(c, L, SB_KIND_FACE);
   if (zs != 2)
     for (int A = 3 - c->dim; A < 3; ++A) CK(cudaMemsetAsync(cur[A], 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_face(c, l, cur, rhs, sm.omega, s == 0 ? zs : 0);
   } else {
-    for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_face(c, l, cur, rhs, sm.omega, s == 0 ? zs : 0);
     Level& Lc = c->lv[l + 1];
     CPtr3 xc{{cur[0], cur[1], cur[2]}};
     if (L.split_rr) {
@@ -639,10 +555,8 @@ void vcycle_face(sb_ctx* c, int l, const double* const* rhs, double* const* x, c
     vcycle_face(c, l + 1, Lc.frhs, Lc.fx, sm);
     for (int A = 3 - c->dim; A < 3; ++A)
       launch_face_prolong_add(c->st, L.d, Lc.d, c->dim, A, Lc.fx[A], cur[A]);
-    for (int s = 0; s < sm.sweeps_up; ++s) sweep_face(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.sweeps_up; ++s) sweep_face(c, l, cur, rhs, sm.omega);
   }
-  for (int A = 3 - c->dim; A < 3; ++A)  // odd sweep counts leave the iterate in the partner buffer
-    if (cur[A] != x[A]) CK(cudaMemcpyAsync(x[A], cur[A], L.block * 8, cudaMemcpyDeviceToDevice, c->st));
 }
 
 void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smoother& sm) {
@@ -653,14 +567,13 @@ void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smooth
   }
   Level& L = c->lv[l];
   double* cur = x;
-  double* alt = L.cxa;
   const int zs = first_sweep_mode(c, L, SB_KIND_CELL);
   if (zs != 2) CK(cudaMemsetAsync(cur, 0, L.block * 8, c->st));
   const int last = (int)c->lv.size() - 1;
   if (l == last) {
-    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
+    for (int s = 0; s < sm.bottom_sweeps; ++s) sweep_cell(c, l, cur, rhs, sm.omega, s == 0 ? zs : 0);
   } else {
-    for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega, s == 0 ? zs : 0);
+    for (int s = 0; s < sm.sweeps_down; ++s) sweep_cell(c, l, cur, rhs, sm.omega, s == 0 ? zs : 0);
     Level& Lc = c->lv[l + 1];
     if (L.split_rr) {
       launch_cell_res(c->st, L.d, c->dim, cur, rhs, L.cres);
@@ -670,9 +583,8 @@ void vcycle_cell(sb_ctx* c, int l, const double* rhs, double* x, const sb_smooth
     }
     vcycle_cell(c, l + 1, Lc.crhs, Lc.cx, sm);
     launch_cell_prolong_add(c->st, L.d, Lc.d, c->dim, Lc.cx, cur);
-    for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, cur, alt, rhs, sm.omega);
+    for (int s = 0; s < sm.sweeps_up; ++s) sweep_cell(c, l, cur, rhs, sm.omega);
   }
-  if (cur != x) CK(cudaMemcpyAsync(x, cur, L.block * 8, cudaMemcpyDeviceToDevice, c->st));
 }
 
 // multigrid.py:442-460 on level-0 device buffers
@@ -1920,17 +1832,14 @@ int sb_smooth(sb_ctx* c, int kind, int level, double omega, double* const* x, co
         copy_in(c, L, A, x[r], bx[A]);
         copy_in(c, L, A, rhs[r], br[A]);
       }
-      Level& Lw = c->lv[level];
       double* cur[3] = {bx[0], bx[1], bx[2]};
-      double* alt[3] = {Lw.fxa[0], Lw.fxa[1], Lw.fxa[2]};
-      sweep_face(c, level, cur, alt, br, omega);
+      sweep_face(c, level, cur, br, omega);
       for (int r = 0; r < c->dim; ++r) copy_out(c, L, r + c->off, cur[r + c->off], x[r]);
     } else {
       copy_in(c, L, -1, x[0], bx[0]);
       copy_in(c, L, -1, rhs[0], br[0]);
       double* cur = bx[0];
-      double* alt = c->lv[level].cxa;
-      sweep_cell(c, level, cur, alt, br[0], omega);
+      sweep_cell(c, level, cur, br[0], omega);
       copy_out(c, L, -1, cur, x[0]);
     }
     sync(c);

@@ -248,10 +248,10 @@ def test_full_size_c3_properties():
                                       ((24, 16, 16), "pp nn ff"), ((16, 32, 40), "fn nf nn"),
                                       ((40, 16, 48), "pp pp nn")])
 @pytest.mark.parametrize("form,theta", [("stress", 0.0), ("stress", 0.9), ("laplacian", 0.3)])
-def test_fused_two_colour_sweeps_vs_oracle(cells, bc, form, theta):
-    """Streaming two-colour sweep kernels (sb_sweep.cu, tile 16x32 marching axis 0,
-    tiles/chunks straddling periodic wraps and walls) == the reference's
-    sequential red-then-black passes, all components, face and cell."""
+def test_colour_sweeps_vs_oracle(cells, bc, form, theta):
+    """One smoother sweep (the per-colour passes) on grids mixing periodic,
+    no-slip and free-slip axes == the reference's sequential red-then-black
+    passes, all components, face and cell."""
     from oracle import stokes_oracle as O
     from paper_1308_4605_b200 import multigrid as MG
     from paper_1308_4605_b200.grid import BoundaryCondition, CellField, FaceField, GridSpec
