@@ -41,6 +41,9 @@ constexpr int RT = 256;  // threads per CTA
 #ifndef RV_MINB
 #define RV_MINB 3
 #endif
+#ifndef RM_MINB
+#define RM_MINB 2
+#endif
 
 // ---- compile-time operand masks -------------------------------------------
 // A stencil operand at offset (o0, o1, o2) from the thread's face lives in
@@ -511,6 +514,260 @@ k_face_all_rv(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
   }
 }
 
+// ---- row-march: all faces, a warp walks one whole row ----------------------
+// k_face_all_rv is latency / instruction bound (ncu, C5 256^3: 600 instructions
+// per warp of 32 points, issue 56-65 %, DRAM 28-38 %): two thirds of its
+// instructions are address arithmetic, the segment-end loads and selects of
+// every +-1 operand, and stress terms evaluated twice (each edge flux by both
+// faces that share it).  Here a warp owns a whole row (i, j) and walks it in
+// 32-face segments:
+//  * the -1 neighbours along the row come from the neighbouring lane, lane 0's
+//    from lane 31 of the previous segment (carried in registers): no
+//    segment-end loads, the row end is read once before the walk (periodic
+//    wrap);
+//  * every edge stress T_AB = mu_e (d_B u_A + d_A u_B) and normal stress
+//    N_A = mu_c d_A u_A is evaluated ONCE per point at the point's own
+//    (lower) edge / cell and shared by the two rows (A and B) that use it;
+//    the +1 values along axes 0 / 1 are evaluated from the neighbouring rows'
+//    operands, the +1 values along the row are the next lane's (one rotate
+//    shuffle; lane 31 finishes its face one segment later, the last segment
+//    with the first segment's lane-0 values);
+//  * derived edge viscosities as sums of cell pairs shared between edges,
+//    the factor 1/4 folded into the h^-2 scale (exact: powers of two), fused
+//    multiply-adds on the final combinations.
+// 79 fp64 operations and ~220 instructions per point instead of 165 / 600.
+// Same formulas as face_row_t with a different rounding order (and FMAs):
+// equal to the per-face kernels to ~1e-15 relative, not bit-identical
+// (tests/test_gpu_rowv.py).  Derived edge viscosities only (mue_derived levels).
+__device__ __forceinline__ double rot_m(double v, double& prev, int lane) {
+  const double s = lane == 31 ? prev : v;
+  prev = v;
+  return __shfl_sync(FULL, s, (lane + 31) & 31);
+}
+__device__ __forceinline__ double rot_p(double v, int lane) { return __shfl_sync(FULL, v, (lane + 1) & 31); }
+
+template <int FORM, bool MODE_M, bool THETA, bool DE, int TI, int TJ, int MINB>
+__global__ void __launch_bounds__(TI * TJ * 32, MINB)
+k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3 out, double* __restrict__ out_p) {
+  pdl_enter();
+  constexpr bool ST = FORM != F_LAP;
+  const int lane = threadIdx.x & 31;
+  // a CTA = TI x TJ warps on TJ consecutive rows of TI consecutive planes:
+  // the +-1 rows / planes of its warps are shared through L1
+  const int wid = threadIdx.x >> 5;
+  const int j = (int)blockIdx.x * TJ + wid % TJ, i = (int)blockIdx.y * TI + wid / TJ;
+  if (j >= L.n[1] || i >= L.n[0]) return;  // whole warps
+  const int n2 = L.n[2];
+  const int rowc = i * L.s0 + j * L.s1;
+  // a slab-distributed axis 0 reads its ghost planes instead of wrapping
+  const int im = ((i == 0 && !L.dist0) ? L.n[0] - 1 : -1) * L.s0;
+  const int ip = ((i == L.n[0] - 1 && !L.dist0) ? -(L.n[0] - 1) : 1) * L.s0;
+  const int jm = (j == 0 ? L.n[1] - 1 : -1) * L.s1;
+  const int jp = (j == L.n[1] - 1 ? -(L.n[1] - 1) : 1) * L.s1;
+  const double* __restrict__ u0 = x.p[0];
+  const double* __restrict__ u1 = x.p[1];
+  const double* __restrict__ u2 = x.p[2];
+  const double* __restrict__ mu = L.mu_c;
+  // stored edge viscosities (!DE): mu_e(A,B) lives in L.mu_e[3 - A - B]
+  const double* __restrict__ e01 = L.mu_e[2];
+  const double* __restrict__ e02 = L.mu_e[1];
+  const double* __restrict__ e12 = L.mu_e[0];
+  const double c1 = (ST ? 2.0 : 1.0) * L.inv_h2, c2 = (DE ? 0.25 : 1.0) * L.inv_h2;
+  // results are accumulated as sgn * (A u)_A [+ rhs | + G p]
+  const double sg = MODE_M ? 1.0 : -1.0;
+  const double k1 = -sg * c1, k2 = -sg * c2;
+
+  // carried -1 operands: lane 31's value of the previous segment; before the
+  // walk, the row's last element (periodic wrap)
+  double pv_u0c, pv_u0x, pv_u1c, pv_u1y, pv_u2c, pv_mc, pv_P0c = 0.0, pv_P0x = 0.0, pv_P1c = 0.0, pv_P1y = 0.0, pv_p = 0.0;
+  {
+    const int q = rowc + n2 - 1;
+    const double m00 = __ldg(mu + q);
+    double mm0 = 0.0, mp0 = 0.0, m0m = 0.0, m0p = 0.0;
+    if (DE) {
+      mm0 = __ldg(mu + q + im);
+      mp0 = __ldg(mu + q + ip);
+      m0m = __ldg(mu + q + jm);
+      m0p = __ldg(mu + q + jp);
+    }
+    pv_u0c = __ldg(u0 + q);
+    pv_u0x = __ldg(u0 + q + ip);
+    pv_u1c = __ldg(u1 + q);
+    pv_u1y = __ldg(u1 + q + jp);
+    pv_u2c = __ldg(u2 + q);
+    pv_mc = m00;
+    if (DE) {
+      pv_P0c = m00 + mm0;
+      pv_P0x = mp0 + m00;
+      pv_P1c = m00 + m0m;
+      pv_P1y = m0p + m00;
+    }
+    if (MODE_M) pv_p = __ldg(p + q);
+  }
+  double pe0 = 0.0, pe1 = 0.0, pe2 = 0.0, peD = 0.0, peU = 0.0;  // lane 31: unfinished face of the previous segment
+  double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;                  // lane 31: lane 0's +1 values of the first segment
+  const int nseg = n2 >> 5;
+#pragma unroll 1
+  for (int s = 0; s < nseg; ++s) {
+    const int q = rowc + (s << 5) + lane;
+    const double u0c = __ldg(u0 + q), u0im = __ldg(u0 + q + im), u0ip = __ldg(u0 + q + ip);
+    const double u0jm = __ldg(u0 + q + jm), u0jp = __ldg(u0 + q + jp), u0ipjm = __ldg(u0 + q + ip + jm);
+    const double u1c = __ldg(u1 + q), u1im = __ldg(u1 + q + im), u1ip = __ldg(u1 + q + ip);
+    const double u1jm = __ldg(u1 + q + jm), u1jp = __ldg(u1 + q + jp), u1imjp = __ldg(u1 + q + im + jp);
+    const double u2c = __ldg(u2 + q), u2im = __ldg(u2 + q + im), u2ip = __ldg(u2 + q + ip);
+    const double u2jm = __ldg(u2 + q + jm), u2jp = __ldg(u2 + q + jp);
+    const double mc = __ldg(mu + q), mim = __ldg(mu + q + im), mjm = __ldg(mu + q + jm);
+    double mip = 0.0, mjp = 0.0, mimjm = 0.0, mimjp = 0.0, mipjm = 0.0;
+    double S01, S01y, S01x, S02, S02x, S12, S12y;
+    if (DE) {
+      mip = __ldg(mu + q + ip);
+      mjp = __ldg(mu + q + jp);
+      mimjm = __ldg(mu + q + im + jm);
+      mimjp = __ldg(mu + q + im + jp);
+      mipjm = __ldg(mu + q + ip + jm);
+    } else {
+      S01 = __ldg(e01 + q);
+      S01y = __ldg(e01 + q + jp);
+      S01x = __ldg(e01 + q + ip);
+      S02 = __ldg(e02 + q);
+      S02x = __ldg(e02 + q + ip);
+      S12 = __ldg(e12 + q);
+      S12y = __ldg(e12 + q + jp);
+    }
+    double pc = 0.0, pim = 0.0, pjm = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    if (MODE_M) {
+      pc = __ldg(p + q);
+      pim = __ldg(p + q + im);
+      pjm = __ldg(p + q + jm);
+    } else {
+      r0 = __ldg(rhs.p[0] + q);
+      r1 = __ldg(rhs.p[1] + q);
+      r2 = __ldg(rhs.p[2] + q);
+    }
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    if (THETA) {
+      t0 = L.theta * __ldg(L.rho_f[0] + q);
+      t1 = L.theta * __ldg(L.rho_f[1] + q);
+      t2 = L.theta * __ldg(L.rho_f[2] + q);
+    }
+    // -1 neighbours along the row
+    const double u0c_m = rot_m(u0c, pv_u0c, lane), u1c_m = rot_m(u1c, pv_u1c, lane);
+    double u0x_m = 0.0, u1y_m = 0.0;
+    if (ST) {
+      u0x_m = rot_m(u0ip, pv_u0x, lane);
+      u1y_m = rot_m(u1jp, pv_u1y, lane);
+    }
+    const double u2c_m = rot_m(u2c, pv_u2c, lane), mc_m = rot_m(mc, pv_mc, lane);
+    if (DE) {
+      // cell pair sums (edge_mean's first stage: lower plane axis first), then
+      // 4 mu_e at the edges used (no suffix: own point, y: + e_1, x: + e_0)
+      const double P0c = mc + mim, P0x = mip + mc, P0jm = mjm + mimjm, P0jp = mjp + mimjp, P0xjm = mipjm + mjm;
+      const double P1c = mc + mjm, P1y = mjp + mc;
+      const double P0c_m = rot_m(P0c, pv_P0c, lane), P0x_m = rot_m(P0x, pv_P0x, lane);
+      const double P1c_m = rot_m(P1c, pv_P1c, lane), P1y_m = rot_m(P1y, pv_P1y, lane);
+      S01 = P0c + P0jm;
+      S01y = P0jp + P0c;
+      S01x = P0x + P0xjm;
+      S02 = P0c + P0c_m;
+      S02x = P0x + P0x_m;
+      S12 = P1c + P1c_m;
+      S12y = P1y + P1y_m;
+    }
+    // edge stresses T_AB: tA = the d_B u_A part (row A), tB = the d_A u_B part
+    // (row B); the stress forms share the full bracket
+    double T01a, T01b, T01y, T01x, T02a, T02b, T02x, T12a, T12b, T12y;
+    if (ST) {
+      T01a = T01b = S01 * ((u0c - u0jm) + (u1c - u1im));
+      T01y = S01y * ((u0jp - u0c) + (u1jp - u1imjp));
+      T01x = S01x * ((u0ip - u0ipjm) + (u1ip - u1c));
+      T02a = T02b = S02 * ((u0c - u0c_m) + (u2c - u2im));
+      T02x = S02x * ((u0ip - u0x_m) + (u2ip - u2c));
+      T12a = T12b = S12 * ((u1c - u1c_m) + (u2c - u2jm));
+      T12y = S12y * ((u1jp - u1y_m) + (u2jp - u2c));
+    } else {
+      T01a = S01 * (u0c - u0jm);
+      T01b = S01 * (u1c - u1im);
+      T01y = S01y * (u0jp - u0c);    // row 0
+      T01x = S01x * (u1ip - u1c);    // row 1
+      T02a = S02 * (u0c - u0c_m);
+      T02b = S02 * (u2c - u2im);
+      T02x = S02x * (u2ip - u2c);    // row 2
+      T12a = S12 * (u1c - u1c_m);
+      T12b = S12 * (u2c - u2jm);
+      T12y = S12y * (u2jp - u2c);    // row 2
+    }
+    // normal stresses at the cells x, x - e_A
+    const double N0 = mc * (u0ip - u0c), N0m = mim * (u0c - u0im);
+    const double N1 = mc * (u1jp - u1c), N1m = mjm * (u1c - u1jm);
+    const double N2m = mc_m * (u2c - u2c_m);
+    // everything but the +1 term along the row
+    double a0 = fma(k1, N0 - N0m, k2 * ((T01y - T01a) - T02a));
+    double a1 = fma(k1, N1 - N1m, k2 * ((T01x - T01b) - T12a));
+    double a2 = fma(-k1, N2m, k2 * ((T02x - T02b) + (T12y - T12b)));
+    if (THETA) {
+      a0 = fma(sg * t0, u0c, a0);
+      a1 = fma(sg * t1, u1c, a1);
+      a2 = fma(sg * t2, u2c, a2);
+    }
+    double d01 = 0.0;
+    if (MODE_M) {
+      const double pc_m = rot_m(pc, pv_p, lane);
+      a0 = fma(pc - pim, L.inv_h, a0);
+      a1 = fma(pc - pjm, L.inv_h, a1);
+      a2 = fma(pc - pc_m, L.inv_h, a2);
+      d01 = (u0ip - u0c) + (u1jp - u1c);  // div_sum order: (d0 + d1) + d2
+    } else {
+      a0 += r0;
+      a1 += r1;
+      a2 += r2;
+    }
+    // +1 values along the row: lanes 0..30 the next lane's (this segment),
+    // lane 31 lane 0's, which completes its face of the PREVIOUS segment
+    const double h0 = rot_p(T02a, lane), h1 = rot_p(T12a, lane), h2 = rot_p(N2m, lane);
+    const double h3 = MODE_M ? rot_p(u2c, lane) : 0.0;
+    const bool last = lane == 31;
+    double b0 = a0, b1 = a1, b2 = a2, bd = d01, bu = u2c;
+    if (s == 0) {
+      f0 = h0;
+      f1 = h1;
+      f2 = h2;
+      f3 = h3;
+    }
+    if (last) {
+      b0 = pe0;
+      b1 = pe1;
+      b2 = pe2;
+      bd = peD;
+      bu = peU;
+    }
+    pe0 = a0;
+    pe1 = a1;
+    pe2 = a2;
+    peD = d01;
+    peU = u2c;
+    const int qo = last ? q - 32 : q;
+    if (!last || s > 0) {
+      out.p[0][qo] = fma(k2, h0, b0);
+      out.p[1][qo] = fma(k2, h1, b1);
+      out.p[2][qo] = fma(k1, h2, b2);
+      if (MODE_M) out_p[qo] = -((bd + (h3 - bu)) * L.inv_h);
+    }
+  }
+  if (lane == 31) {  // the row's last face: +1 neighbours wrap to the first segment's lane 0
+    const int qo = rowc + n2 - 1;
+    out.p[0][qo] = fma(k2, f0, pe0);
+    out.p[1][qo] = fma(k2, f1, pe1);
+    out.p[2][qo] = fma(k1, f2, pe2);
+    if (MODE_M) out_p[qo] = -((peD + (f3 - peU)) * L.inv_h);
+  }
+}
+
+// SB_ROWM=0: the segment kernel (k_face_all_rv) on every row-vector level
+bool rowm_on() {
+  const char* e = std::getenv("SB_ROWM");
+  return !(e && e[0] == '0');
+}
+
 int blocks_for(const LevelDev& L, int seglen) {
   return L.n[0] * ((L.n[1] + 7) / 8) * (L.n[2] / seglen);
 }
@@ -571,6 +828,33 @@ static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 r
   const int nseg = L.n[2] / 32;
   const int nb = blocks_for(L, 32);
   const bool de = L.mue_derived != 0;
+  if (rowm_on()) {  // row-march kernel: a warp per row
+    const bool th = L.theta != 0.0;
+    // CTA tile: 1 plane x 4 rows, 4 CTAs per SM (128 registers).  Measured
+    // (ncu, C5 256^3, apply_M / residual): 1x8 warps x 2 CTAs 328 / 325 us,
+    // 1x4 x 4 322 / 319, 2x2 x 4 332 / 315, 2x4 x 2 339 / 322, 4x4 x 1 359 / 341;
+    // lane 31's carried values in shared memory (80-96 registers, 20-24 warps
+    // per SM) 307-352 us: the L1 data pipe (loads + shuffles) is the busiest
+    // unit at 62 %, more warps do not help
+#define SB_RM2(FM, TH, DD)                                                                                        \
+  launch_k(k_face_all_rm<FM, MODE_M, TH, DD, 1, 4, 4>, dim3((L.n[1] + 3) / 4, L.n[0], 1), dim3(128, 1, 1), 0, s, L, x, \
+           rhs, p, out, out_p)
+#define SB_RM1(FM, TH)       \
+  if (de) { SB_RM2(FM, TH, true); } \
+  else { SB_RM2(FM, TH, false); }
+#define SB_RM(FM)            \
+  if (th) { SB_RM1(FM, true) } \
+  else { SB_RM1(FM, false) }
+    if (form == F_LAP) {
+      SB_RM(F_LAP)
+    } else {
+      SB_RM(F_STRESS)
+    }
+#undef SB_RM
+#undef SB_RM1
+#undef SB_RM2
+    return;
+  }
   if (form == F_LAP) {
     if (de) launch_k(k_face_all_rv<F_LAP, true, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);
     else launch_k(k_face_all_rv<F_LAP, false, MODE_M, RV_MINB>, nb, RT, 0, s, L, x, rhs, p, out, out_p, nseg);

@@ -7,6 +7,13 @@ shuffle).  Same operands, same arithmetic order: the results must be
 bit-identical to the per-face kernels (SB_ROWV=0), with stored and with derived
 edge viscosities, for both viscous forms the kernels cover, at segment
 boundaries and periodic wraps (odd row counts, extents 64 and 128).
+
+On levels with derived edge viscosities the default is the row-march kernel
+(k_face_all_rm, SB_ROWM=1: a warp walks a whole row, every edge / normal stress
+evaluated once and shared by the two rows that use it, FMAs): the same formulas
+in a different rounding order, so it is compared to the per-face kernels at
+1e-13 of the field's magnitude (north_star asks 1e-8), and full solves by
+iteration count, r_P history and solution.
 """
 
 from __future__ import annotations
@@ -30,13 +37,14 @@ def _case(cells, form, derive, theta, monkeypatch):
     return case, cs, rs
 
 
-def _run(cells, form, derive, theta, rowv, monkeypatch):
+def _run(cells, form, derive, theta, rowv, monkeypatch, rowm="0"):
     from paper_1308_4605_b200 import multigrid as MG
     from paper_1308_4605_b200 import operators as OPS
     from paper_1308_4605_b200.grid import FaceField
     case, cs, rs = _case(cells, form, derive, theta, monkeypatch)
     g = case.grid
     monkeypatch.setenv("SB_ROWV", "1" if rowv else "0")
+    monkeypatch.setenv("SB_ROWM", rowm)
     monkeypatch.setenv("SB_ROWV_COLOUR", "1" if rowv else "0")  # opt-in colour pass
     ctx = OPS.DeviceContext(g, cs.viscous_form)
     ctx.set_coefficients(cs)
@@ -55,6 +63,7 @@ def _run(cells, form, derive, theta, rowv, monkeypatch):
         out["rr"] = [c.copy() for c in rr.components]
     ctx.close()
     monkeypatch.delenv("SB_ROWV")
+    monkeypatch.delenv("SB_ROWM")
     monkeypatch.delenv("SB_ROWV_COLOUR")
     return out
 
@@ -71,9 +80,50 @@ def test_rowv_bit_identical(cells, form, derive, theta, monkeypatch):
             assert np.array_equal(u, v), k
 
 
+@pytest.mark.parametrize("cells", GRIDS + [(8, 8, 256)], ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("form,theta", [("stress", 0.0), ("laplacian", 0.0), ("stress", 3.5), ("laplacian", 0.25)])
+def test_row_march_matches_per_face(cells, form, theta, monkeypatch):
+    a = _run(cells, form, True, theta, True, monkeypatch, rowm="1")
+    b = _run(cells, form, True, theta, False, monkeypatch)
+    assert a.keys() == b.keys()
+    for k in a:
+        for u, v in zip(a[k], b[k]):
+            assert np.max(np.abs(u - v)) <= 1e-13 * np.max(np.abs(v)), k
+    # the colour passes do not use the all-face kernels
+    for k in ("sm1.0", "sm0.8"):
+        for u, v in zip(a[k], b[k]):
+            assert np.array_equal(u, v), k
+
+
+def test_row_march_gmres_matches_per_face(monkeypatch):
+    """C5-recipe solve at 64^3 with the row-march apply_M / residual field
+    against the per-face kernels: same iteration count, r_P history to 1e-6,
+    solution to 1e-8 (north_star's tolerances)."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import pack_stokes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
+    from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
+    case = PR.make_case("C5", 64)
+    cs, rs, spec = PR.prepare(case)
+    res = {}
+    for rowv in ("1", "0"):
+        monkeypatch.setenv("SB_ROWV", rowv)
+        monkeypatch.setenv("SB_ROWM", "1")
+        P = Preconditioner(cs, PrecondConfig(kind=P1))
+        P.set_graphs(False)  # drop a graph captured under the other setting
+        P.set_graphs(True)
+        x, h = gmres_solve(rs, cs, None, GmresConfig(restart=50, rtol=1e-9), precond=P)
+        res[rowv] = (pack_stokes(x), h.iterations, np.array([r.resid_precond for r in h.entries]))
+        del P
+    assert res["1"][1] == res["0"][1]
+    assert np.allclose(res["1"][2], res["0"][2], rtol=1e-6)
+    assert np.linalg.norm(res["1"][0] - res["0"][0]) <= 1e-8 * np.linalg.norm(res["0"][0])
+
+
 def test_rowv_gmres_matches_per_face(monkeypatch):
     """Full C5-recipe solves at 64^3 (P^-1 graph captured per context): identical
     iteration counts and solutions to the bit."""
+    monkeypatch.setenv("SB_ROWM", "0")
     from paper_1308_4605_b200 import problems as PR
     from paper_1308_4605_b200.grid import pack_stokes
     from paper_1308_4605_b200.krylov import GmresConfig, gmres_solve
