@@ -546,7 +546,7 @@ __device__ __forceinline__ double rot_m(double v, double& prev, int lane) {
 }
 __device__ __forceinline__ double rot_p(double v, int lane) { return __shfl_sync(FULL, v, (lane + 1) & 31); }
 
-template <int FORM, bool MODE_M, bool THETA, bool DE, int TI, int TJ, int MINB>
+template <int FORM, bool MODE_M, bool THETA, bool DE, bool W2, int TI, int TJ, int MINB>
 __global__ void __launch_bounds__(TI * TJ * 32, MINB)
 k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3 out, double* __restrict__ out_p) {
   pdl_enter();
@@ -578,10 +578,14 @@ k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
   const double k1 = -sg * c1, k2 = -sg * c2;
 
   // carried -1 operands: lane 31's value of the previous segment; before the
-  // walk, the row's last element (periodic wrap)
+  // walk, the row's last element (periodic wrap) or, W2 (walls at both ends
+  // of the row), the ghost values behind the low wall: -u (no-slip: the wall
+  // flux mu_e 2 u / h, operators.py:267-300) or +u (free-slip: no flux) for the
+  // tangential components, the boundary cell's mu (two-cell boundary mean)
   double pv_u0c, pv_u0x, pv_u1c, pv_u1y, pv_u2c, pv_mc, pv_P0c = 0.0, pv_P0x = 0.0, pv_P1c = 0.0, pv_P1y = 0.0, pv_p = 0.0;
   {
-    const int q = rowc + n2 - 1;
+    const int q = W2 ? rowc : rowc + n2 - 1;
+    const double gl = W2 ? (L.bclo[2] == BC_FREESLIP ? 1.0 : -1.0) : 1.0;
     const double m00 = __ldg(mu + q);
     double mm0 = 0.0, mp0 = 0.0, m0m = 0.0, m0p = 0.0;
     if (DE) {
@@ -590,11 +594,11 @@ k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
       m0m = __ldg(mu + q + jm);
       m0p = __ldg(mu + q + jp);
     }
-    pv_u0c = __ldg(u0 + q);
-    pv_u0x = __ldg(u0 + q + ip);
-    pv_u1c = __ldg(u1 + q);
-    pv_u1y = __ldg(u1 + q + jp);
-    pv_u2c = __ldg(u2 + q);
+    pv_u0c = gl * __ldg(u0 + q);
+    pv_u0x = gl * __ldg(u0 + q + ip);
+    pv_u1c = gl * __ldg(u1 + q);
+    pv_u1y = gl * __ldg(u1 + q + jp);
+    pv_u2c = W2 ? 0.0 : __ldg(u2 + q);  // W2: face 0 of component 2 is a wall face (its row is not formed)
     pv_mc = m00;
     if (DE) {
       pv_P0c = m00 + mm0;
@@ -749,12 +753,25 @@ k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
     if (!last || s > 0) {
       out.p[0][qo] = fma(k2, h0, b0);
       out.p[1][qo] = fma(k2, h1, b1);
-      out.p[2][qo] = fma(k1, h2, b2);
+      if (!(W2 && s == 0 && lane == 0)) out.p[2][qo] = fma(k1, h2, b2);
+      else if (MODE_M) out.p[2][qo] = 0.0;  // wall face (k_apply_M's m_face); the residual field leaves it
       if (MODE_M) out_p[qo] = -((bd + (h3 - bu)) * L.inv_h);
     }
   }
   if (lane == 31) {  // the row's last face: +1 neighbours wrap to the first segment's lane 0
     const int qo = rowc + n2 - 1;
+    if (W2) {
+      // ... or sit on the high wall: edge stresses from the ghost values (-u /
+      // +u), the normal stress of the last cell against the wall face u_2 = 0
+      const double gh = (L.bchi[2] == BC_FREESLIP ? 1.0 : -1.0) - 1.0;
+      const double s02 = DE ? 2.0 * pv_P0c : __ldg(e02 + qo + 1);
+      const double s12 = DE ? 2.0 * pv_P1c : __ldg(e12 + qo + 1);
+      f0 = s02 * (gh * pv_u0c);
+      f1 = s12 * (gh * pv_u1c);
+      f2 = pv_mc * (0.0 - pv_u2c);
+      f3 = 0.0;
+      if (MODE_M) out.p[2][qo + 1] = 0.0;  // the high wall face
+    }
     out.p[0][qo] = fma(k2, f0, pe0);
     out.p[1][qo] = fma(k2, f1, pe1);
     out.p[2][qo] = fma(k1, f2, pe2);
@@ -801,12 +818,14 @@ bool rowv_colour_on() {
 bool rowv_supported(const LevelDev& L, int dim, int form) {
   if (dim != 3 || form == F_BULK || !rowv_on()) return false;
   for (int a = 0; a < 3; ++a)
-    if (L.bclo[a] != BC_PER || L.n[a] < 2) return false;
-  return L.n[2] % 64 == 0;
+    if (L.n[a] < 2) return false;
+  if (L.bclo[0] != BC_PER || L.bclo[1] != BC_PER || L.n[2] % 64 != 0) return false;
+  // walls along the contiguous axis (C4's z walls): the row-march kernel only
+  return L.bclo[2] == BC_PER || rowm_on();
 }
 
 bool rowv_colour_supported(const LevelDev& L, int dim, int form) {
-  return rowv_colour_on() && rowv_supported(L, dim, form);
+  return rowv_colour_on() && L.bclo[2] == BC_PER && rowv_supported(L, dim, form);
 }
 
 void launch_face_colour_rv(cudaStream_t s, const LevelDev& L, int form, int A, Ptr3 u, const double* rhsA,
@@ -828,7 +847,8 @@ static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 r
   const int nseg = L.n[2] / 32;
   const int nb = blocks_for(L, 32);
   const bool de = L.mue_derived != 0;
-  if (rowm_on()) {  // row-march kernel: a warp per row
+  const bool w2 = L.bclo[2] != BC_PER;
+  if (rowm_on() || w2) {  // row-march kernel: a warp per row
     const bool th = L.theta != 0.0;
     // CTA tile: 1 plane x 4 rows, 4 CTAs per SM (128 registers).  Measured
     // (ncu, C5 256^3, apply_M / residual): 1x8 warps x 2 CTAs 328 / 325 us,
@@ -837,8 +857,10 @@ static void all_rv(cudaStream_t s, const LevelDev& L, int form, CPtr3 x, CPtr3 r
     // per SM) 307-352 us: the L1 data pipe (loads + shuffles) is the busiest
     // unit at 62 %, more warps do not help
 #define SB_RM2(FM, TH, DD)                                                                                        \
-  launch_k(k_face_all_rm<FM, MODE_M, TH, DD, 1, 4, 4>, dim3((L.n[1] + 3) / 4, L.n[0], 1), dim3(128, 1, 1), 0, s, L, x, \
-           rhs, p, out, out_p)
+  if (w2) launch_k(k_face_all_rm<FM, MODE_M, TH, DD, true, 1, 4, 4>, dim3((L.n[1] + 3) / 4, L.n[0], 1), dim3(128, 1, 1), 0, \
+                   s, L, x, rhs, p, out, out_p);                                                                  \
+  else launch_k(k_face_all_rm<FM, MODE_M, TH, DD, false, 1, 4, 4>, dim3((L.n[1] + 3) / 4, L.n[0], 1), dim3(128, 1, 1), 0, \
+                s, L, x, rhs, p, out, out_p)
 #define SB_RM1(FM, TH)       \
   if (de) { SB_RM2(FM, TH, true); } \
   else { SB_RM2(FM, TH, false); }

@@ -143,3 +143,74 @@ def test_rowv_gmres_matches_per_face(monkeypatch):
     assert res["1"][1] == res["0"][1]
     assert res["1"][2] == res["0"][2]
     assert np.array_equal(res["1"][0], res["0"][0])
+
+
+# ---- walls along the contiguous axis (C4's z walls) --------------------------
+
+WALL_GRIDS = [(64, 64, 64), (6, 10, 128), (4, 6, 64)]
+
+
+def _wall_case(cells, form, theta, bc2):
+    """Seeded variable rho / mu on a box periodic in x, y with walls in z."""
+    from paper_1308_4605_b200 import grid as G
+    from paper_1308_4605_b200.grid import CellField, FaceField, StokesVector
+    from paper_1308_4605_b200.operators import ViscousForm, make_coefficients, rescale
+    kinds = {"n": G.NO_SLIP, "f": G.FREE_SLIP}
+    g = G.GridSpec(cells, 1.0 / cells[2], ((G.PERIODIC, G.PERIODIC), (G.PERIODIC, G.PERIODIC),
+                                           (kinds[bc2[0]], kinds[bc2[1]])))
+    rng = np.random.default_rng(11)
+    rho = CellField(g, 1.0 + 99.0 * rng.random(g.cells))
+    mu = CellField(g, 10.0 ** (3.0 * rng.random(g.cells)))
+    cs = make_coefficients(g, theta, rho, mu, viscous_form=ViscousForm(form))
+    f = FaceField(g, tuple(rng.standard_normal(g.face_shape(a)) for a in range(3)))
+    # wall-normal boundary faces carry no unknown
+    f.components[2][..., 0] = 0.0
+    f.components[2][..., -1] = 0.0
+    rs = StokesVector(f, CellField(g, rng.standard_normal(g.cells)))
+    cs, rs, _ = rescale(cs, rs)
+    return g, cs, rs
+
+
+def _wall_run(cells, form, theta, bc2, derive, rowv, monkeypatch):
+    from paper_1308_4605_b200 import multigrid as MG
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200.grid import FaceField
+    g, cs, rs = _wall_case(cells, form, theta, bc2)
+    monkeypatch.setenv("SB_ROWV", "1" if rowv else "0")
+    monkeypatch.setenv("SB_MUE_DERIVED", "2" if derive else "0")
+    ctx = OPS.DeviceContext(g, cs.viscous_form)
+    ctx.set_coefficients(cs)
+    assert ctx.mue_derived(0) == derive
+    hier = MG.MgHierarchy(ctx, cs)
+    out = {}
+    m = OPS.apply_M(rs, cs, ctx=ctx)
+    out["Mu"] = [c.copy() for c in m.u.components] + [m.p.data.copy()]
+    rng = np.random.default_rng(5)
+    x = FaceField(g, tuple(rng.standard_normal(g.face_shape(a)) for a in range(3)))
+    x.components[2][..., 0] = 0.0
+    x.components[2][..., -1] = 0.0
+    if all(c % 2 == 0 and c >= 4 for c in cells):
+        rr = MG.residual_restrict(hier, 0, "face", x, rs.u)
+        out["rr"] = [c.copy() for c in rr.components]
+    ctx.close()
+    monkeypatch.delenv("SB_ROWV")
+    monkeypatch.delenv("SB_MUE_DERIVED")
+    return out
+
+
+@pytest.mark.parametrize("cells", WALL_GRIDS, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("form,theta,bc2,derive", [
+    ("stress", 0.7, "nn", False), ("stress", 0.0, "ff", False), ("laplacian", 0.7, "nf", False),
+    ("stress", 0.7, "fn", True), ("laplacian", 0.0, "nn", True)])
+def test_row_march_walls_match_per_face(cells, form, theta, bc2, derive, monkeypatch):
+    """Walls (no-slip / free-slip, any mix) at both ends of the marched row:
+    ghost values behind the low wall, wall-edge stresses at the high wall, the
+    wall-normal component's boundary faces left alone.  Against the per-face
+    kernels (SB_ROWV=0) at 1e-13 of the field's magnitude."""
+    a = _wall_run(cells, form, theta, bc2, derive, True, monkeypatch)
+    b = _wall_run(cells, form, theta, bc2, derive, False, monkeypatch)
+    assert a.keys() == b.keys()
+    for k in a:
+        for u, v in zip(a[k], b[k]):
+            assert u.shape == v.shape
+            assert np.max(np.abs(u - v)) <= 1e-13 * np.max(np.abs(v)), k
