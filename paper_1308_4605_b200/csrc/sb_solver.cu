@@ -389,7 +389,10 @@ double face_pass_bytes(const sb_ctx* c, const Level& L) {
   return per * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
 }
 double cell_pass_bytes(const sb_ctx* c, const Level& L) {
-  const double per = 16.0 + 8.0 * c->dim;
+  // phi + 1/2 rhs + 1/2 write, plus the d arrays of 1/rho_face -- which a
+  // constant-density level does not stream (LevelDev::beta_const), so they are
+  // not credited there
+  const double per = 16.0 + (L.d.beta_const ? 0.0 : 8.0 * c->dim);
   return per * (double)L.d.n[0] * L.d.n[1] * L.d.n[2];
 }
 

@@ -11,6 +11,13 @@ Conventions: domain [0,1]^d, h = 1/n; rhs u = f on unknown faces,
 rhs p = -g (M's second row is -D u, ``operators.py:365``); for fully periodic
 steady cases each f component's mean is removed; ``rescale`` is applied
 (``cli.py:340-343``) by ``prepare``.
+
+The bubble problem (``BubbleSpec``, ``bubble_profile``, ``bubble_coefficients``,
+``bubble_density``, ``inviscid_coefficients``, ``make_rhs``) is a DELIBERATE
+restatement of the reference's ``problems.py:36-135``: the reference's tests,
+presets and driver goldens feed these exact inputs, so the generator must
+replay the same Philox draws and formulas to be bit-identical on the host.  It
+is input generation, off the device path.
 """
 
 from __future__ import annotations
