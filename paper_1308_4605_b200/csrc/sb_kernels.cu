@@ -1254,6 +1254,7 @@ __global__ void k_box_axpy(LevelDev L, double* y, const double* __restrict__ x, 
 
 constexpr int kRedBlocks = kSMs * 8;   // partial-sum slots per reduction (8 CTAs/SM)
 constexpr int kMaxVec = 128;           // max basis vectors in one multi-dot
+constexpr int kVecChunk = 120;         // vectors per launch when a basis is longer (launch_cgs2 / launch_combo)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -3061,9 +3062,48 @@ void launch_scale_div(cudaStream_t s, const double* w, double d, double* out, lo
 
 void launch_combo(cudaStream_t s, double* out, const double* x, const double* V, long long vstride, int nv,
                   const double* y, long long n) {
-  ++g_kernel_launches;
-  launch_k(k_combo, grid_for(n / 2), kThreads, 0, s, reinterpret_cast<double2*>(out),
-                                                reinterpret_cast<const double2*>(x), V, vstride, nv, y, n / 2);
+  // the kernels stage <= kMaxVec coefficients in shared memory: longer
+  // combinations (GMRES restart >= 128) run in chunks, out accumulating
+  for (int c0 = 0; c0 < nv || c0 == 0; c0 += kVecChunk) {
+    const int nc = std::min(kVecChunk, nv - c0);
+    ++g_kernel_launches;
+    launch_k(k_combo, grid_for(n / 2), kThreads, 0, s, reinterpret_cast<double2*>(out),
+             reinterpret_cast<const double2*>(c0 == 0 ? x : out), V + (long long)c0 * vstride, vstride, nc, y + c0,
+             n / 2);
+  }
+}
+
+// Textbook CGS2 Arnoldi step on nv basis vectors (krylov.py:111-115 with MGS
+// replaced): h1 = V^T w, w -= V h1, h2 = V^T w, w -= V h2,
+// nrm2 = ||w||^2.  Up to kVecChunk vectors the update and the next reduction
+// share one read of the basis; a longer basis (restart >= 128) is processed in
+// chunks of kVecChunk vectors -- the dots of a pass all see the same w, the
+// updates accumulate.
+void launch_cgs2(cudaStream_t s, const double* V, long long vstride, int nv, double* w, long long n,
+                 double* partials, double* h1, double* h2, double* nrm2) {
+  if (nv <= kVecChunk) {
+    launch_multi_dot(s, V, vstride, nv, w, n, partials);
+    launch_finalize(s, partials, nv, h1);
+    launch_update_dot(s, V, vstride, nv, h1, w, n, partials, 0);
+    launch_finalize(s, partials, nv, h2);
+    launch_update_dot(s, V, vstride, nv, h2, w, n, partials, 1);
+    launch_finalize(s, partials, 1, nrm2);
+    return;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    double* h = pass == 0 ? h1 : h2;
+    for (int c0 = 0; c0 < nv; c0 += kVecChunk) {
+      const int nc = std::min(kVecChunk, nv - c0);
+      launch_multi_dot(s, V + (long long)c0 * vstride, vstride, nc, w, n, partials);
+      launch_finalize(s, partials, nc, h + c0);
+    }
+    for (int c0 = 0; c0 < nv; c0 += kVecChunk) {
+      const int nc = std::min(kVecChunk, nv - c0);
+      launch_update_dot(s, V + (long long)c0 * vstride, vstride, nc, h + c0, w, n, partials, 1);
+      if (pass == 1 && c0 + nc == nv) launch_finalize(s, partials, 1, nrm2);  // ||w||^2 after the last update
+      else g_red_blocks_used = kRedBlocks;
+    }
+  }
 }
 
 void launch_sub(cudaStream_t s, const double* a, const double* b, double* out, long long n) {

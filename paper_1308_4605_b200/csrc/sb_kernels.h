@@ -182,7 +182,10 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
 void launch_sum_partial(cudaStream_t s, const double* x, long long n, double* partials);
 void launch_scale_div(cudaStream_t s, const double* w, double d, double* out, long long n);
 void launch_combo(cudaStream_t s, double* out, const double* x, const double* V, long long vstride,
-                  int nv, const double* y, long long n);  // out = x + sum y_i V_i (y on device)
+                  int nv, const double* y, long long n);
+// CGS2 Arnoldi step (any number of basis vectors; chunked above 120)
+void launch_cgs2(cudaStream_t s, const double* V, long long vstride, int nv, double* w, long long n,
+                 double* partials, double* h1, double* h2, double* nrm2);  // out = x + sum y_i V_i (y on device)
 void launch_sub(cudaStream_t s, const double* a, const double* b, double* out, long long n);  // out=a-b
 void launch_sub_norm(cudaStream_t s, const double* a, const double* b, long long n, double* partials);
 

@@ -98,6 +98,9 @@ struct sb_ctx {
   double* dpart = nullptr;
   double* dsmall = nullptr;   // [h1 kMaxVec][h2 kMaxVec][misc 64][y kMaxVec]
   double* hsmall = nullptr;   // pinned mirror
+  double* dbig = nullptr;     // restart >= kMaxVec: [h1 M][h2 M][y M]
+  double* hbig = nullptr;     // pinned mirror
+  int bigcap = 0;
   long long vlen = 0;         // vector length (nblk * block)
   double *vb = nullptr, *vz0 = nullptr, *vx = nullptr, *vw = nullptr, *vMv = nullptr, *vt = nullptr;
   double* basis = nullptr;
@@ -951,7 +954,20 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     check_ready(c);
   }
   const int m = gc.restart;
-  if (m < 1 || m >= kMaxVec) throw ArgErr(SB_EINVAL, "restart must be in [1, 127] on the device path");
+  if (m < 1) throw ArgErr(SB_EINVAL, "restart must be >= 1");
+  // restart >= kMaxVec: the delayed-reorthogonalisation kernels keep one
+  // partial sum per basis vector in shared memory, so a longer basis takes the
+  // textbook CGS2 step in chunks (launch_cgs2); the reference's GmresConfig
+  // has no upper bound (krylov.py:23-38)
+  const bool big = m >= kMaxVec;
+  const int bigM = (m + 2 + 3) / 4 * 4;
+  if (big && c->bigcap < bigM) {
+    if (c->hbig) cudaFreeHost(c->hbig);
+    c->hbig = nullptr;
+    c->dbig = dalloc(c, 3LL * bigM);
+    CK(cudaMallocHost(&c->hbig, (size_t)3 * bigM * 8));
+    c->bigcap = bigM;
+  }
   ensure_vectors(c);
   ensure_basis(c, m);
   if (c->profiling) prof_reset(c);
@@ -1009,6 +1025,9 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
     return e && std::strcmp(e, "gram1") == 0;
   }();
   std::vector<double> G((m + 1) * (m + 1), 0.0), tv(m + 1);
+  const bool cgs2_l = cgs2 || big, gram_l = gram && !big;
+  double* const yd = big ? c->dbig + 2 * c->bigcap : dy(c);  // least-squares solution y on the device
+  double* const yh = big ? c->hbig + 2 * c->bigcap : hy(c);
   double gam = 1.0;
   int k = 0;
   bool first = true;
@@ -1038,22 +1057,28 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
       // the Gram pass B subtracts the deferred null-space means while it
       // streams w (P^-1 M Q has zero means in exact arithmetic, so pass A's
       // dots with the basis are unaffected); the other variants project here
-      if (!gram) finish_projection(c, c->vw);
+      if (!gram_l) finish_projection(c, c->vw);
       *vcyc += precond_cost(c, pc);
       ++k;
       double hn;
-      if (cgs2) {
+      if (cgs2_l) {
         // CGS2 Arnoldi (parity-safe replacement of MGS)
         const int nv = j + 1;
-        launch_multi_dot(c->st, V, vl, nv, c->vw, vl, c->dpart);
-        launch_finalize(c->st, c->dpart, nv, dh1(c));
-        launch_update_dot(c->st, V, vl, nv, dh1(c), c->vw, vl, c->dpart, 0);
-        launch_finalize(c->st, c->dpart, nv, dh2(c));
-        launch_update_dot(c->st, V, vl, nv, dh2(c), c->vw, vl, c->dpart, 1);
-        launch_finalize(c->st, c->dpart, 1, dmisc(c) + 1);
+        double* h1d = big ? c->dbig : dh1(c);
+        double* h2d = big ? c->dbig + c->bigcap : dh2(c);
+        launch_cgs2(c->st, V, vl, nv, c->vw, vl, c->dpart, h1d, h2d, dmisc(c) + 1);
+        const double *h1h, *h2h;
+        if (big) {
+          CK(cudaMemcpyAsync(c->hbig, c->dbig, (size_t)2 * c->bigcap * 8, cudaMemcpyDeviceToHost, c->st));
+          h1h = c->hbig;
+          h2h = c->hbig + c->bigcap;
+        } else {
+          h1h = hh1(c);
+          h2h = hh2(c);
+        }
         CK(cudaMemcpyAsync(c->hsmall, c->dsmall, (4 * kMaxVec + 2) * 8, cudaMemcpyDeviceToHost, c->st));
         sync(c);
-        for (int i = 0; i <= j; ++i) H[i * m + j] = hh1(c)[i] + hh2(c)[i];
+        for (int i = 0; i <= j; ++i) H[i * m + j] = h1h[i] + h2h[i];
         hn = std::sqrt(hmisc(c)[1]);
       } else {
         // CGS2 with delayed reorthogonalisation: two passes over the basis.
@@ -1263,11 +1288,11 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
       double rt = NAN;
       if (gc.track_true_residual || conv || brk) {
         solve_upper(H, m, g.data(), ydim, y.data());
-        std::memcpy(hy(c), y.data(), ydim * 8);
-        CK(cudaMemcpyAsync(dy(c), hy(c), ydim * 8, cudaMemcpyHostToDevice, c->st));
+        std::memcpy(yh, y.data(), ydim * 8);
+        CK(cudaMemcpyAsync(yd, yh, ydim * 8, cudaMemcpyHostToDevice, c->st));
       }
       if (gc.track_true_residual) {
-        launch_combo(c->st, c->vt, c->vx, V, vl, ydim, dy(c), vl);
+        launch_combo(c->st, c->vt, c->vx, V, vl, ydim, yd, vl);
         apply_M_vec(c, c->vt, c->vMv);
         launch_sub_norm(c->st, c->vb, c->vMv, vl, c->dpart);
         launch_finalize(c->st, c->dpart, 1, dmisc(c) + 2);
@@ -1275,17 +1300,17 @@ int gmres(sb_ctx* c, const sb_precond& pc, const sb_gmres& gc, const sb_smoother
       }
       add_row(k, rp, rt, j == 0 && !first);
       if (conv || brk) {
-        launch_combo(c->st, c->vx, c->vx, V, vl, ydim, dy(c), vl);
+        launch_combo(c->st, c->vx, c->vx, V, vl, ydim, yd, vl);
         return finish(conv ? SB_STATUS_CONVERGED : SB_STATUS_BREAKDOWN);
       }
-      if (cgs2) launch_scale_div(c->st, c->vw, hn, V + (long long)(j + 1) * vl, vl);
+      if (cgs2_l) launch_scale_div(c->st, c->vw, hn, V + (long long)(j + 1) * vl, vl);
       ++j;
     }
     // x = x + V[:j] y  (the last iteration's least-squares solution)
     solve_upper(H, m, g.data(), ydim, y.data());
-    std::memcpy(hy(c), y.data(), ydim * 8);
-    CK(cudaMemcpyAsync(dy(c), hy(c), ydim * 8, cudaMemcpyHostToDevice, c->st));
-    launch_combo(c->st, c->vx, c->vx, V, vl, ydim, dy(c), vl);
+    std::memcpy(yh, y.data(), ydim * 8);
+    CK(cudaMemcpyAsync(yd, yh, ydim * 8, cudaMemcpyHostToDevice, c->st));
+    launch_combo(c->st, c->vx, c->vx, V, vl, ydim, yd, vl);
     first = false;
     if (k >= gc.max_iters) return finish(SB_STATUS_MAXITER);
     // r = z0 - P^{-1} M x
@@ -1535,6 +1560,7 @@ void sb_destroy(sb_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->hsmall) cudaFreeHost(c->hsmall);
+  if (c->hbig) cudaFreeHost(c->hbig);
   if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
 }

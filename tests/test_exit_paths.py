@@ -147,3 +147,51 @@ def test_device_zero_diagonal_raises(dim):
     hier = build_hierarchy(g, coeff)
     with pytest.raises(ZeroDivisionError):
         vcycle(rhs.u, hier, SmootherParams(), "face")
+
+
+@pytest.mark.gpu
+def test_large_restart_matches_oracle():
+    """GmresConfig.restart has no upper bound in the reference (krylov.py:23-38).
+    Beyond 127 basis vectors the device takes the chunked CGS2 step
+    (launch_cgs2): a slowly converging flat system that needs > 240 Arnoldi
+    vectors in one cycle (two full chunks and a remainder), against the
+    oracle's restatement; and a Stokes solve (C4 recipe at 16^3, 99 iterations
+    unrestarted) with restart 160 -- the large-restart path -- against the
+    default path with restart 110: neither restarts, same Krylov space."""
+    from oracle import stokes_oracle as O
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import pack_stokes
+    from paper_1308_4605_b200.krylov import GmresConfig, gmres_kernel, gmres_solve
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    rng = np.random.default_rng(3)
+    n = 800
+    M = np.eye(n) + 0.99 * rng.standard_normal((n, n)) / np.sqrt(n)
+    b = rng.standard_normal(n)
+    tgt = 1e-11 * np.linalg.norm(b)
+    rows_g, rows_r = [], []
+    xg, sg, kg = gmres_kernel(lambda v: M @ v, b, 300, 900, tgt, 1e-14, lambda k, xk, rp, rf: rows_g.append((k, rp, rf)))
+    xr, sr, kr = O.gmres_flat(lambda v: M @ v, b, 300, 900, tgt, 1e-14, lambda k, xk, rp, rf: rows_r.append((k, rp, rf)))
+    assert kr > 241, kr  # the case exercises three chunks (120 + 120 + remainder)
+    assert sg == sr and abs(kg - kr) <= 1
+    kk = min(len(rows_g), len(rows_r))
+    rp_g, rp_r = np.array([r[1] for r in rows_g[:kk]]), np.array([r[1] for r in rows_r[:kk]])
+    keep = rp_r > 1e-9 * np.linalg.norm(b)
+    assert np.allclose(rp_g[keep], rp_r[keep], rtol=1e-6)
+    assert np.linalg.norm(xg - xr) <= 1e-8 * np.linalg.norm(xr)
+    assert np.linalg.norm(M @ xg - b) <= 1e-10 * np.linalg.norm(b)
+
+    case = PR.make_case("C4", 16)
+    cs, rs, _ = PR.prepare(case)
+    res = {}
+    for m in (110, 160):
+        x, h = gmres_solve(rs, cs, PrecondConfig(kind=P1),
+                           GmresConfig(restart=m, max_iters=400, rtol=1e-9, track_true_residual=True))
+        res[m] = (pack_stokes(x), h)
+    ha, hb = res[110][1], res[160][1]
+    assert ha.status == hb.status == "converged"
+    assert hb.iterations == ha.iterations
+    ra = np.array([e.resid_precond for e in ha.entries])
+    rb = np.array([e.resid_precond for e in hb.entries])
+    assert np.allclose(ra, rb, rtol=1e-6)
+    assert ha.iterations == 99
+    assert np.linalg.norm(res[110][0] - res[160][0]) <= 1e-8 * np.linalg.norm(res[110][0])
