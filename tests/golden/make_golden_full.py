@@ -16,7 +16,11 @@ as the CLI does (``cli.py:340-343``) and solved by the reference's
   (the full solve; ~7 min here);
 * ``C4_256_k3`` -- C4 at 256^3, P1, GMRES(30), ``max_iters=3`` (SURVEY §8c:
   C4/C5 are compared over their first k iterations);
-* ``C5_256_k3`` -- C5's single-GPU point 256^3, P1, GMRES(50), ``max_iters=3``.
+* ``C5_256_k3`` -- C5's single-GPU point 256^3, P1, GMRES(50), ``max_iters=3``;
+* ``C4_256_P5_k2``, ``C4_256_P2_k2``, ``C5_256_P3_k2`` -- the other
+  preconditioner families (P5: two velocity solves; P2 / P3: triangular forms,
+  the Schur complement with its Poisson solve on C4's theta > 0) at 256^3,
+  ``max_iters=2``.
 
 Stored per case (``tests/golden/full_<case>.npz``): the history rows
 (k, scalar V-cycles, r_P, r_true, restart flag), iterations and status, the
@@ -50,6 +54,10 @@ CASES = {  # name: (config, n, precond, max_iters, subsample stride)
     "C3_128": ("C3", 128, "P1", 500, 64),
     "C4_256_k3": ("C4", 256, "P1", 3, 512),
     "C5_256_k3": ("C5", 256, "P1", 3, 512),
+    # the other preconditioner families at BASELINE size (two iterations each)
+    "C4_256_P5_k2": ("C4", 256, "P5", 2, 1024),
+    "C5_256_P3_k2": ("C5", 256, "P3", 2, 1024),
+    "C4_256_P2_k2": ("C4", 256, "P2", 2, 1024),
 }
 
 
