@@ -123,45 +123,9 @@ struct UA7 {
 template <bool CG>
 __device__ __forceinline__ double ldu(const double* p, int i) { return CG ? __ldcg(p + i) : p[i]; }
 
-// VEC (3D all-periodic levels with an even contiguous extent): the value at f
-// and its neighbour along the contiguous axis inside the same aligned pair
-// (f ^ 1: the +1 neighbour of an even f, the -1 neighbour of an odd f) come
-// from ONE 16-byte load.  A colour pass reads every other face of a row, so
-// its scalar loads touch four 128-B lines per warp for 256 useful bytes; the
-// pair load delivers two operands for the same four lines.  Every array of a
-// level is 16-B aligned with even row starts (pitched box, P2 a multiple of
-// 4), so f is even exactly when its contiguous index is.  Same values, same
-// arithmetic: bit-identical to the scalar loads.
-template <bool NC>
-__device__ __forceinline__ void ldpair(const double* p, int f, double& own, double& other) {
-  const double2* q = reinterpret_cast<const double2*>(p + (f & ~1));
-  const double2 v = NC ? __ldg(q) : *q;
-  const bool odd = f & 1;
-  own = odd ? v.y : v.x;
-  other = odd ? v.x : v.y;
-}
-
-template <int DIM, int A, int PA = false, bool CG = false, bool VEC = false>
+template <int DIM, int A, int PA = false, bool CG = false>
 __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, int f, const int* ci) {
   UA7 s;
-  if (VEC) {
-    // u_A is relaxed in place, but this pass writes only the thread's own face
-    // of the pair: the plain 16-B load sees no race on the value it uses
-    double o;
-    ldpair<false>(ua, f, s.c, o);
-    const bool odd = f & 1;
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int dp = b == 0 ? dplus<0, PA>(L, ci[0]) : dplus<1, PA>(L, ci[1]);
-      const int dm = b == 0 ? dminus<0, PA>(L, ci[0]) : dminus<1, PA>(L, ci[1]);
-      s.p[b] = ua[f + dp];
-      s.m[b] = ua[f + dm];
-    }
-    const double far = ua[f + (odd ? dplus<2, PA>(L, ci[2]) : dminus<2, PA>(L, ci[2]))];
-    s.p[2] = odd ? far : o;
-    s.m[2] = odd ? o : far;
-    return s;
-  }
   s.c = ldu<CG>(ua, f);
 #pragma unroll
   for (int b = 3 - DIM; b < 3; ++b) {
@@ -191,7 +155,7 @@ __device__ __forceinline__ UA7 gather_ua(const LevelDev& L, const double* ua, in
 // ZM: bit B set = component B is known to be identically zero (the first
 // sweep of a V-cycle level starts from x = 0, multigrid.py:409-439), so its
 // loads are replaced by the value they would return.
-template <int DIM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0, bool VEC = false>
+template <int DIM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0>
 struct GAcc {
   const LevelDev& L;
   const double* const* u;
@@ -200,95 +164,10 @@ struct GAcc {
   int dmA;
   double mf, mfa;      // DE: mu_c at f, f - e_A (loaded once)
   double me[3][2];     // DE: derived edge viscosities [B][hi edge]
-  double ubv[3][2][2]; // VEC: the cross-term operands u_B [B][hi edge][low A], pair-loaded
-  // VEC: mu_c (x + o, x + o - e_X) pairs along the contiguous axis: v0 = value at
-  // x, v1 = its contiguous neighbour on the low (LOW) / high side
-  template <bool LOW>
-  __device__ __forceinline__ void mu_pair(int x, double& v0, double& v1) const {
-    double o;
-    ldpair<true>(L.mu_c, x, v0, o);
-    const bool odd = x & 1;
-    if (LOW) v1 = odd ? o : ld(L.mu_c, x + dminus<2, PA>(L, ci[2]));
-    else v1 = odd ? ld(L.mu_c, x + dplus<2, PA>(L, ci[2])) : o;
-  }
   __device__ __forceinline__ GAcc(const LevelDev& L_, const double* const* u_, int f_, const int* ci_)
       : L(L_), u(u_), f(f_), ci(ci_) {
     dmA = (A == 0) ? dminus<0, PA>(L, ci[0]) : (A == 1 ? dminus<1, PA>(L, ci[1]) : dminus<2, PA>(L, ci[2]));
-    if (DE && VEC) {
-      // 3D, all periodic, no zero masks.  Same operands and expressions as the
-      // scalar branch below; operands adjacent along the contiguous axis share
-      // one 16-byte load
-      const bool odd = f & 1;
-      const int p2 = dplus<2, PA>(L, ci[2]), m2 = dminus<2, PA>(L, ci[2]);
-      if (A != 2) {
-        constexpr int B1 = A == 0 ? 1 : 0;  // the non-contiguous tangent
-        // rows (0,0) and (-e_A): k-1, k, k+1
-        double o, oa;
-        ldpair<true>(L.mu_c, f, mf, o);
-        ldpair<true>(L.mu_c, f + dmA, mfa, oa);
-        const double far = ld(L.mu_c, f + (odd ? p2 : m2)), fara = ld(L.mu_c, f + (odd ? p2 : m2) + dmA);
-        const double fbm2 = odd ? o : far, fbma2 = odd ? oa : fara;
-        const double fbp2 = odd ? far : o, fbpa2 = odd ? fara : oa;
-        const double mA = 0.5 * (mf + mfa);
-        // B = 2 > A: lower plane axis A first
-        me[2][0] = 0.5 * (mA + 0.5 * (fbm2 + fbma2));
-        me[2][1] = 0.5 * (0.5 * (fbp2 + fbpa2) + mA);
-        const int pB = B1 == 0 ? dplus<0, PA>(L, ci[0]) : dplus<1, PA>(L, ci[1]);
-        const int mB = B1 == 0 ? dminus<0, PA>(L, ci[0]) : dminus<1, PA>(L, ci[1]);
-        const double fbm = ld(L.mu_c, f + mB), fbma = ld(L.mu_c, f + mB + dmA);
-        const double fbp = ld(L.mu_c, f + pB), fbpa = ld(L.mu_c, f + pB + dmA);
-        me[B1][0] = A < B1 ? 0.5 * (mA + 0.5 * (fbm + fbma)) : 0.5 * (0.5 * (mf + fbm) + 0.5 * (mfa + fbma));
-        me[B1][1] = A < B1 ? 0.5 * (0.5 * (fbp + fbpa) + mA) : 0.5 * (0.5 * (fbp + mf) + 0.5 * (fbpa + mfa));
-        // cross terms: u_2 at f, f + e_2 (rows (0,0), (-e_A)); u_B1 scalar
-        double a0, a1, b0, b1;
-        {
-          double oo, ooa;
-          ldpair<NC>(u[2], f, a0, oo);
-          ldpair<NC>(u[2], f + dmA, b0, ooa);
-          if (odd) {
-            a1 = NC ? ld(u[2], f + p2) : u[2][f + p2];
-            b1 = NC ? ld(u[2], f + p2 + dmA) : u[2][f + p2 + dmA];
-          } else {
-            a1 = oo;
-            b1 = ooa;
-          }
-        }
-        ubv[2][0][0] = a0;
-        ubv[2][0][1] = b0;
-        ubv[2][1][0] = a1;
-        ubv[2][1][1] = b1;
-        ubv[B1][0][0] = NC ? ld(u[B1], f) : u[B1][f];
-        ubv[B1][0][1] = NC ? ld(u[B1], f + dmA) : u[B1][f + dmA];
-        ubv[B1][1][0] = NC ? ld(u[B1], f + pB) : u[B1][f + pB];
-        ubv[B1][1][1] = NC ? ld(u[B1], f + pB + dmA) : u[B1][f + pB + dmA];
-      } else {
-        // A = 2: every (x, x - e_2) operand pair lies along the contiguous axis
-        mu_pair<true>(f, mf, mfa);
-        const double mA = 0.5 * (mf + mfa);  // unused by the A > B order below; kept for symmetry
-        (void)mA;
-#pragma unroll
-        for (int B = 0; B < 2; ++B) {
-          const int pB = B == 0 ? dplus<0, PA>(L, ci[0]) : dplus<1, PA>(L, ci[1]);
-          const int mB = B == 0 ? dminus<0, PA>(L, ci[0]) : dminus<1, PA>(L, ci[1]);
-          double fbm, fbma, fbp, fbpa;
-          mu_pair<true>(f + mB, fbm, fbma);
-          mu_pair<true>(f + pB, fbp, fbpa);
-          // A = 2 > B: lower plane axis B first
-          me[B][0] = 0.5 * (0.5 * (mf + fbm) + 0.5 * (mfa + fbma));
-          me[B][1] = 0.5 * (0.5 * (fbp + mf) + 0.5 * (fbpa + mfa));
-          double o0, o1;
-          ldpair<NC>(u[B], f, ubv[B][0][0], o0);
-          ldpair<NC>(u[B], f + pB, ubv[B][1][0], o1);
-          if (odd) {
-            ubv[B][0][1] = o0;
-            ubv[B][1][1] = o1;
-          } else {
-            ubv[B][0][1] = NC ? ld(u[B], f + m2) : u[B][f + m2];
-            ubv[B][1][1] = NC ? ld(u[B], f + pB + m2) : u[B][f + pB + m2];
-          }
-        }
-      }
-    } else if (DE) {
+    if (DE) {
       // every mu_c operand of the row loaded once: f, f-e_A, f-+e_B, f-+e_B-e_A
       mf = ld(L.mu_c, f);
       mfa = ld(L.mu_c, f + dmA);
@@ -335,7 +214,6 @@ struct GAcc {
   }
   template <int B>
   __device__ __forceinline__ double ub(bool hi, bool lowA) const {
-    if (DE && VEC) return ubv[B][hi ? 1 : 0][lowA ? 1 : 0];
     if (ZM & (1 << B)) return 0.0;
     const int e = hi ? f + eB<B>() : f;
     return NC ? ld(u[B], lowA ? e + dmA : e) : u[B][lowA ? e + dmA : e];
@@ -438,10 +316,10 @@ __device__ __forceinline__ double face_row_t(const LevelDev& L, const UA7& s, co
   return tr - res;
 }
 
-template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0, bool VEC = false>
+template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool DE = false, int ZM = 0>
 __device__ __forceinline__ double face_row_core(const LevelDev& L, const UA7& s, const double* const* u, int f,
                                                 const int* ci, double& diag) {
-  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE, ZM, VEC>(L, u, f, ci), ci, diag);
+  return face_row_t<DIM, FORM, A, PA>(L, s, GAcc<DIM, A, PA, NC, DE, ZM>(L, u, f, ci), ci, diag);
 }
 
 template <int DIM, int FORM, int A, int PA = false, bool NC = true, bool CG = false, bool DE = false>

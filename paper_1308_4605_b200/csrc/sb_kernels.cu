@@ -119,7 +119,7 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 template <int A>
 __host__ __device__ constexpr int later_mask() { return A == 0 ? 6 : (A == 1 ? 4 : 0); }
 
-template <int DIM, int FORM, int A, int PHASE, int PA, bool DE = false, int Z = 0, bool VEC = false>
+template <int DIM, int FORM, int A, int PHASE, int PA, bool DE = false, int Z = 0>
 __global__ void __launch_bounds__(kThreads)
 k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, int parity,
               double omega, Box b, unsigned half2, unsigned total) {
@@ -154,10 +154,10 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
       return;
     }
     constexpr int ZM = Z == 1 ? later_mask<A>() : 0;
-    const UA7 s7 = gather_ua<DIM, A, PA, false, VEC>(L, uc[A], f, ci);
-    const double au = face_row_core<DIM, FORM, A, PA, true, DE, ZM, VEC>(L, s7, uc, f, ci, dg);
+    const double au =
+        face_row_core<DIM, FORM, A, PA, true, DE, ZM>(L, gather_ua<DIM, A, PA>(L, uc[A], f, ci), uc, f, ci, dg);
     const double res = __ldg(rhs + f) - au;
-    const double nv = (VEC ? s7.c : uc[A][f]) + omega * (res / dg);
+    const double nv = uc[A][f] + omega * (res / dg);
     if (PHASE == 2) tmp[f] = nv;
     else u.p[A][f] = nv;
   }
@@ -2365,16 +2365,7 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
     if (derive_mue(L)) launch_k(k_face_colour<DIM, FM, A, 0, PAT, true, ZZ>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total); \
     else launch_k(k_face_colour<DIM, FM, A, 0, PAT, false, ZZ>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);            \
   })
-    // plain passes on 3D all-periodic levels with derived mu_e: operands
-    // adjacent along the contiguous axis by 16-byte pair loads (sb_device.cuh
-    // ldpair); SB_FC_VEC=0 keeps the scalar loads (bit-identical either way)
-    static const bool vec_on = [] {
-      const char* e = std::getenv("SB_FC_VEC");
-      return !(e && e[0] == '0');
-    }();
-    if (z == 0 && DIM == 3 && vec_on && derive_mue(L) && all_periodic(L) && (L.n[2] & 1) == 0) {
-      launch_k(k_face_colour<DIM, FM, A, 0, 1, true, 0, (DIM == 3)>, g, kb, 0, s, L, u, rhs, nullptr, parity, omega, b, half2, total);
-    } else if (z == 2) {
+    if (z == 2) {
       SB_FC_Z(2);
     } else if (z == 1) {
       SB_FC_Z(1);
