@@ -24,7 +24,7 @@ def _nccl_dir():
 
 NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"] + os.environ.get("SB_NVCC_EXTRA", "").split()
 
 
 def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
