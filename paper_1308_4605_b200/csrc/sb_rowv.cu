@@ -1,33 +1,35 @@
-// sb_rowv.cu -- row-vector stencil kernels for large all-periodic 3D levels
-// (sm_100a): the face residual field of the split residual -> restriction
-// and apply_M (default), and the face colour passes (opt-in).
+// sb_rowv.cu -- row kernels for large 3D levels (sm_100a): the face residual
+// field of the split residual -> restriction and apply_M (default), and the
+// face colour passes (opt-in).
 //
 // The one-face-per-thread kernels (sb_kernels.cu) issue one load per stencil
 // operand; a colour pass reads every other face of a row, so each warp-wide
 // load touches four 128-B lines for 256 useful bytes, and the all-face
-// kernels evaluate three face rows per thread from ~70 separate loads.  Here
-// a warp owns a contiguous row segment and every operand ROW is read once,
-// contiguously: a colour pass maps lane t to the face pair (2t, 2t+1) of a
-// 64-face segment (one 16-B load per row), the all-face kernels map lane t to
-// face t of a 32-face segment; the +-1 neighbours along the contiguous axis
-// come from the neighbouring lane (__shfl), the segment ends from one
-// uniform-address load.  Each operand array contributes only the rows its
-// stencil touches (compile-time masks).  All loads are issued before any
-// shuffle (Rows::issue / finish) so they are in flight together.
+// kernels evaluate three face rows per thread from ~70 separate loads.
 //
-// Measured (ncu, C5 256^3 finest level, tools/rv_ab.sh): residual field
-// 465 -> 426 us, apply_M 533 -> 490 us; the colour pass is NOT faster than
-// the per-face kernel with derived edge viscosities (173-195 vs 155-164 us:
-// 74-80 registers, 24 resident warps, latency bound), so it is opt-in
-// (SB_ROWV_COLOUR=1).
+// Two generations live here:
+//  * k_face_all_rm (default, "row-march"): a warp walks one whole row in
+//    32-face segments, -1 neighbours carried between segments, every edge /
+//    normal stress evaluated once and shared by the two rows that use it,
+//    FMAs on the final combinations; all-periodic levels and levels with walls
+//    along the contiguous axis (C4).  ncu C5 256^3: apply_M 322 us, residual
+//    field 319 us (0.77 / 0.85 of the measured HBM peak).  Equal to the
+//    per-face kernels to ~1e-15 relative (different rounding order).
+//  * k_face_all_rv / k_face_colour_rv ("segment" kernels, SB_ROWM=0 /
+//    SB_ROWV_COLOUR=1): a warp owns a 32- or 64-face row segment and every
+//    operand ROW is read once, contiguously; the +-1 neighbours along the
+//    contiguous axis come from the neighbouring lane (__shfl), the segment
+//    ends from one uniform-address load.  Same arithmetic as face_row_t on
+//    the same operands: bit-identical to the per-face kernels
+//    (tests/test_gpu_rowv.py).  Measured (ncu, C5 256^3): residual field
+//    465 -> 413 us, apply_M 533 -> 510 us against the per-face kernels; the
+//    colour pass is NOT faster than the per-face kernel with derived edge
+//    viscosities (173-195 vs 155-164 us: 74-80 registers, latency bound).
 //
-// The arithmetic is face_row_t (sb_device.cuh) on the same operand values,
-// in the same order: results are bit-identical to the per-face kernels
-// (tests/test_gpu_rowv.py).
-//
-// Scope: 3D, all axes periodic (a slab-distributed axis 0 reads ghost
+// Scope: 3D, axes 0 and 1 periodic (a slab-distributed axis 0 reads ghost
 // planes), LAPLACIAN / STRESS forms, contiguous extent a multiple of 64
-// (rowv_supported).
+// (rowv_supported); walls along the contiguous axis only in the row-march
+// kernel.
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include "sb_kernels.h"
