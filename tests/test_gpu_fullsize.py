@@ -94,3 +94,57 @@ def test_arnoldi_pass_a_variants(name, n, monkeypatch):
         assert i == i0, v
         assert np.allclose(r, r0, rtol=1e-9), v
         assert np.linalg.norm(x - x0) <= 1e-11 * np.linalg.norm(x0), v
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_operator_properties(name):
+    """apply_M at 256^3 (the row-march kernel; C4: walls along z, theta > 0;
+    C5: periodic, derived edge viscosities) through properties that need no
+    oracle: M = [[A, G], [-D, 0]] is symmetric (A = A^T, G = -D^T), linear, and
+    maps a constant pressure to zero."""
+    from paper_1308_4605_b200 import operators as OPS
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import CellField, FaceField, StokesVector, dot
+    case = PR.make_case(name)
+    assert case.grid.cells == (256, 256, 256)
+    cs, rs, spec = PR.prepare(case)
+    g = case.grid
+    ctx = OPS.DeviceContext(g, cs.viscous_form)
+    ctx.set_coefficients(cs)
+    rng = np.random.default_rng(17)
+
+    def rand_vec():
+        comps = []
+        for a in range(3):
+            c = rng.standard_normal(g.face_shape(a))
+            if not g.periodic(a):  # wall-normal boundary faces carry no unknown
+                idx = [slice(None)] * 3
+                idx[a] = 0
+                c[tuple(idx)] = 0.0
+                idx[a] = -1
+                c[tuple(idx)] = 0.0
+            comps.append(c)
+        return StokesVector(FaceField(g, tuple(comps)), CellField(g, rng.standard_normal(g.cells)))
+
+    x, y = rand_vec(), rand_vec()
+    Mx = OPS.apply_M(x, cs, ctx=ctx)
+    My = OPS.apply_M(y, cs, ctx=ctx)
+    # symmetry: <y, M x> = <M y, x> over the unknowns
+    a, b = dot(y, Mx), dot(My, x)
+    scale = np.sqrt(dot(x, x) * dot(Mx, Mx))
+    assert abs(a - b) <= 1e-12 * scale
+    # linearity
+    z = StokesVector(FaceField(g, tuple(2.0 * u - 0.5 * v for u, v in zip(x.u.components, y.u.components))),
+                     CellField(g, 2.0 * x.p.data - 0.5 * y.p.data))
+    Mz = OPS.apply_M(z, cs, ctx=ctx)
+    for c in range(3):
+        want = 2.0 * Mx.u.components[c] - 0.5 * My.u.components[c]
+        assert np.max(np.abs(Mz.u.components[c] - want)) <= 1e-12 * np.max(np.abs(want))
+    want = 2.0 * Mx.p.data - 0.5 * My.p.data
+    assert np.max(np.abs(Mz.p.data - want)) <= 1e-12 * np.max(np.abs(want))
+    # a constant pressure has zero gradient
+    one = StokesVector(FaceField.zeros(g), CellField.full(g, 3.25))
+    M1 = OPS.apply_M(one, cs, ctx=ctx)
+    assert all(np.all(c == 0.0) for c in M1.u.components)
+    assert np.all(M1.p.data == 0.0)
+    ctx.close()
