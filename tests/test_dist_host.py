@@ -138,3 +138,76 @@ def test_two_rank_gloo_decomposition():
         assert res[r]["ids_equal"]
         assert res[r]["partition_roundtrip"]
         assert res[r]["sweep_err"] <= 1e-13, res[r]
+
+
+def _slabs_in_threads(cells, world):
+    """make_c5_slab on `world` simulated ranks (threads), its `reduce` callback
+    played by a barrier-synchronised all-reduce -- the bench's per-rank input
+    generation at N > 1 (bench.py run_dist) without GPUs."""
+    import threading
+
+    from paper_1308_4605_b200 import problems as PR
+    bar = threading.Barrier(world)
+    box = [None] * world
+    out = [None] * world
+    err = []
+
+    def reducer(rank):
+        def reduce(kind, a, b):
+            box[rank] = (a, b)
+            bar.wait()
+            vals = list(box)
+            bar.wait()
+            if kind == "minmax":
+                return min(v[0] for v in vals), max(v[1] for v in vals)
+            return sum(v[0] for v in vals), sum(v[1] for v in vals)
+        return reduce
+
+    def work(rank):
+        try:
+            out[rank] = PR.make_c5_slab(cells, world, rank, reduce=reducer(rank))
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+            bar.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not err, err
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c5_slab_generation_matches_the_global_recipe(world):
+    """The weak-scaling bench generates each rank's planes of C5 locally
+    (problems.make_c5_slab, global min / max / means through the reduce
+    callback).  The assembled coefficient field must be the global recipe's
+    (problems.make_case: same Fourier modes, same averaging), independent of
+    the number of ranks, and the right-hand side must have zero global means."""
+    from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.dist import assemble
+    cells = (16, 8, 12)
+    one = _slabs_in_threads(cells, 1)[0]
+    many = _slabs_in_threads(cells, world)
+    grid, c1 = one[0], one[3]
+    assert all(m[3] == c1 for m in many)  # the same global rescale factor on every rank
+    assert all(m[0].cells == cells for m in many)
+    cat = lambda pick: assemble([pick(m) for m in many])
+    assert np.array_equal(cat(lambda m: m[1].mu_cell.data), one[1].mu_cell.data)
+    for key in ((0, 1), (0, 2), (1, 2)):
+        assert np.array_equal(cat(lambda m: m[1].mu_node_edge.arrays[key]), one[1].mu_node_edge.arrays[key])
+    for a in range(3):
+        assert np.array_equal(cat(lambda m: m[1].rho_face.components[a]), one[1].rho_face.components[a])
+        fa = cat(lambda m: m[2].u.components[a])
+        assert abs(fa.mean()) <= 1e-15 * np.abs(fa).max() * fa.size ** 0.5
+    gp = cat(lambda m: m[2].p.data)
+    assert abs(gp.mean()) <= 1e-15 * np.abs(gp).max() * gp.size ** 0.5
+    # against the global recipe (unrescaled mu; h differs at this size, the field does not)
+    case = PR.make_case("C5", cells)
+    mu_glob = case.coeff.mu_cell.data
+    assert np.allclose(one[1].mu_cell.data / c1, mu_glob, rtol=1e-12)
+    for key in ((0, 1), (0, 2), (1, 2)):
+        assert np.allclose(one[1].mu_node_edge.arrays[key] / c1, case.coeff.mu_node_edge.arrays[key], rtol=1e-12)
+    assert c1 == pytest.approx((1.0 / 512) / mu_glob.max(), rel=1e-12)
