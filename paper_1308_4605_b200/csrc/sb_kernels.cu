@@ -2331,10 +2331,14 @@ static bool odd_periodic(const LevelDev& L, int dim) {
 
 template <int DIM, int FM, int A>
 static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0, int ext0 = 0) {
+                          int parity, double omega, int z = 0, int ext0 = 0, int w_lo = 0, int w_hi = -1) {
   Box b = face_box(L, DIM, A);
   b.lo[0] -= ext0;  // slab levels: also relax the ghost planes (sb_dist.inc dsweep_face)
   b.hi[0] += ext0;
+  if (w_hi >= w_lo) {  // a window of planes
+    b.lo[0] = w_lo;
+    b.hi[0] = w_hi;
+  }
   const unsigned len2 = (unsigned)(b.hi[2] - b.lo[2] + 1);
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
@@ -2381,7 +2385,7 @@ static void face_colour_t(cudaStream_t s, const LevelDev& L, Ptr3 u, const doubl
 }
 
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z, int ext0) {
+                        const double* rhsA, int parity, double omega, int z, int ext0, int w_lo, int w_hi) {
   ++g_kernel_launches;
   // odd periodic extents need the two-phase (Jacobi-within-colour) form; the
   // caller's level scratch is passed through u.p[?] is not available here, so
@@ -2392,12 +2396,12 @@ void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, in
   }
   SB_DISPATCH_FORM(form, {
     if (dim == 3) {
-      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
-      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
-      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      if (A == 0) face_colour_t<3, FM, 0>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, w_lo, w_hi);
+      else if (A == 1) face_colour_t<3, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, w_lo, w_hi);
+      else face_colour_t<3, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, w_lo, w_hi);
     } else {
-      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
-      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0);
+      if (A == 1) face_colour_t<2, FM, 1>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, w_lo, w_hi);
+      else face_colour_t<2, FM, 2>(s, L, u, rhsA, nullptr, parity, omega, z, ext0, w_lo, w_hi);
     }
   });
 }
@@ -2419,10 +2423,14 @@ void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form
 
 template <int DIM>
 static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const double* rhs, double* tmp,
-                          int parity, double omega, int z = 0, int ext0 = 0) {
+                          int parity, double omega, int z = 0, int ext0 = 0, int w_lo = 0, int w_hi = -1) {
   Box b = cell_box(L);
   b.lo[0] -= ext0;
   b.hi[0] += ext0;
+  if (w_hi >= w_lo) {
+    b.lo[0] = w_lo;
+    b.hi[0] = w_hi;
+  }
   const unsigned len2 = (unsigned)L.n[2];
   const unsigned half2 = (len2 + 1) / 2;
   const unsigned total = half2;
@@ -2451,10 +2459,10 @@ static void cell_colour_t(cudaStream_t s, const LevelDev& L, double* phi, const 
 }
 
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z, int ext0) {
+                        int parity, double omega, int z, int ext0, int w_lo, int w_hi) {
   ++g_kernel_launches;
-  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
-  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z, ext0);
+  if (dim == 3) cell_colour_t<3>(s, L, phi, rhs, nullptr, parity, omega, z, ext0, w_lo, w_hi);
+  else cell_colour_t<2>(s, L, phi, rhs, nullptr, parity, omega, z, ext0, w_lo, w_hi);
 }
 
 void launch_cell_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,

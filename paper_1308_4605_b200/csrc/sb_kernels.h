@@ -55,10 +55,13 @@ struct CoarseChain {
 // components zero, 2 also the relaxed array zero, 3 as 2 + store the partner's
 // zero (replaces the zero fill; all-periodic pad-free levels only).
 // ext0: also relax ext0 ghost planes on each side of axis 0 (slab levels)
+// w_lo..w_hi (w_hi >= w_lo): only these axis-0 planes (slab levels relax their
+// boundary planes first so the halo exchange overlaps the interior)
 void launch_face_colour(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
-                        const double* rhsA, int parity, double omega, int z = 0, int ext0 = 0);
+                        const double* rhsA, int parity, double omega, int z = 0, int ext0 = 0, int w_lo = 0,
+                        int w_hi = -1);
 void launch_cell_colour(cudaStream_t s, const LevelDev& L, int dim, double* phi, const double* rhs,
-                        int parity, double omega, int z = 0, int ext0 = 0);
+                        int parity, double omega, int z = 0, int ext0 = 0, int w_lo = 0, int w_hi = -1);
 // two-phase variants for levels with an odd periodic extent (same-colour
 // cells couple through the wrap): compute all, then update (reference order)
 void launch_face_colour_tmp(cudaStream_t s, const LevelDev& L, int dim, int form, int A, Ptr3 u,
