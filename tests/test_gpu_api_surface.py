@@ -188,12 +188,12 @@ def test_gmres_kernel_known_answers():
 
 
 def test_reference_test_modules_against_the_package():
-    """The reference's own test_multigrid / test_precond / test_schur /
-    test_operators / test_krylov / test_grid, unmodified, with ``stokesmg``
-    resolving to this package (tools/ref_shim.py; staged under
+    """The reference's own test modules (test_multigrid / precond / schur /
+    operators / krylov / grid / problems / spectrum / acceptance / cli),
+    unmodified, with ``stokesmg`` resolving to this package (tools/ref_shim.py; staged under
     baseline/_ref_tests, git-ignored like the baseline/_ref install)."""
     stage = ROOT / "baseline" / "_ref_tests"
-    if not (stage / "test_multigrid.py").exists():
+    if not (stage / "test_cli.py").exists():
         pytest.skip("reference tests not staged (python tools/ref_shim.py stage)")
     out = subprocess.run([sys.executable, str(ROOT / "tools" / "ref_shim.py"), "run", "-q", "-x"],
                          capture_output=True, text=True, timeout=1800, cwd=str(ROOT))

@@ -10,8 +10,10 @@ read-only there) into ``baseline/_ref_tests/`` -- git-ignored like the
 box but is never part of the repository.
 
 ``run`` makes ``import stokesmg`` resolve to ``paper_1308_4605_b200`` (grid,
-operators, multigrid, schur, precond, krylov, problems and the dense study
-tooling _exact) and runs the staged reference tests under pytest, unmodified.
+operators, multigrid, schur, precond, krylov, problems, spectrum, cli and the
+dense study tooling _exact) and runs the staged reference tests under pytest,
+unmodified: the hot-path modules and test_problems / test_spectrum /
+test_acceptance / test_cli (the CLI tests drive the device driver).
 Nothing is taken from the real reference (``FROM_REFERENCE`` is empty).  Test
 cases that inspect implementation details the drop-in does not share are
 deselected in ``DESELECT`` with the reason.
@@ -30,8 +32,10 @@ STAGE = ROOT / "baseline" / "_ref_tests"
 REF_PKG = ROOT / "baseline" / "_ref" / "stokesmg"
 SRC_TESTS = pathlib.Path("/root/reference/pkg/tests")
 FILES = ["conftest.py", "reference.py", "test_multigrid.py", "test_precond.py", "test_schur.py",
-         "test_operators.py", "test_krylov.py", "test_grid.py"]
-SUBMODULES = ["grid", "operators", "multigrid", "schur", "precond", "krylov", "problems", "_exact"]
+         "test_operators.py", "test_krylov.py", "test_grid.py", "test_problems.py", "test_spectrum.py",
+         "test_acceptance.py", "test_cli.py"]
+SUBMODULES = ["grid", "operators", "multigrid", "schur", "precond", "krylov", "problems", "_exact", "spectrum",
+              "cli"]
 FROM_REFERENCE = {"modules": [], "attrs": {}}  # nothing is taken from the reference
 DESELECT = {
     # spies on np.zeros for the (m+1, n) basis block: the drop-in's basis is
@@ -73,12 +77,37 @@ def install_alias():
                 setattr(sys.modules[f"stokesmg.{sub}"], n, getattr(ref, n))
 
 
+def subprocess_alias():
+    """Child processes the reference tests start (``python -m stokesmg.cli``,
+    test_cli.py:242-247) resolve ``stokesmg`` through a generated alias package
+    on PYTHONPATH -- written by this tool, nothing from the reference."""
+    import os
+    pkg = STAGE / "_alias" / "stokesmg"
+    pkg.mkdir(parents=True, exist_ok=True)
+    subs = [m for m in SUBMODULES if m != "cli"]
+    (pkg / "__init__.py").write_text(
+        "import importlib, sys\n"
+        "from paper_1308_4605_b200 import *  # noqa: F401,F403\n"
+        f"for _s in {subs!r}:\n"
+        "    sys.modules['stokesmg.' + _s] = importlib.import_module('paper_1308_4605_b200.' + _s)\n")
+    (pkg / "cli.py").write_text(
+        "import sys\n"
+        "from paper_1308_4605_b200.cli import *  # noqa: F401,F403\n"
+        "from paper_1308_4605_b200.cli import main\n"
+        "if __name__ == '__main__':\n"
+        "    sys.exit(main())\n")
+    extra = [str(pkg.parent), str(ROOT)]
+    old = os.environ.get("PYTHONPATH")
+    os.environ["PYTHONPATH"] = os.pathsep.join(extra + ([old] if old else []))
+
+
 def run(args):
     import pytest
     if not STAGE.exists():
         print(f"no staged reference tests at {STAGE} (run `stage` in the build container)")
         return 2
     install_alias()
+    subprocess_alias()
     sel = [str(STAGE / f) for f in FILES if f.startswith("test_")]
     desel = ["-k", " and ".join(f"not {name}" for name in DESELECT.values())]
     return pytest.main(["-p", "no:cacheprovider", "--rootdir", str(STAGE), *desel, *sel, *args])
