@@ -350,3 +350,18 @@ def test_dist_exchange_overlap_is_bit_identical(name, n, nslab, nccl_self, monke
     for a in range(3):
         assert np.array_equal(res["1"][0][a], res["0"][0][a])
     assert np.array_equal(res["1"][1], res["0"][1])
+
+
+def test_dist_large_restart_is_rejected():
+    """The slab solver keeps the 127-vector basis cap: a larger
+    restart is refused with the reference's exception type, not truncated."""
+    from paper_1308_4605_b200.dist import DistSolver
+    from paper_1308_4605_b200.krylov import GmresConfig
+    from paper_1308_4605_b200.precond import P1, PrecondConfig
+    case, cs, rs = _case("C5", 32)
+    D = DistSolver(case.grid, cs.viscous_form, nslab=2)
+    D.set_coefficients(cs)
+    with pytest.raises(ValueError):
+        D.gmres_solve(rs, PrecondConfig(kind=P1), GmresConfig(restart=128, max_iters=5, rtol=1e-9))
+    xu, xp, h = D.gmres_solve(rs, PrecondConfig(kind=P1), GmresConfig(restart=127, max_iters=3, rtol=1e-9))
+    assert h.iterations == 3 and h.status == "maxiter"
