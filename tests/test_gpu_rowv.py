@@ -80,7 +80,7 @@ def test_rowv_bit_identical(cells, form, derive, theta, monkeypatch):
             assert np.array_equal(u, v), k
 
 
-@pytest.mark.parametrize("cells", GRIDS + [(8, 8, 256)], ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("cells", GRIDS + [(8, 8, 256), (2, 4, 512)], ids=lambda c: "x".join(map(str, c)))
 @pytest.mark.parametrize("form,theta", [("stress", 0.0), ("laplacian", 0.0), ("stress", 3.5), ("laplacian", 0.25)])
 def test_row_march_matches_per_face(cells, form, theta, monkeypatch):
     a = _run(cells, form, True, theta, True, monkeypatch, rowm="1")
@@ -147,7 +147,7 @@ def test_rowv_gmres_matches_per_face(monkeypatch):
 
 # ---- walls along the contiguous axis (C4's z walls) --------------------------
 
-WALL_GRIDS = [(64, 64, 64), (6, 10, 128), (4, 6, 64)]
+WALL_GRIDS = [(64, 64, 64), (6, 10, 128), (4, 6, 64), (2, 4, 512)]
 
 
 def _wall_case(cells, form, theta, bc2):
