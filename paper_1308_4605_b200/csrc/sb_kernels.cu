@@ -1886,6 +1886,197 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pass A with the basis staged by the TMA (cp.async.bulk, sm_100a).
+//
+// k_dcgs_a_g3 keeps G*CH 16-byte basis loads per thread in registers (120
+// registers, 16 resident warps per SM) and reaches 6.1 TB/s where pass B, at
+// 47 registers, reaches 6.8 TB/s (ncu): pass A is short of bytes in flight.
+// Here thread 0 streams each basis vector's chunk (CH * 256 double2 = 16 KB)
+// into an S-deep shared-memory ring with one bulk copy per stage
+// (cp.async.bulk.shared::cluster.global, completion on an mbarrier); the
+// CTA's threads wait on the stage's mbarrier, read their own elements with
+// conflict-free 16-byte shared loads and, after a __syncthreads, thread 0
+// refills the stage with the chunk S steps ahead -- across chunk boundaries,
+// so the ring never drains.  w and s_j stay in registers as before.  Same
+// element-to-thread mapping, same accumulation order: bit-identical to
+// k_dcgs_a_g3<4, 2>.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+constexpr int kTmaCH = 4;      // double2 per thread per chunk (as k_dcgs_a_g3<4, 2>)
+constexpr int kTmaStages = 4;  // ring depth: 4 x 16 KB per CTA
+
+template <bool MEANS>
+__global__ void __launch_bounds__(kThreads, 2)
+k_dcgs_a_tma(double* __restrict__ Q, long long vstride, int k, const double* __restrict__ c, double inv_gamma,
+             const double* __restrict__ w, long long n2, double* __restrict__ partials,
+             const double* __restrict__ means, long long bb) {
+  pdl_enter();
+  constexpr int CH = kTmaCH, S = kTmaStages, G = 2;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  double2* const ring = reinterpret_cast<double2*>(dsm);  // [S][kThreads * CH]
+  __shared__ unsigned long long full[S];
+  __shared__ double acc[2 * kMaxVec + 2][kThreads / 32];
+  __shared__ double cs[kMaxVec];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nslot = 2 * k + 2;
+  for (int i = threadIdx.x; i < nslot * (kThreads / 32); i += blockDim.x) acc[i / (kThreads / 32)][i % (kThreads / 32)] = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
+  const long long span = (long long)blockDim.x * CH;
+  const long long gstep = (long long)gridDim.x * span;
+  const long long first = blockIdx.x * span;
+  const long long nchunk = first < n2 ? (n2 - first + gstep - 1) / gstep : 0;
+  const long long total = nchunk * k;  // stage loads of this CTA: (chunk, vector) pairs in order
+  // producer (thread 0): stage load number L
+  auto issue = [&](long long L) {
+    const long long ci = L / k;
+    const int i = (int)(L - ci * k);
+    const long long base = first + ci * gstep;
+    const unsigned bytes = (unsigned)((n2 - base < span ? n2 - base : span) * sizeof(double2));
+    const int slot = (int)(L % S);
+    mbar_expect_tx(&full[slot], bytes);
+    bulk_g2s(ring + (long long)slot * span, reinterpret_cast<const double2*>(Q + (long long)i * vstride) + base, bytes,
+             &full[slot]);
+  };
+  long long Lp = 0, Lc = 0;
+  if (threadIdx.x == 0)
+    for (; Lp < S && Lp < total; ++Lp) issue(Lp);
+  for (long long base = first; base < n2; base += gstep) {
+    double2 wv[CH], sv[CH], q[CH];
+    bool ok[CH];
+    long long bnd = 0;
+    double m_lo = 0.0, m_hi = 0.0;
+    int b_lo = 0;
+    const bool chunked = span <= bb;
+    if (MEANS && chunked) {
+      b_lo = (base >= bb) + (base >= 2 * bb) + (base >= 3 * bb);
+      bnd = (long long)(b_lo + 1) * bb;
+      m_lo = __ldg(means + b_lo);
+      m_hi = b_lo < 3 ? __ldg(means + b_lo + 1) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      const long long e = base + t * blockDim.x + threadIdx.x;
+      ok[t] = e < n2;
+      wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      if (MEANS && ok[t]) {
+        const int bf = chunked ? (e < bnd ? b_lo : b_lo + 1) : (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
+        const double m = chunked ? (e < bnd ? m_lo : m_hi) : __ldg(means + bf);
+        wv[t].x = wv[t].x - m;
+        wv[t].y = wv[t].y - m;
+      }
+      sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
+      q[t] = sv[t];
+    }
+    int i = 0;
+    for (; i + G <= k; i += G) {
+      const double2* st[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const long long L = Lc + g;
+        mbar_wait(&full[L % S], (unsigned)((L / S) & 1));
+        st[g] = ring + (L % S) * span + threadIdx.x;
+      }
+      double dv[2 * G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double ci = cs[i + g];
+        double dw = 0.0, dsv = 0.0;
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+          const double2 a = ok[t] ? st[g][t * blockDim.x] : make_double2(0.0, 0.0);
+          q[t].x -= ci * a.x;
+          q[t].y -= ci * a.y;
+          dw += a.x * wv[t].x + a.y * wv[t].y;
+          dsv += a.x * sv[t].x + a.y * sv[t].y;
+        }
+        dv[2 * g] = dw;
+        dv[2 * g + 1] = dsv;
+      }
+      __syncthreads();  // every thread has read its elements: the two stages can be refilled
+      if (threadIdx.x == 0)
+        for (int g = 0; g < G && Lp < total; ++g, ++Lp) issue(Lp);
+      Lc += G;
+      const double r = warp_sum_many<2 * G>(dv, lane);
+      if (lane < 2 * G) {
+        const int g = lane >> 1;
+        acc[(lane & 1) ? k + 1 + i + g : i + g][warp] += r;
+      }
+    }
+    for (; i < k; ++i) {
+      double2 a[CH];
+      mbar_wait(&full[Lc % S], (unsigned)((Lc / S) & 1));
+      const double2* st = ring + (Lc % S) * span;
+#pragma unroll
+      for (int t = 0; t < CH; ++t) a[t] = ok[t] ? st[t * blockDim.x + threadIdx.x] : make_double2(0.0, 0.0);
+      __syncthreads();
+      if (threadIdx.x == 0 && Lp < total) issue(Lp++);
+      ++Lc;
+      const double ci = cs[i];
+      double dv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        q[t].x -= ci * a[t].x;
+        q[t].y -= ci * a[t].y;
+        dv[0] += a[t].x * wv[t].x + a[t].y * wv[t].y;
+        dv[1] += a[t].x * sv[t].x + a[t].y * sv[t].y;
+      }
+      const double r = warp_sum_many<2>(dv, lane);
+      if (lane < 2) acc[lane ? k + 1 + i : i][warp] += r;
+    }
+    double dv[2] = {0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      if (k > 0) {
+        q[t].x *= inv_gamma;
+        q[t].y *= inv_gamma;
+        if (ok[t]) s2[base + t * blockDim.x + threadIdx.x] = q[t];
+      }
+      dv[0] += q[t].x * wv[t].x + q[t].y * wv[t].y;
+      dv[1] += sv[t].x * sv[t].x + sv[t].y * sv[t].y;
+    }
+    const double r = warp_sum_many<2>(dv, lane);
+    if (lane < 2) acc[lane ? 2 * k + 1 : k][warp] += r;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    double s = 0.0;
+    for (int kk = 0; kk < kThreads / 32; ++kk) s += acc[i][kk];
+    partials[i * kRedBlocks + blockIdx.x] = s;
+  }
+}
+
 // Gram variant, pass B: w' = w - sum_i d_i Q_i written to `out`, ||w'||^2 only
 // (one streaming read of the basis).  means (nullable): the null-space
 // projection of w deferred from P^-1 -- w - means[b] on the b-th block of
@@ -2960,6 +3151,36 @@ void launch_dcgs_b(cudaStream_t s, const double* Q, long long vstride, int nv, c
 void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const double* c, double inv_gamma,
                      const double* w, long long n, double* partials, const double* means, long long block) {
   ++g_kernel_launches;
+  // default: the basis staged through shared memory by TMA bulk copies
+  // (k_dcgs_a_tma; bit-identical to k_dcgs_a_g3<4, 2>).  ncu, C5 256^3, the 31
+  // launches of a solve: 47.9 ms vs 49.1 ms, at j = 30 2.55 vs 2.69 ms
+  // (6.95 TB/s); solve 0.3336-0.3355 vs 0.3361-0.3366 s.  SB_DCGS_TMA=0 (or any
+  // SB_DCGS_A variant) selects the register-staged kernels.
+  {
+    const char* et = std::getenv("SB_DCGS_TMA");
+    if (!(et && et[0] == '0') && !std::getenv("SB_DCGS_A") && k > 0) {
+      constexpr size_t ring_bytes = (size_t)kTmaStages * kThreads * kTmaCH * sizeof(double2);
+      static const int grid_t = [] {
+        cudaFuncSetAttribute(k_dcgs_a_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_bytes);
+        cudaFuncSetAttribute(k_dcgs_a_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_bytes);
+        int occ = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dcgs_a_tma<true>, kThreads, ring_bytes) != cudaSuccess ||
+            occ < 1)
+          occ = 2;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = kSMs;
+        return std::max(1, std::min(occ * sms, kRedBlocks));
+      }();
+      g_red_blocks_used = grid_t;
+      if (means)
+        launch_k(k_dcgs_a_tma<true>, grid_t, kThreads, ring_bytes, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials,
+                 means, block / 2);
+      else
+        launch_k(k_dcgs_a_tma<false>, grid_t, kThreads, ring_bytes, s, Q, vstride, k, c, inv_gamma, w, n / 2, partials,
+                 nullptr, 0LL);
+      return;
+    }
+  }
   if (means) {  // deferred null projection: the grouped kernel with the means applied on load
     static const int grid_m = wave_grid(k_dcgs_a_g3<4, 2, 2, true>);
     g_red_blocks_used = grid_m;
