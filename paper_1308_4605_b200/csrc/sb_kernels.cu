@@ -1898,7 +1898,8 @@ k_dcgs_a_g3(double* __restrict__ Q, long long vstride, int k, const double* __re
 // CTA's threads wait on the stage's mbarrier, read their own elements with
 // conflict-free 16-byte shared loads and, after a __syncthreads, thread 0
 // refills the stage with the chunk S steps ahead -- across chunk boundaries,
-// so the ring never drains.  w and s_j stay in registers as before.  Same
+// so the ring never drains.  w and s_j of a chunk come through the ring too
+// (then live in registers while the basis streams past).  Same
 // element-to-thread mapping, same accumulation order: bit-identical to
 // k_dcgs_a_g3<4, 2>.
 // ---------------------------------------------------------------------------
@@ -1951,23 +1952,24 @@ k_dcgs_a_tma(double* __restrict__ Q, long long vstride, int k, const double* __r
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* s2 = reinterpret_cast<double2*>(Q + k * vstride);
   const long long span = (long long)blockDim.x * CH;
   const long long gstep = (long long)gridDim.x * span;
   const long long first = blockIdx.x * span;
   const long long nchunk = first < n2 ? (n2 - first + gstep - 1) / gstep : 0;
-  const long long total = nchunk * k;  // stage loads of this CTA: (chunk, vector) pairs in order
+  // stage loads of this CTA, in order: per chunk w, s_j, Q_0 .. Q_{k-1}
+  const int kk = k + 2;
+  const long long total = nchunk * kk;
   // producer (thread 0): stage load number L
   auto issue = [&](long long L) {
-    const long long ci = L / k;
-    const int i = (int)(L - ci * k);
+    const long long ci = L / kk;
+    const int r = (int)(L - ci * kk);
     const long long base = first + ci * gstep;
     const unsigned bytes = (unsigned)((n2 - base < span ? n2 - base : span) * sizeof(double2));
     const int slot = (int)(L % S);
+    const double* src = r == 0 ? w : (r == 1 ? Q + (long long)k * vstride : Q + (long long)(r - 2) * vstride);
     mbar_expect_tx(&full[slot], bytes);
-    bulk_g2s(ring + (long long)slot * span, reinterpret_cast<const double2*>(Q + (long long)i * vstride) + base, bytes,
-             &full[slot]);
+    bulk_g2s(ring + (long long)slot * span, reinterpret_cast<const double2*>(src) + base, bytes, &full[slot]);
   };
   long long Lp = 0, Lc = 0;
   if (threadIdx.x == 0)
@@ -1985,20 +1987,29 @@ k_dcgs_a_tma(double* __restrict__ Q, long long vstride, int k, const double* __r
       m_lo = __ldg(means + b_lo);
       m_hi = b_lo < 3 ? __ldg(means + b_lo + 1) : 0.0;
     }
+    // w and s_j of the chunk arrive through the ring like the basis
+    mbar_wait(&full[Lc % S], (unsigned)((Lc / S) & 1));
+    mbar_wait(&full[(Lc + 1) % S], (unsigned)(((Lc + 1) / S) & 1));
+    const double2* stw = ring + (Lc % S) * span + threadIdx.x;
+    const double2* sts = ring + ((Lc + 1) % S) * span + threadIdx.x;
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
       const long long e = base + t * blockDim.x + threadIdx.x;
       ok[t] = e < n2;
-      wv[t] = ok[t] ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      wv[t] = ok[t] ? stw[t * blockDim.x] : make_double2(0.0, 0.0);
       if (MEANS && ok[t]) {
         const int bf = chunked ? (e < bnd ? b_lo : b_lo + 1) : (e >= bb) + (e >= 2 * bb) + (e >= 3 * bb);
         const double m = chunked ? (e < bnd ? m_lo : m_hi) : __ldg(means + bf);
         wv[t].x = wv[t].x - m;
         wv[t].y = wv[t].y - m;
       }
-      sv[t] = ok[t] ? s2[e] : make_double2(0.0, 0.0);
+      sv[t] = ok[t] ? sts[t * blockDim.x] : make_double2(0.0, 0.0);
       q[t] = sv[t];
     }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int g = 0; g < 2 && Lp < total; ++g, ++Lp) issue(Lp);
+    Lc += 2;
     int i = 0;
     for (; i + G <= k; i += G) {
       const double2* st[G];
@@ -3153,9 +3164,12 @@ void launch_dcgs_a_g(cudaStream_t s, double* Q, long long vstride, int k, const 
   ++g_kernel_launches;
   // default: the basis staged through shared memory by TMA bulk copies
   // (k_dcgs_a_tma; bit-identical to k_dcgs_a_g3<4, 2>).  ncu, C5 256^3, the 31
-  // launches of a solve: 47.9 ms vs 49.1 ms, at j = 30 2.55 vs 2.69 ms
-  // (6.95 TB/s); solve 0.3336-0.3355 vs 0.3361-0.3366 s.  SB_DCGS_TMA=0 (or any
-  // SB_DCGS_A variant) selects the register-staged kernels.
+  // launches of a solve: 42.95 ms vs 49.08 ms (j = 1: 0.30 vs 0.51 ms, j = 30:
+  // 2.46 vs 2.69 ms = 7.2 TB/s); solve 0.3296-0.3299 vs 0.3356-0.3365 s.
+  // SB_DCGS_TMA=0 (or any SB_DCGS_A variant) selects the register-staged
+  // kernels.  The same ring under pass B gains 1.7 % of that pass (43.6 vs
+  // 44.3 ms: it already runs at 6.8 TB/s) and changes the order of its norm
+  // partial sums; not kept.
   {
     const char* et = std::getenv("SB_DCGS_TMA");
     if (!(et && et[0] == '0') && !std::getenv("SB_DCGS_A") && k > 0) {
