@@ -12,8 +12,8 @@
 //    32-face segments, -1 neighbours carried between segments, every edge /
 //    normal stress evaluated once and shared by the two rows that use it,
 //    FMAs on the final combinations; all-periodic levels and levels with walls
-//    along the contiguous axis (C4).  ncu C5 256^3: apply_M 322 us, residual
-//    field 319 us (0.77 / 0.85 of the measured HBM peak).  Equal to the
+//    along the contiguous axis (C4).  ncu C5 256^3: apply_M 301 us, residual
+//    field 289 us (0.83 / 0.93 of the measured HBM peak).  Equal to the
 //    per-face kernels to ~1e-15 relative (different rounding order).
 //  * k_face_all_rv / k_face_colour_rv ("segment" kernels, SB_ROWM=0 /
 //    SB_ROWV_COLOUR=1): a warp owns a 32- or 64-face row segment and every
@@ -541,6 +541,12 @@ k_face_all_rv(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
 // Same formulas as face_row_t with a different rounding order (and FMAs):
 // equal to the per-face kernels to ~1e-15 relative, not bit-identical
 // (tests/test_gpu_rowv.py).  Derived edge viscosities only (mue_derived levels).
+// L2 prefetch distance of the row walk in segments (ncu, C5 256^3, apply_M /
+// residual field: 0: 321 / 318 us, 1: 301 / 289, 2: 290 / 301, 4: 303 / 327)
+#ifndef RM_PF
+#define RM_PF 1
+#endif
+__device__ __forceinline__ void pf_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ double rot_m(double v, double& prev, int lane) {
   const double s = lane == 31 ? prev : v;
   prev = v;
@@ -616,6 +622,24 @@ k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
 #pragma unroll 1
   for (int s = 0; s < nseg; ++s) {
     const int q = rowc + (s << 5) + lane;
+#if RM_PF > 0
+    // the rows this plane touches first (plane i + 1 of u and mu, the own row of
+    // p / rhs) come from DRAM: ask L2 for them RM_PF segments ahead
+    if (s + RM_PF < nseg) {
+      const int qp = q + 32 * RM_PF;
+      pf_l2(u0 + qp + ip);
+      pf_l2(u1 + qp + ip);
+      pf_l2(u2 + qp + ip);
+      pf_l2(mu + qp + ip);
+      if (MODE_M) {
+        pf_l2(p + qp);
+      } else {
+        pf_l2(rhs.p[0] + qp);
+        pf_l2(rhs.p[1] + qp);
+        pf_l2(rhs.p[2] + qp);
+      }
+    }
+#endif
     const double u0c = __ldg(u0 + q), u0im = __ldg(u0 + q + im), u0ip = __ldg(u0 + q + ip);
     const double u0jm = __ldg(u0 + q + jm), u0jp = __ldg(u0 + q + jp), u0ipjm = __ldg(u0 + q + ip + jm);
     const double u1c = __ldg(u1 + q), u1im = __ldg(u1 + q + im), u1ip = __ldg(u1 + q + ip);
