@@ -116,6 +116,12 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 // other-colour partner face (k ^ 1), which replaces the level's zero fill on
 // all-periodic pad-free levels (every block entry is then written).  Same
 // arithmetic on the same values as the plain pass: bit-identical.
+// L2 prefetch distance of the colour passes in planes (ncu, C5 256^3, finest face
+// pass of components 0 / 1 / 2: off 157 / 158 / 161 us, 1: 142 / 138 / 144,
+// 2: 140 / 137 / 143, 4: 141 / 136 / 144)
+#ifndef FC_PF
+#define FC_PF 2
+#endif
 template <int A>
 __host__ __device__ constexpr int later_mask() { return A == 0 ? 6 : (A == 1 ? 4 : 0); }
 
@@ -154,6 +160,21 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
       return;
     }
     constexpr int ZM = Z == 1 ? later_mask<A>() : 0;
+#if FC_PF > 0
+    // planes are scheduled in ascending order (blockIdx.z): ask L2 for this
+    // thread's column FC_PF planes ahead, where later CTAs read it first.  Only
+    // the derived-mu_e row, which is latency / L1 bound (C5: 157-161 -> 137-143 us
+    // per finest pass); the stored-mu_e row already saturates HBM and the
+    // extra requests cost it 3 % (C4: 198 / 198 / 181 -> 197 / 204 / 187 us)
+    if (DIM == 3 && DE && Z <= 1 && ci[0] + FC_PF <= b.hi[0]) {
+      const int fp = f + FC_PF * L.s0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(uc[0] + fp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(uc[1] + fp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(uc[2] + fp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(L.mu_c + fp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rhs + fp));
+    }
+#endif
     const double au =
         face_row_core<DIM, FORM, A, PA, true, DE, ZM>(L, gather_ua<DIM, A, PA>(L, uc[A], f, ci), uc, f, ci, dg);
     const double res = __ldg(rhs + f) - au;
@@ -194,6 +215,20 @@ k_cell_colour(LevelDev L, double* phi, const double* __restrict__ rhs, double* t
       if (Z == 3) phi[(k & 1) ? c - 1 : c + 1] = 0.0;
       return;
     }
+#if FC_PF > 0
+    // as k_face_colour: this column, FC_PF planes ahead (C4, streamed 1/rho:
+    // 136 -> 121 us per finest pass; C5, constant 1/rho: 64 -> 63 us)
+    if (DIM == 3 && ci[0] + FC_PF <= b.hi[0]) {
+      const int cp = c + FC_PF * L.s0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(phi + cp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rhs + cp));
+      if (!L.beta_const) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(L.beta_f[0] + cp));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(L.beta_f[1] + cp));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(L.beta_f[2] + cp));
+      }
+    }
+#endif
     const double lp = cell_row<DIM, PA>(L, phi, c, ci, dg);
     const double res = __ldg(rhs + c) - lp;
     const double nv = phi[c] + omega * res / dg;
