@@ -1429,15 +1429,20 @@ void build_from_level0(sb_ctx* c) {
     for (size_t l = 0; l < c->lv.size(); ++l) launch_check_diag(c->st, c->lv[l].d, c->dim, c->form, c->dflags);
     // levels whose edge viscosities are the four-cell mean of mu_c: the face
     // rows derive them instead of streaming mu_e.  SB_MUE_DERIVED: 1 (default)
-    // all-periodic levels, 2 also wall-bounded levels (two-cell boundary
-    // means; bit-compatible but measured no faster on C4: 200 -> 204 us per
-    // finest colour pass, the walled row turns L1/issue-bound), 0 never
+    // all-periodic levels and 3D levels with walls along the contiguous axis
+    // only, 2 every wall-bounded level too (two-cell boundary means;
+    // bit-compatible), 0 never
     const int derive_mode = [] {  // read per upload: tests compare the paths in one process
       const char* e = std::getenv("SB_MUE_DERIVED");
       return e ? std::atoi(e) : 1;
     }();
-    const bool per_all = c->bc[0][0] == BC_PER && c->bc[1][0] == BC_PER && c->bc[2][0] == BC_PER;
-    const bool derive_on = derive_mode == 2 || (derive_mode == 1 && per_all);
+    // default: all-periodic levels and 3D levels whose only walls are along
+    // the contiguous axis (C4) -- with the L2 prefetch of the derived-edge row
+    // the walled row now beats the stored one (C4 256^3: 182 / 196 / 178 vs
+    // 195 / 198 / 180 us per finest pass, solve 2.18 vs 2.22 s)
+    const bool per_01 = c->bc[0][0] == BC_PER && c->bc[1][0] == BC_PER;
+    const bool per_all = per_01 && c->bc[2][0] == BC_PER;
+    const bool derive_on = derive_mode == 2 || (derive_mode == 1 && (per_all || (c->dim == 3 && per_01)));
     if (derive_on)
       for (int l = 0; l < nl; ++l) launch_check_mue(c->st, c->lv[l].d, c->dim, c->dflags + 16 + l);
     int hm[kFlagInts - 16];

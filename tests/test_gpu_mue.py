@@ -74,17 +74,26 @@ def test_walls_and_foreign_edges_keep_stored_path(monkeypatch):
     from dataclasses import replace
     from paper_1308_4605_b200 import operators as OPS
     from paper_1308_4605_b200.grid import NodeEdgeField
-    # a wall-bounded finest level derives when asked (SB_MUE_DERIVED=2, two-cell
-    # boundary means); its coarse levels inject mu_e and keep the stored path.
-    # By default (1) only all-periodic levels derive.
+    # a wall-bounded finest level derives (two-cell boundary means); its coarse
+    # levels inject mu_e and keep the stored path.  By default (1) all-periodic
+    # levels and 3D levels with walls along the contiguous axis only (C4)
+    # derive; walls along another axis keep the stored path unless asked
+    # (SB_MUE_DERIVED=2).
     _, _, _, P = _setup("C4", 16, True, monkeypatch)
     assert P.ctx.mue_derived(0) and not P.ctx.mue_derived(1)
     del P
     from paper_1308_4605_b200 import problems as PR
+    from paper_1308_4605_b200.grid import NO_SLIP, PERIODIC, CellField, GridSpec
+    from paper_1308_4605_b200.operators import make_coefficients
     from paper_1308_4605_b200.precond import P1, PrecondConfig, Preconditioner
     case = PR.make_case("C4", 16)
     cs4, _, _ = PR.prepare(case)
-    assert not Preconditioner(cs4, PrecondConfig(kind=P1)).ctx.mue_derived(0)
+    monkeypatch.delenv("SB_MUE_DERIVED", raising=False)
+    assert Preconditioner(cs4, PrecondConfig(kind=P1)).ctx.mue_derived(0)
+    gy = GridSpec((16, 16, 16), 1.0 / 16, ((PERIODIC, PERIODIC), (NO_SLIP, NO_SLIP), (PERIODIC, PERIODIC)))
+    rng = np.random.default_rng(2)
+    csy = make_coefficients(gy, 0.5, CellField(gy, 1.0 + rng.random(gy.cells)), CellField(gy, 1.0 + rng.random(gy.cells)))
+    assert not Preconditioner(csy, PrecondConfig(kind=P1)).ctx.mue_derived(0)
 
     # harmonic edge means: not the arithmetic cell mean -> stored path, and the
     # operator is the one of the given mu_edge (oracle)
