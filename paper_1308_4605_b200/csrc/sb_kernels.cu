@@ -122,6 +122,10 @@ template <> struct Others<2, 2> { static constexpr int B1 = 1, B2 = -1; };
 #ifndef FC_PF
 #define FC_PF 2
 #endif
+// this thread's column FC_PF planes ahead of plane i0 (see k_face_colour)
+__device__ __forceinline__ void pf_plane(const double* p, int idx) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + idx));
+}
 template <int A>
 __host__ __device__ constexpr int later_mask() { return A == 0 ? 6 : (A == 1 ? 4 : 0); }
 
@@ -549,6 +553,24 @@ k_face_pa8(LevelDev Lf, LevelDev Lc, const double* __restrict__ coarse, double* 
     }
   }
   const bool wallA = Lf.bclo[A] != BC_PER;
+#if FC_PF > 0
+  if (DIM == 3 && C[0] + 1 <= cb.hi[0]) {  // the 8 fine faces of the next coarse plane (2 fine planes ahead)
+#pragma unroll
+    for (int pa = 0; pa < 2; ++pa)
+#pragma unroll
+      for (int p1 = 0; p1 < 2; ++p1) {
+        int F[3] = {0, 0, 0};
+        F[A] = 2 * I + pa;
+        F[O::B1] = 2 * C[O::B1] + p1;
+        F[O::B2] = 2 * C[O::B2];
+        pf_plane(fine, lin(Lf, F) + 2 * Lf.s0);  // both p2 faces share the 16 bytes when B2 is contiguous
+        if (O::B2 != 2) {
+          F[O::B2] += 1;
+          pf_plane(fine, lin(Lf, F) + 2 * Lf.s0);
+        }
+      }
+  }
+#endif
 #pragma unroll
   for (int pa = 0; pa < 2; ++pa) {
     if (wallA && pa == 0 && I == 0) continue;  // fine wall face, not an unknown
@@ -747,6 +769,18 @@ k_cell_res(LevelDev L, const double* x, const double* __restrict__ rhs, double* 
   pdl_enter();
   int ci[3];
   if (!box_point(b, ci)) return;
+#if FC_PF > 0
+  if (DIM == 3 && ci[0] + FC_PF <= b.hi[0]) {
+    const int cp = lin(L, ci) + FC_PF * L.s0;
+    pf_plane(x, cp);
+    pf_plane(rhs, cp);
+    if (!L.beta_const) {
+      pf_plane(L.beta_f[0], cp);
+      pf_plane(L.beta_f[1], cp);
+      pf_plane(L.beta_f[2], cp);
+    }
+  }
+#endif
   out[lin(L, ci)] = cell_resid_at<DIM, PA>(L, x, rhs, ci);
 }
 
@@ -808,6 +842,15 @@ k_div_add(LevelDev L, CPtr3 u, const double* __restrict__ rp, double* __restrict
     int ci[3];
     if (!box_point(b, ci)) return;
     const int c = lin(L, ci);
+#if FC_PF > 0
+    if (DIM == 3 && ci[0] + FC_PF <= b.hi[0]) {
+      const int cp = c + FC_PF * L.s0;
+      pf_plane(u.p[0], cp);
+      pf_plane(u.p[1], cp);
+      pf_plane(u.p[2], cp);
+      pf_plane(rp, cp);
+    }
+#endif
     out[c] = div_sum<DIM>(L, u.p, c, ci) * L.inv_h + __ldg(rp + c);
   }
 }
@@ -835,6 +878,17 @@ k_p1_glue(LevelDev L, int form, Ptr3 xu, const double* __restrict__ phi, const d
   {
     int ci[3];
     if (!box_point(b, ci)) return;
+#if FC_PF > 0
+    if (DIM == 3 && ci[0] + FC_PF <= b.hi[0]) {
+      const int cp = lin(L, ci) + FC_PF * L.s0;
+      pf_plane(xu.p[0], cp);
+      pf_plane(xu.p[1], cp);
+      pf_plane(xu.p[2], cp);
+      pf_plane(phi, cp);
+      pf_plane(bc, cp);
+      pf_plane(L.mu_c, cp);
+    }
+#endif
     if (DIM == 3) glue_face<0>(L, xu.p[0], phi, ci);
     glue_face<1>(L, xu.p[1], phi, ci);
     glue_face<2>(L, xu.p[2], phi, ci);
