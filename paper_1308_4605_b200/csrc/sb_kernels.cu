@@ -153,6 +153,17 @@ k_face_colour(LevelDev L, Ptr3 u, const double* __restrict__ rhs, double* tmp, i
     double dg;
     if (Z >= 2) {
       constexpr int ZM = later_mask<A>() | (1 << A);
+#if FC_PF > 0
+      // zero-first pass: only the arrays it reads (mu_c, rhs, the components
+      // relaxed before A) are worth asking for
+      if (DIM == 3 && DE && ci[0] + FC_PF <= b.hi[0]) {
+        const int fp = f + FC_PF * L.s0;
+        pf_plane(L.mu_c, fp);
+        pf_plane(rhs, fp);
+        if (A > 0) pf_plane(uc[0], fp);
+        if (A > 1) pf_plane(uc[1], fp);
+      }
+#endif
       UA7 s0;
       s0.c = 0.0;
 #pragma unroll
