@@ -538,6 +538,11 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "bytes_per_launch": fine_launch_bytes, "ms_per_launch": fine_launch_ms,
+                         # the kernel derives the edge viscosities from mu_c where it can, so
+                         # it moves fewer bytes than the SURVEY §8d model credits (frac may
+                         # exceed 1): the ncu DRAM traffic over the same live launch time
+                         "traffic_frac": (traffic / (fine_launch_ms * 1e-3) / 1e9 / peak)
+                         if (traffic and fine_launch_ms > 0) else None,
                          "peak_source": peak_src},
             "smoother": smoother_report(st, peak),
             "e2e": e2e, "gpu_launches": int(launches), "clocks": ck, "cpu_baseline": cpu,
