@@ -12,8 +12,8 @@
 //    32-face segments, -1 neighbours carried between segments, every edge /
 //    normal stress evaluated once and shared by the two rows that use it,
 //    FMAs on the final combinations; all-periodic levels and levels with walls
-//    along the contiguous axis (C4).  ncu C5 256^3: apply_M 301 us, residual
-//    field 289 us (0.83 / 0.93 of the measured HBM peak).  Equal to the
+//    along the contiguous axis (C4).  ncu C5 256^3: apply_M 273 us, residual
+//    field 263 us (0.91 / 1.03 of the measured HBM peak by the byte model).  Equal to the
 //    per-face kernels to ~1e-15 relative (different rounding order).
 //  * k_face_all_rv / k_face_colour_rv ("segment" kernels, SB_ROWM=0 /
 //    SB_ROWV_COLOUR=1): a warp owns a 32- or 64-face row segment and every
@@ -541,10 +541,13 @@ k_face_all_rv(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
 // Same formulas as face_row_t with a different rounding order (and FMAs):
 // equal to the per-face kernels to ~1e-15 relative, not bit-identical
 // (tests/test_gpu_rowv.py).  Derived edge viscosities only (mue_derived levels).
-// L2 prefetch distance of the row walk in segments (ncu, C5 256^3, apply_M /
-// residual field: 0: 321 / 318 us, 1: 301 / 289, 2: 290 / 301, 4: 303 / 327)
+// L2 prefetch of the row walk (ncu, C5 256^3, apply_M / residual field; off:
+// 321 / 318 us).  RM_PF > 0: the first-touched rows RM_PF segments ahead along
+// the row (1: 301 / 289, 2: 290 / 301, 4: 303 / 327); RM_PF < 0: this warp's own
+// row -RM_PF planes beyond the last plane it reads, for the CTAs of the later
+// planes (-1: 281 / 269, -2: 273 / 263 (default), -3 and -4: the same)
 #ifndef RM_PF
-#define RM_PF 1
+#define RM_PF -2
 #endif
 __device__ __forceinline__ void pf_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ double rot_m(double v, double& prev, int lane) {
@@ -637,6 +640,25 @@ k_face_all_rm(LevelDev L, CPtr3 x, CPtr3 rhs, const double* __restrict__ p, Ptr3
         pf_l2(rhs.p[0] + qp);
         pf_l2(rhs.p[1] + qp);
         pf_l2(rhs.p[2] + qp);
+      }
+    }
+#elif RM_PF < 0
+    // plane-ahead variant: this warp's row, -RM_PF planes after plane i + 1
+    {
+      const int pl = i + 1 - RM_PF;
+      if (pl < L.n[0] + (L.dist0 ? 1 : 0)) {
+        const int qp = q + (pl - i) * L.s0;
+        pf_l2(u0 + qp);
+        pf_l2(u1 + qp);
+        pf_l2(u2 + qp);
+        pf_l2(mu + qp);
+        if (MODE_M) {
+          pf_l2(p + qp - L.s0);
+        } else {
+          pf_l2(rhs.p[0] + qp - L.s0);
+          pf_l2(rhs.p[1] + qp - L.s0);
+          pf_l2(rhs.p[2] + qp - L.s0);
+        }
       }
     }
 #endif
